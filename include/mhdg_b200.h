@@ -1,0 +1,166 @@
+/*
+ * mhdg_b200.h -- C ABI of the B200 macro-element HDG operator library
+ * (libmhdg_b200.so).
+ *
+ * The reference (macrohdg, pure Python) has no FFI; its drop-in surface is
+ * the duck-typed Discretization / LinearizedSystem object API.  Each entry
+ * point below replaces one method of that API (cited per function); the
+ * Python shim `paper_2507_22195_b200.assembly` binds them with ctypes and
+ * keeps the reference's method names, argument meaning and exceptions.
+ *
+ * Conventions
+ *  - All array pointers are caller-owned DEVICE buffers of float64 in the
+ *    reference layouts: w (E, nc, 5), trace (F, nt, 5), offset
+ *    (E, n_sub, nq, 5).  Lin buffers are caller-allocated with the sizes
+ *    reported by mhdg_lin_sizes().
+ *  - `stream` is a cudaStream_t (may be NULL = legacy default stream).
+ *    Calls are stream-ordered; calls that return a status synchronize the
+ *    stream before returning, the others do not.
+ *  - Return codes map 1:1 onto the reference's exception classes
+ *    (macrohdg/errors.py); details come back in mhdg_status.
+ */
+#ifndef MHDG_B200_H
+#define MHDG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum mhdg_code {
+  MHDG_OK = 0,
+  MHDG_NON_ADMISSIBLE = 1,          /* NonAdmissibleState            */
+  MHDG_NON_ADMISSIBLE_ENTROPY = 2,  /* NonAdmissibleEntropyState     */
+  MHDG_SINGULAR_LOCAL = 3,          /* SingularLocalMatrix(macro)    */
+  MHDG_SINGULAR_BLOCK = 4,          /* SingularBlock(face)           */
+  MHDG_INVALID_CONFIG = 5,          /* InvalidConfig                 */
+  MHDG_CUDA_ERROR = 6,
+  MHDG_OUT_OF_MEMORY = 7
+};
+
+/* where_kind: 0 = "volume sub <index>", 1 = "face tile <index>",
+ *             2 = "trace tile <index>" (assembly.py:428-438, :471-531) */
+typedef struct {
+  int code;
+  int where_kind;
+  int where_index;
+  int64_t item; /* first offending macro (residual / local factor) or face */
+  int n_unsym;  /* face blocks not symmetric (debug log, assembly.py:1025) */
+} mhdg_status;
+
+/* Host-side tables of one Discretization (paper_2507_22195_b200/tables.py),
+ * uploaded once by mhdg_create.  Integer maps are int64 as in the reference. */
+typedef struct {
+  int dim, p, m;
+  int n_macros, n_faces;
+  int nn, nq, nfn, nqf, n_st, n_sub;
+  int formulation; /* 0 conservative, 1 entropy        */
+  int flux_kind;   /* 0 lf, 1 ec, 2 es, 3 kepes        */
+  double gamma;
+  const double* phi;          /* (nq, nn)        */
+  const double* dphi;         /* (nq, nn, 3)     */
+  const double* quad_wts;     /* (nq)            */
+  const double* phi_face;     /* (n_st, nqf, nfn)*/
+  const double* fphi;         /* (nqf, nfn)      */
+  const double* facet_wts;    /* (nqf)           */
+  const int64_t* face_rows;   /* (n_st, nfn)     */
+  const double* sub_det;      /* (E)             */
+  const double* sub_inv_jac;  /* (E, 3, 3)       */
+  const double* face_normals; /* (E, n_st, 3)    */
+  const double* face_area;    /* (E, n_st) area*(d-1)! */
+  const int64_t* face_id_st;  /* (E, n_st)       */
+  const int64_t* trace_idx;   /* (E, n_st, nfn)  */
+  const uint8_t* boundary_st; /* (E, n_st)       */
+  const int64_t* face_sides;  /* (F, 2) macro*n_st+tile, -1 if none */
+  const double* freestream;   /* (5) conservative far-field state or NULL */
+} mhdg_tables;
+
+typedef struct mhdg_ctx mhdg_ctx;
+
+/* Caller-allocated storage of one linearization (LinearizedSystem). */
+typedef struct {
+  double* sinv; /* (E, 5nc, 5nc) S^-1 per macro, column-major          */
+  double* hw;   /* (E, n_st, nqf, 5, 5) dF^/dw at face quadrature      */
+  double* hhat; /* (E, n_st, nqf, 5, 5) dF^/dw^                        */
+  double* hh;   /* (E, n_st, nqf, 5, 5) hhat + ghost + trace ptc       */
+  double* pinv; /* (F, 5nt, 5nt) face-block inverse, column-major      */
+} mhdg_lin_buffers;
+
+/* Discretization.__init__ (assembly.py:120-153): upload tables. */
+mhdg_ctx* mhdg_create(const mhdg_tables* tables, int device, int* err);
+void mhdg_destroy(mhdg_ctx* ctx);
+/* element counts of the five mhdg_lin_buffers arrays */
+void mhdg_lin_sizes(const mhdg_ctx* ctx, int64_t sizes[5]);
+
+/* Discretization.residuals (assembly.py:459-549).  offset may be NULL;
+ * has_stage = 0 means stage None.  check = 0 skips the rho/P checks
+ * (residuals(check=False)).  sync = 0 leaves the status on the device
+ * (retrieve with mhdg_status_fetch). */
+int mhdg_residual(mhdg_ctx* ctx, const double* w, const double* trace,
+                  int has_stage, double alpha, const double* offset, int check,
+                  double* r_w, double* r_trace, int sync, mhdg_status* st,
+                  void* stream);
+int mhdg_status_fetch(mhdg_ctx* ctx, mhdg_status* st, void* stream);
+
+/* Discretization.jacobian / LinearizedSystem.__init__ (assembly.py:697-1026):
+ * linearization tensors, S assembly, per-macro S^-1, face-block inverses. */
+int mhdg_linearize(mhdg_ctx* ctx, const double* w, const double* trace,
+                   double alpha, double ptc_weight, const mhdg_lin_buffers* lin,
+                   mhdg_status* st, void* stream);
+
+/* LinearizedSystem.matvec (assembly.py:1131-1143): y = A^ x */
+int mhdg_matvec(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* x,
+                double* y, void* stream);
+/* LinearizedSystem.condensed_rhs (assembly.py:1145-1157) */
+int mhdg_condensed_rhs(mhdg_ctx* ctx, const mhdg_lin_buffers* lin,
+                       const double* r_w, const double* r_trace, double* b,
+                       void* stream);
+/* LinearizedSystem.recover (assembly.py:1159-1173): d_w */
+int mhdg_recover(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* r_w,
+                 const double* d_trace, double* d_w, void* stream);
+/* LinearizedSystem.apply_preconditioner (assembly.py:1175-1180) */
+int mhdg_precond(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* r,
+                 double* z, void* stream);
+
+/* Discretization.volume_quad_states (assembly.py:417-426): (E,1,nq,5) */
+int mhdg_volume_quad_states(mhdg_ctx* ctx, const double* w, double* out,
+                            mhdg_status* st, void* stream);
+/* to_conservative / from_conservative on n nodal states (n, 5) */
+int mhdg_to_conservative(mhdg_ctx* ctx, int64_t n, const double* w, double* u,
+                         mhdg_status* st, void* stream);
+int mhdg_from_conservative(mhdg_ctx* ctx, int64_t n, const double* u, double* w,
+                           void* stream);
+/* Discretization.integrals (assembly.py:595-620): out_host[5] =
+ * entropy, thermo_entropy, kinetic_energy, mass, total_energy */
+int mhdg_integrals(mhdg_ctx* ctx, const double* w, double* out_host,
+                   void* stream);
+
+/* FGMRES vector kernels (solver.py:42-118), deterministic reductions.
+ * mhdg_dot: out_dev[0] = x . y
+ * mhdg_mgs: modified Gram-Schmidt of w against rows 0..j of V (row stride n):
+ *   for i<=j: h[i] = V_i . w; w -= h[i] V_i;  h[j+1] = ||w||;
+ *   V_{j+1} = w / h[j+1] if h[j+1] > 1e-300.  h_dev has j+2 slots.
+ * mhdg_combine: x += sum_i y_dev[i] Z_i, i < k
+ * mhdg_scale: y = x * (a_dev ? a_dev[0] : a) ; mhdg_axpby: z = a x + b y */
+int mhdg_dot(mhdg_ctx* ctx, int64_t n, const double* x, const double* y,
+             double* out_dev, void* stream);
+int mhdg_mgs(mhdg_ctx* ctx, int64_t n, int j, double* V, double* w,
+             double* h_dev, void* stream);
+int mhdg_combine(mhdg_ctx* ctx, int64_t n, int k, const double* Z,
+                 const double* y_dev, double* x, void* stream);
+int mhdg_scale(mhdg_ctx* ctx, int64_t n, const double* x, double a,
+               const double* a_dev, int invert, double* y, void* stream);
+int mhdg_axpby(mhdg_ctx* ctx, int64_t n, double a, const double* x, double b,
+               const double* y, double* z, void* stream);
+
+/* number of library kernels launched since creation (evidence counter) */
+int64_t mhdg_launch_count(const mhdg_ctx* ctx);
+/* FP64 FMA throughput probe (roofline denominator), returns GFLOP/s */
+double mhdg_fp64_probe(int device, void* stream);
+const char* mhdg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

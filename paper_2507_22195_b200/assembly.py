@@ -1,0 +1,407 @@
+"""Device-resident Discretization / LinearizedSystem: the drop-in surface.
+
+Mirrors the reference's object API (macrohdg assembly.py): same class and
+method names, argument meaning, return containers and exceptions, so the
+Newton/DIRK/Krylov callers (`time_march`, `solver`) and user code written
+against the reference work unchanged.  Every operator runs in
+libmhdg_b200.so on the GPU; arrays are torch CUDA tensors (numpy inputs are
+uploaded).  There is no CPU fallback.
+
+  Discretization.residuals        -> mhdg_residual        (assembly.py:459-549)
+  Discretization.jacobian         -> mhdg_linearize       (assembly.py:697-976)
+  LinearizedSystem.matvec         -> mhdg_matvec          (assembly.py:1131-1143)
+  LinearizedSystem.condensed_rhs  -> mhdg_condensed_rhs   (assembly.py:1145-1157)
+  LinearizedSystem.recover        -> mhdg_recover         (assembly.py:1159-1173)
+  LinearizedSystem.apply_preconditioner -> mhdg_precond   (assembly.py:1175-1180)
+  Discretization.volume_quad_states / integrals / to_/from_conservative
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import InvalidConfig
+from .fluxes import DissipationSpec
+from .gas import GasModel
+from .tables import HDGTables
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def as_device(a, device):
+    """float64 contiguous CUDA tensor view/copy of a numpy array or tensor."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        t = a
+        if t.device != device or t.dtype != torch.float64:
+            t = t.to(device=device, dtype=torch.float64)
+        return t.contiguous()
+    return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=device)
+
+
+@dataclass
+class FieldSet:
+    """Nodal coefficients: w (E, nc, n_s), trace (F, nt, n_s), q if viscous."""
+
+    w: object
+    trace: object
+    q: object = None
+
+    def copy(self):
+        return FieldSet(self.w.clone() if hasattr(self.w, "clone") else self.w.copy(),
+                        self.trace.clone() if hasattr(self.trace, "clone") else self.trace.copy(),
+                        None if self.q is None else self.q.clone())
+
+
+@dataclass
+class ResidualSet:
+    r_w: object
+    r_trace: object
+    r_q: object = None
+    _disc: object = None
+
+    def norm(self):
+        parts = [self.r_w, self.r_trace] + ([self.r_q] if self.r_q is not None else [])
+        if self._disc is not None:
+            return math.sqrt(sum(self._disc.vdot(p, p) for p in parts))
+        return math.sqrt(sum(float((p * p).sum()) for p in parts))
+
+    def max_abs(self):
+        parts = [self.r_w, self.r_trace] + ([self.r_q] if self.r_q is not None else [])
+        return max(float(p.abs().max()) for p in parts)
+
+
+@dataclass(frozen=True)
+class StageContext:
+    """Temporal term alpha * u(w) + offset at volume quadrature points."""
+
+    alpha: float
+    offset: object = None
+    dt: float | None = None
+
+
+@dataclass(frozen=True)
+class FreeStream:
+    state: np.ndarray
+
+
+def boundary_trace_operator(kind, state=None):
+    if kind == "periodic":
+        return None
+    if kind == "freestream":
+        if state is None:
+            raise InvalidConfig("freestream boundary needs a state")
+        return FreeStream(np.asarray(state, dtype=float))
+    raise InvalidConfig(f"unsupported boundary kind {kind!r}")
+
+
+class Discretization:
+    """Spatial operator on a macro mesh at degree p, evaluated on the GPU.
+
+    Supported on the device: d = 3, m = 1, p = 1..4, default quadrature,
+    entropy or conservative formulation, lf/ec/es/kepes fluxes, periodic or
+    free-stream boundaries, inviscid.  Anything else raises InvalidConfig
+    (the reference-only features are listed in DESIGN.md).
+    """
+
+    def __init__(self, mesh, p, gas=None, formulation="entropy", flux=None,
+                 viscosity=None, quad_degree=None, boundary=None, supg=False,
+                 device=None):
+        if formulation not in ("conservative", "entropy"):
+            raise InvalidConfig(f"unknown formulation {formulation!r}")
+        if supg:
+            raise InvalidConfig("SUPG streamline term is not on the B200 path")
+        if viscosity is not None:
+            raise InvalidConfig("viscous operator (level-1 q condensation) is not on the "
+                                "B200 path yet")
+        if mesh.has_boundary and boundary is None:
+            raise InvalidConfig("mesh has boundary faces, a boundary treatment is required")
+        if mesh.dim != 3 or mesh.m != 1:
+            raise InvalidConfig("the B200 operator is 3D with m = 1 macro subdivision")
+        if quad_degree not in (None, 2 * p + 1):
+            raise InvalidConfig("the B200 operator uses the default quadrature degree 2p+1")
+        if not 1 <= p <= 4:
+            raise InvalidConfig("the B200 operator supports p = 1..4")
+        torch = _torch()
+        lib = N.require_cuda()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.mesh = mesh
+        self.p = p
+        self.gas = gas or GasModel()
+        self.formulation = formulation
+        self.flux = flux or DissipationSpec("kepes")
+        self.viscosity = None
+        self.supg = False
+        self.boundary = boundary
+        self.d = mesh.dim
+        self.n_s = self.d + 2
+        self.tables = t = HDGTables(mesh, p, quad_degree)
+        self.basis, self.layout = t.basis, t.layout
+        self.n_st, self.n_faces = t.n_st, t.n_faces
+        self.phi = t.phi
+        self.domain_volume = t.domain_volume
+        self._lib = lib
+        self._keep = []
+        tab = N.Tables()
+        tab.dim, tab.p, tab.m = 3, p, mesh.m
+        tab.n_macros, tab.n_faces = mesh.n_macros, t.n_faces
+        tab.nn, tab.nq = t.phi.shape[1], t.phi.shape[0]
+        tab.nfn, tab.nqf = t.fphi.shape[1], t.fphi.shape[0]
+        tab.n_st, tab.n_sub = t.n_st, t.layout.n_sub
+        tab.formulation = 1 if formulation == "entropy" else 0
+        tab.flux_kind = self.flux.code
+        tab.gamma = float(self.gas.gamma)
+
+        def keep(a, dtype):
+            a = np.ascontiguousarray(a, dtype=dtype)
+            self._keep.append(a)
+            return N.np_ptr(a)
+
+        tab.phi = keep(t.phi, np.float64)
+        tab.dphi = keep(t.dphi, np.float64)
+        tab.quad_wts = keep(t.quad_wts, np.float64)
+        tab.phi_face = keep(t.phi_face, np.float64)
+        tab.fphi = keep(t.fphi, np.float64)
+        tab.facet_wts = keep(t.facet_wts, np.float64)
+        tab.face_rows = keep(t.face_rows, np.int64)
+        tab.sub_det = keep(t.sub_det[:, 0], np.float64)
+        tab.sub_inv_jac = keep(t.sub_inv_jac[:, 0], np.float64)
+        tab.face_normals = keep(t.face_normals, np.float64)
+        tab.face_area = keep(t.face_area, np.float64)
+        tab.face_id_st = keep(t.face_id_st, np.int64)
+        tab.trace_idx = keep(t.trace_idx, np.int64)
+        tab.boundary_st = keep(t.boundary_st, np.uint8)
+        tab.face_sides = keep(t.face_sides, np.int64)
+        tab.freestream = keep(boundary.state, np.float64) if boundary is not None else None
+        err = C.c_int(0)
+        with torch.cuda.device(self.device):
+            self._ctx = lib.mhdg_create(C.byref(tab), self.device.index, C.byref(err))
+        if not self._ctx:
+            N.raise_for(err.value or 6, None, "(mhdg_create)")
+        self._keep = []
+        self._scalar = torch.zeros(8, dtype=torch.float64, device=self.device)
+        sizes = (C.c_int64 * 5)()
+        lib.mhdg_lin_sizes(self._ctx, sizes)
+        self.lin_sizes = tuple(int(s) for s in sizes)
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx:
+            try:
+                self._lib.mhdg_destroy(ctx)
+            except Exception:
+                pass
+            self._ctx = None
+
+    # -- geometry views (host) -------------------------------------------------
+    @property
+    def node_coords(self):
+        return self.tables.node_coords
+
+    @property
+    def trace_coords(self):
+        return self.tables.trace_coords
+
+    @property
+    def quad_coords(self):
+        return self.tables.quad_coords
+
+    @property
+    def vol_w(self):
+        return self.tables.vol_w
+
+    @property
+    def face_rows(self):
+        return self.tables.face_rows
+
+    @property
+    def face_id_st(self):
+        return self.tables.face_id_st
+
+    @property
+    def trace_idx(self):
+        return self.tables.trace_idx
+
+    @property
+    def launch_count(self):
+        return int(self._lib.mhdg_launch_count(self._ctx))
+
+    # -- helpers ---------------------------------------------------------------
+    def _dev(self, a):
+        return as_device(a, self.device)
+
+    def _fields(self, fields):
+        return self._dev(fields.w), self._dev(fields.trace)
+
+    def vdot(self, x, y):
+        """Deterministic device dot product (float)."""
+        self._lib.mhdg_dot(self._ctx, x.numel(), N.ptr(x), N.ptr(y), N.ptr(self._scalar),
+                           N.stream_handle())
+        return float(self._scalar[0].item())
+
+    # -- state handling ------------------------------------------------------
+    def to_conservative(self, w, where=""):
+        if self.formulation == "conservative":
+            return self._dev(w)
+        w = self._dev(w)
+        out = self._torch_empty_like(w)
+        st = N.Status()
+        rc = self._lib.mhdg_to_conservative(self._ctx, w.numel() // 5, N.ptr(w), N.ptr(out),
+                                            C.byref(st), N.stream_handle())
+        if rc:
+            from .errors import NonAdmissibleEntropyState
+
+            raise NonAdmissibleEntropyState("non-positive inverse temperature", where=where)
+        return out
+
+    def from_conservative(self, u):
+        if self.formulation == "conservative":
+            return self._dev(u)
+        u = self._dev(u)
+        out = self._torch_empty_like(u)
+        self._lib.mhdg_from_conservative(self._ctx, u.numel() // 5, N.ptr(u), N.ptr(out),
+                                         N.stream_handle())
+        return out
+
+    def _torch_empty_like(self, t):
+        return _torch().empty_like(t)
+
+    def project(self, state_fn):
+        """Nodal interpolation of an exact conservative-state function; the
+        conversion to working variables uses the host gas algebra so the
+        projected coefficients are bit-identical to the reference's."""
+        u_nodes = state_fn(self.node_coords)
+        u_trace = state_fn(self.trace_coords)
+        if self.formulation == "entropy":
+            u_nodes, u_trace = self.gas.entropy_vars(u_nodes), self.gas.entropy_vars(u_trace)
+        return FieldSet(w=self._dev(u_nodes), trace=self._dev(u_trace))
+
+    def volume_quad_states(self, fields):
+        torch = _torch()
+        w = self._dev(fields.w)
+        E = self.mesh.n_macros
+        out = torch.empty((E, 1, self.phi.shape[0], 5), dtype=torch.float64, device=self.device)
+        st = N.Status()
+        rc = self._lib.mhdg_volume_quad_states(self._ctx, N.ptr(w), N.ptr(out), C.byref(st),
+                                               N.stream_handle())
+        N.raise_for(rc, st)
+        return out
+
+    # -- residuals -------------------------------------------------------------
+    def residuals(self, fields, stage=None, check=True, sync=True):
+        torch = _torch()
+        w, tr = self._fields(fields)
+        r_w = torch.empty_like(w)
+        r_tr = torch.empty_like(tr)
+        off = None
+        if stage is not None and stage.offset is not None:
+            off = self._dev(stage.offset)
+        st = N.Status()
+        rc = self._lib.mhdg_residual(
+            self._ctx, N.ptr(w), N.ptr(tr), int(stage is not None),
+            float(stage.alpha) if stage is not None else 0.0, N.ptr(off), int(bool(check)),
+            N.ptr(r_w), N.ptr(r_tr), int(bool(sync)), C.byref(st), N.stream_handle())
+        N.raise_for(rc, st)
+        return ResidualSet(r_w=r_w, r_trace=r_tr, r_q=None, _disc=self)
+
+    def jacobian(self, fields, stage=None, ptc_weight=0.0, sparse_local_threshold=2048):
+        return LinearizedSystem(self, fields, stage, ptc_weight)
+
+    # -- monitors ----------------------------------------------------------------
+    def integrals(self, fields):
+        w = self._dev(fields.w)
+        out = (C.c_double * 5)()
+        self._lib.mhdg_integrals(self._ctx, N.ptr(w), out, N.stream_handle())
+        keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+        return {k: float(out[i]) for i, k in enumerate(keys)}
+
+    def total_generalized_entropy(self, fields):
+        v = self.integrals(fields)
+        return v["entropy"], v["thermo_entropy"]
+
+    def l2_error(self, fields, exact_fn, component=0):
+        u_q = self.volume_quad_states(fields).cpu().numpy()
+        u_ex = exact_fn(self.quad_coords[:, 0])
+        diff = u_q[:, 0, :, component] - u_ex[..., component]
+        return math.sqrt(float(np.sum(self.vol_w[:, 0] * diff ** 2)))
+
+    def max_wavespeed(self, fields):
+        u = self.volume_quad_states(fields).cpu().numpy()
+        rho, vel, p = self.gas.primitive(u)
+        c = np.sqrt(self.gas.gamma * p / rho)
+        return float((np.linalg.norm(vel, axis=-1) + c).max())
+
+
+class LinearizedSystem:
+    """Static condensation on the device: S^-1 per macro, face linearization
+    tensors, face-block preconditioner inverses (assembly.py:755-1180)."""
+
+    def __init__(self, disc, fields, stage, ptc_weight):
+        torch = _torch()
+        self.disc = disc
+        self.viscous = False
+        w, tr = disc._fields(fields)
+        self.trace_shape = tuple(tr.shape)
+        sz = disc.lin_sizes
+        dev = disc.device
+        self.sinv = torch.empty(sz[0], dtype=torch.float64, device=dev)
+        self.hw = torch.empty(sz[1], dtype=torch.float64, device=dev)
+        self.hhat = torch.empty(sz[2], dtype=torch.float64, device=dev)
+        self.hh = torch.empty(sz[3], dtype=torch.float64, device=dev)
+        self.pinv = torch.empty(sz[4], dtype=torch.float64, device=dev)
+        self._buf = N.LinBuffers(N.ptr(self.sinv), N.ptr(self.hw), N.ptr(self.hhat),
+                                 N.ptr(self.hh), N.ptr(self.pinv))
+        alpha = float(stage.alpha) if stage is not None else 0.0
+        st = N.Status()
+        rc = disc._lib.mhdg_linearize(disc._ctx, N.ptr(w), N.ptr(tr), alpha, float(ptc_weight),
+                                      C.byref(self._buf), C.byref(st), N.stream_handle())
+        N.raise_for(rc, st)
+        self.n_unsym = int(st.n_unsym)
+
+    def _out_trace(self):
+        return _torch().empty(self.trace_shape, dtype=_torch().float64, device=self.disc.device)
+
+    def matvec(self, xh):
+        d = self.disc
+        x = d._dev(xh).reshape(self.trace_shape)
+        y = self._out_trace()
+        rc = d._lib.mhdg_matvec(d._ctx, C.byref(self._buf), N.ptr(x), N.ptr(y), N.stream_handle())
+        N.raise_for(rc)
+        return y
+
+    def condensed_rhs(self, res):
+        d = self.disc
+        rw, rt = d._dev(res.r_w), d._dev(res.r_trace)
+        b = self._out_trace()
+        rc = d._lib.mhdg_condensed_rhs(d._ctx, C.byref(self._buf), N.ptr(rw), N.ptr(rt), N.ptr(b),
+                                       N.stream_handle())
+        N.raise_for(rc)
+        return b
+
+    def recover(self, res, d_trace):
+        d = self.disc
+        rw = d._dev(res.r_w)
+        x = d._dev(d_trace).reshape(self.trace_shape)
+        dw = _torch().empty_like(rw)
+        rc = d._lib.mhdg_recover(d._ctx, C.byref(self._buf), N.ptr(rw), N.ptr(x), N.ptr(dw),
+                                 N.stream_handle())
+        N.raise_for(rc)
+        return dw, None
+
+    def apply_preconditioner(self, r):
+        d = self.disc
+        r = d._dev(r).reshape(self.trace_shape)
+        z = self._out_trace()
+        rc = d._lib.mhdg_precond(d._ctx, C.byref(self._buf), N.ptr(r), N.ptr(z), N.stream_handle())
+        N.raise_for(rc)
+        return z

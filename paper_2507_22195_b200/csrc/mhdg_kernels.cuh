@@ -1,0 +1,848 @@
+// Device kernels of the macro-element HDG operator (m = 1, 3D, degree P).
+//
+// Data layout in HBM (float64, reference layouts so inputs are drop-in):
+//   w       (E, NN, 5)      nodal working variables per macro
+//   trace   (F, NFN, 5)     trace nodes per skeleton face (owner order)
+//   offset  (E, NQ, 5)      stage offset at volume quadrature points
+//   sinv    (E, NM, NM)     S^-1 per macro, column-major  (NM = 5 NN)
+//   hw/hhat/hh (E, 4, NQF, 5, 5) face-quadrature linearization tensors
+//   pinv    (F, NB, NB)     face-block inverse, column-major (NB = 5 NFN)
+// Per-macro geometry (det, J^-1, normals, areas, face ids, trace
+// permutations) is uploaded once; basis tables are staged in shared memory
+// once per persistent CTA.
+//
+// Trace scatter: with m = 1 every trace node receives exactly two side
+// contributions (one per skeleton side) on a zeroed output, so fp64
+// atomicAdd yields 0 + a + b = the reference's np.add.at sum bit for bit
+// and independent of order (IEEE addition is commutative).
+#pragma once
+#include "mhdg_math.cuh"
+
+namespace mhdg {
+
+template <int P>
+struct Dims {
+  static constexpr int NN = (P + 1) * (P + 2) * (P + 3) / 6;
+  static constexpr int NQ = (P + 1) * (P + 1) * (P + 1);
+  static constexpr int NFN = (P + 1) * (P + 2) / 2;
+  static constexpr int NQF = (P + 1) * (P + 1);
+  static constexpr int NM = 5 * NN;
+  static constexpr int NB = 5 * NFN;
+  // odd strides avoid shared-memory bank conflicts for per-q row access
+  static constexpr int QS = 4 * NN + 1;                  // B table row (q)
+  static constexpr int FS = (NFN % 2) ? NFN : NFN + 1;   // facet table row
+  static constexpr int GS = 21;                          // volume flux row
+};
+
+struct Geo {
+  int E, F;
+  int form, kind;
+  double gamma;
+  // reference tables
+  const double* B;     // (NQ, 4, NN): dphi_x, dphi_y, dphi_z, phi
+  const double* qw;    // (NQ)
+  const double* pf;    // (4, NQF, NFN)
+  const double* fphi;  // (NQF, NFN)
+  const double* fw;    // (NQF)
+  const int* rows;     // (4, NFN)
+  const int* nodef;    // (NN, 3): k*NFN+j of faces containing node, -1 pad
+  // per macro
+  const double* det;   // (E)
+  const double* invj;  // (E, 9)  [k][a]
+  const double* nrm;   // (E, 4, 3)
+  const double* area;  // (E, 4)
+  const int* fid;      // (E, 4)
+  const int* tidx;     // (E, 4, NFN)
+  const unsigned char* bnd;  // (E, 4)
+  const int* fsides;   // (F, 2)
+  int has_uinf;
+  double uinf[5];
+};
+
+// status key: ((loc*4 + sub) << 40) | item ; smallest key = first error in
+// the reference's loop order (volume sub, then tiles; entropy before check)
+__device__ __forceinline__ void report(unsigned long long* st, int loc, int sub, long long item) {
+  unsigned long long key = ((unsigned long long)(loc * 4 + sub) << 40) | (unsigned long long)item;
+  atomicMin(st, key);
+}
+
+template <int P>
+struct Smem {
+  using D = Dims<P>;
+  static constexpr int tables = D::NQ * D::QS + 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF;
+};
+
+// Stage reference tables into shared memory.
+template <int P>
+__device__ void load_tables(const Geo& g, double* sB, double* sPF, double* sFP, double* sQW,
+                            double* sFW, int* sRows, int* sNF) {
+  using D = Dims<P>;
+  for (int i = threadIdx.x; i < D::NQ * 4 * D::NN; i += blockDim.x) {
+    int q = i / (4 * D::NN), r = i % (4 * D::NN);
+    sB[q * D::QS + r] = g.B[i];
+  }
+  for (int i = threadIdx.x; i < 4 * D::NQF * D::NFN; i += blockDim.x) {
+    int kq = i / D::NFN, j = i % D::NFN;
+    sPF[kq * D::FS + j] = g.pf[i];
+  }
+  for (int i = threadIdx.x; i < D::NQF * D::NFN; i += blockDim.x) {
+    int q = i / D::NFN, j = i % D::NFN;
+    sFP[q * D::FS + j] = g.fphi[i];
+  }
+  for (int i = threadIdx.x; i < D::NQ; i += blockDim.x) sQW[i] = g.qw[i];
+  for (int i = threadIdx.x; i < D::NQF; i += blockDim.x) sFW[i] = g.fw[i];
+  if (sRows)
+    for (int i = threadIdx.x; i < 4 * D::NFN; i += blockDim.x) sRows[i] = g.rows[i];
+  if (sNF)
+    for (int i = threadIdx.x; i < 3 * D::NN; i += blockDim.x) sNF[i] = g.nodef[i];
+}
+
+// ===========================================================================
+// K1: residual  (assembly.py:459-549, inviscid)
+// ===========================================================================
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace,
+           int has_stage, double alpha, const double* __restrict__ offset, int check,
+           double* __restrict__ r_w, double* __restrict__ r_tr, unsigned long long* status) {
+  using D = Dims<P>;
+  extern __shared__ double smem[];
+  double* sB = smem;
+  double* sPF = sB + D::NQ * D::QS;
+  double* sFP = sPF + 4 * D::NQF * D::FS;
+  double* sQW = sFP + D::NQF * D::FS;
+  double* sFW = sQW + D::NQ;
+  double* sW = sFW + D::NQF;                 // NN*5
+  double* sTR = sW + D::NN * 5;              // 4*NFN*5
+  double* sG = sTR + 4 * D::NFN * 5;         // NQ*GS
+  double* sH = sG + D::NQ * D::GS;           // 4*NQF*5
+  double* sHg = sH + 4 * D::NQF * 5;         // 4*NQF*5
+  double* sGeo = sHg + 4 * D::NQF * 5;       // 1 + 9 + 12 + 4
+  int* sRows = (int*)(sGeo + 26);
+  int* sNF = sRows + 4 * D::NFN;
+  int* sFid = sNF + 3 * D::NN;               // 4
+  int* sTid = sFid + 4;                      // 4*NFN
+  int* sBnd = sTid + 4 * D::NFN;             // 4
+  load_tables<P>(g, sB, sPF, sFP, sQW, sFW, sRows, sNF);
+  const double gam = g.gamma;
+  const int tid = threadIdx.x;
+
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = tid; i < D::NN * 5; i += NT) sW[i] = w[(size_t)e * D::NN * 5 + i];
+    if (tid < 4) {
+      sFid[tid] = g.fid[e * 4 + tid];
+      sBnd[tid] = g.bnd ? g.bnd[e * 4 + tid] : 0;
+    }
+    for (int i = tid; i < 4 * D::NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * D::NFN + i];
+    if (tid == 0) sGeo[0] = g.det[e];
+    if (tid >= 1 && tid < 10) sGeo[tid] = g.invj[(size_t)e * 9 + tid - 1];
+    if (tid >= 10 && tid < 22) sGeo[tid] = g.nrm[(size_t)e * 12 + tid - 10];
+    if (tid >= 22 && tid < 26) sGeo[tid] = g.area[(size_t)e * 4 + tid - 22];
+    __syncthreads();
+    for (int i = tid; i < 4 * D::NFN * 5; i += NT) {
+      int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
+      sTR[i] = trace[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s];
+    }
+    __syncthreads();
+
+    // ---- pointwise: volume quadrature points and face quadrature points
+    for (int it = tid; it < D::NQ + 4 * D::NQF; it += NT) {
+      if (it < D::NQ) {
+        const int q = it;
+        const double* Bq = sB + q * D::QS + 3 * D::NN;
+        double wq[5] = {0, 0, 0, 0, 0};
+        for (int i = 0; i < D::NN; ++i) {
+          double ph = Bq[i];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) wq[s] += ph * sW[i * 5 + s];
+        }
+        double u[5];
+        if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e);
+        if (check && !admissible(u, gam)) report(status, 0, 2, e);
+        double F[5][3];
+        flux(u, gam, F);
+        const double vw = sQW[q] * sGeo[0];
+        double* G = sG + q * D::GS;
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) G[kk * 5 + s] = -(vw * ((j0 * F[s][0] + j1 * F[s][1]) + j2 * F[s][2]));
+        }
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          double tmp = 0.0;
+          if (has_stage) {
+            tmp = alpha * u[s];
+            if (offset) tmp = tmp + offset[((size_t)e * D::NQ + q) * 5 + s];
+            tmp = vw * tmp;
+          }
+          G[15 + s] = tmp;
+        }
+      } else {
+        const int fi = it - D::NQ;
+        const int k = fi / D::NQF, q = fi % D::NQF;
+        const double* pf = sPF + (k * D::NQF + q) * D::FS;
+        const double* fp = sFP + q * D::FS;
+        double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
+        for (int j = 0; j < D::NFN; ++j) {
+          const double a = pf[j], b = fp[j];
+          const int row = sRows[k * D::NFN + j];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) {
+            wq[s] += a * sW[row * 5 + s];
+            whq[s] += b * sTR[(k * D::NFN + j) * 5 + s];
+          }
+        }
+        double u[5], uh[5];
+        if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e);
+        if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e);
+        if (check && !admissible(u, gam)) report(status, 1 + k, 2, e);
+        if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e);
+        const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
+        double fh[5];
+        numerical_flux(g.kind, u, uh, n, gam, fh);
+        const double fwq = sFW[q] * sGeo[22 + k];
+        double* H = sH + (k * D::NQF + q) * 5;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) H[s] = fwq * fh[s];
+        if (sBnd[k] && g.has_uinf) {
+          const double mn[3] = {-n[0], -n[1], -n[2]};
+          double gh[5];
+          numerical_flux(g.kind, g.uinf, uh, mn, gam, gh);
+#pragma unroll
+          for (int s = 0; s < 5; ++s) sHg[(k * D::NQF + q) * 5 + s] = fwq * gh[s];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- contraction to the macro test functions
+    for (int o = tid; o < D::NN * 5; o += NT) {
+      const int i = o / 5, s = o % 5;
+      double av = 0.0, at = 0.0;
+      for (int q = 0; q < D::NQ; ++q) {
+        const double* Bq = sB + q * D::QS + i;
+        const double* G = sG + q * D::GS + s;
+        av += (Bq[0] * G[0] + Bq[D::NN] * G[5]) + Bq[2 * D::NN] * G[10];
+        at += Bq[3 * D::NN] * G[15];
+      }
+      double r = av + at;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int kj = sNF[i * 3 + c];
+        if (kj < 0) break;
+        const int k = kj / D::NFN, j = kj % D::NFN;
+        double acc = 0.0;
+        for (int q = 0; q < D::NQF; ++q) acc += sPF[(k * D::NQF + q) * D::FS + j] * sH[(k * D::NQF + q) * 5 + s];
+        r += acc;
+      }
+      r_w[(size_t)e * D::NN * 5 + o] = r;
+    }
+    // ---- side contributions to the trace equation
+    for (int o = tid; o < 4 * D::NFN * 5; o += NT) {
+      const int k = o / (D::NFN * 5), j = (o / 5) % D::NFN, s = o % 5;
+      double acc = 0.0;
+      for (int q = 0; q < D::NQF; ++q) acc += sFP[q * D::FS + j] * sH[(k * D::NQF + q) * 5 + s];
+      if (sBnd[k] && g.has_uinf) {
+        double ag = 0.0;
+        for (int q = 0; q < D::NQF; ++q) ag += sFP[q * D::FS + j] * sHg[(k * D::NQF + q) * 5 + s];
+        acc += ag;
+      }
+      atomicAdd(&r_tr[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s], acc);
+    }
+  }
+}
+
+// ===========================================================================
+// In-place Gauss-Jordan inverse with partial (row) pivoting, n x n row-major
+// in `A` (shared or global), whole block cooperating.  Pivot choice: first
+// row of maximal |a_ik| (LAPACK idamax semantics).  Returns false (uniformly
+// across the block) if a pivot is zero or non-finite.
+// ===========================================================================
+__device__ bool gj_inverse(double* A, int n, int lda, int* perm, double* col, int* sflag) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) *sflag = 0;
+  for (int k = 0; k < n; ++k) {
+    __syncthreads();
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = n;
+      for (int r = k + tid; r < n; r += 32) {
+        double v = fabs(A[r * lda + k]);
+        if (v > best || (v != v && best >= 0)) { best = v; bi = r; }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        double ob = __shfl_down_sync(0xffffffffu, best, off);
+        int oi = __shfl_down_sync(0xffffffffu, bi, off);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        perm[k] = bi;
+        double pv = bi < n ? A[bi * lda + k] : 0.0;
+        if (!(fabs(pv) > 0.0) || !isfinite(pv)) *sflag = 1;
+      }
+    }
+    __syncthreads();
+    const int p = perm[k];
+    if (p != k)
+      for (int j = tid; j < n; j += nt) {
+        double t = A[k * lda + j];
+        A[k * lda + j] = A[p * lda + j];
+        A[p * lda + j] = t;
+      }
+    __syncthreads();
+    for (int r = tid; r < n; r += nt) col[r] = A[r * lda + k];
+    __syncthreads();
+    const double pinv = 1.0 / col[k];
+    for (int j = tid; j < n; j += nt) A[k * lda + j] = (j == k ? 1.0 : A[k * lda + j]) * pinv;
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += nt) {
+      const int r = idx / n, j = idx % n;
+      if (r == k) continue;
+      const double base = (j == k) ? 0.0 : A[r * lda + j];
+      A[r * lda + j] = base - A[k * lda + j] * col[r];
+    }
+  }
+  __syncthreads();
+  // undo the row interchanges as column interchanges, in reverse order
+  for (int r = tid; r < n; r += nt)
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = perm[k];
+      if (p != k) {
+        double t = A[r * lda + k];
+        A[r * lda + k] = A[r * lda + p];
+        A[r * lda + p] = t;
+      }
+    }
+  __syncthreads();
+  return *sflag == 0;
+}
+
+// ===========================================================================
+// K2: linearize + assemble S + S^-1   (assembly.py:772-976)
+// ===========================================================================
+template <int P>
+struct LinSmem {
+  using D = Dims<P>;
+  static constexpr int QC = 8;                                // q chunk
+  static constexpr bool S_IN_SMEM = (D::NM * D::NM * 8) <= 100 * 1024;
+  static constexpr int doubles =
+      Smem<P>::tables + D::NN * 5 + 4 * D::NFN * 5 + QC * 100 + D::NQF * 25 + D::NM + 32 +
+      (S_IN_SMEM ? D::NM * D::NM : 0);
+  static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + D::NM + 4;
+  static constexpr size_t bytes = doubles * 8 + ints * 4;
+};
+
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trace, double weight,
+            double ptc, double* __restrict__ sinv, double* __restrict__ hw_out,
+            double* __restrict__ hhat_out, double* __restrict__ hh_out, double* __restrict__ scratch,
+            unsigned long long* status) {
+  using D = Dims<P>;
+  using L = LinSmem<P>;
+  constexpr int QC = L::QC;
+  constexpr int NM = D::NM;
+  extern __shared__ double smem[];
+  double* sB = smem;
+  double* sPF = sB + D::NQ * D::QS;
+  double* sFP = sPF + 4 * D::NQF * D::FS;
+  double* sQW = sFP + D::NQF * D::FS;
+  double* sFW = sQW + D::NQ;
+  double* sW = sFW + D::NQF;
+  double* sTR = sW + D::NN * 5;
+  double* sC = sTR + 4 * D::NFN * 5;          // QC*100  [qq][kk][s][t]
+  double* sHW = sC + QC * 100;                 // NQF*25
+  double* sCol = sHW + D::NQF * 25;            // NM
+  double* sGeo = sCol + NM;                    // 32
+  double* S = L::S_IN_SMEM ? (sGeo + 32) : (scratch + (size_t)blockIdx.x * NM * NM);
+  int* ibase = (int*)(sGeo + 32 + (L::S_IN_SMEM ? NM * NM : 0));
+  int* sRows = ibase;
+  int* sFid = sRows + 4 * D::NFN;
+  int* sTid = sFid + 4;
+  int* sBnd = sTid + 4 * D::NFN;
+  int* sPerm = sBnd + 4;
+  int* sFlag = sPerm + NM;
+  load_tables<P>(g, sB, sPF, sFP, sQW, sFW, sRows, nullptr);
+  const double gam = g.gamma;
+  const int tid = threadIdx.x;
+
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = tid; i < D::NN * 5; i += NT) sW[i] = w[(size_t)e * D::NN * 5 + i];
+    if (tid < 4) {
+      sFid[tid] = g.fid[e * 4 + tid];
+      sBnd[tid] = g.bnd ? g.bnd[e * 4 + tid] : 0;
+    }
+    for (int i = tid; i < 4 * D::NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * D::NFN + i];
+    if (tid == 0) sGeo[0] = g.det[e];
+    if (tid >= 1 && tid < 10) sGeo[tid] = g.invj[(size_t)e * 9 + tid - 1];
+    if (tid >= 10 && tid < 22) sGeo[tid] = g.nrm[(size_t)e * 12 + tid - 10];
+    if (tid >= 22 && tid < 26) sGeo[tid] = g.area[(size_t)e * 4 + tid - 22];
+    for (int i = tid; i < NM * NM; i += NT) S[i] = 0.0;
+    __syncthreads();
+    for (int i = tid; i < 4 * D::NFN * 5; i += NT) {
+      int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
+      sTR[i] = trace[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s];
+    }
+
+    // ---- volume blocks, in chunks of QC quadrature points
+    for (int q0 = 0; q0 < D::NQ; q0 += QC) {
+      __syncthreads();
+      for (int it = tid; it < QC * 5; it += NT) {
+        const int qq = it / 5, t = it % 5, q = q0 + qq;
+        double* C = sC + qq * 100;
+        if (q >= D::NQ) {
+          for (int r = 0; r < 4; ++r)
+            for (int s = 0; s < 5; ++s) C[r * 25 + s * 5 + t] = 0.0;
+          continue;
+        }
+        const double* Bq = sB + q * D::QS + 3 * D::NN;
+        double wq[5] = {0, 0, 0, 0, 0};
+        for (int i = 0; i < D::NN; ++i) {
+          double ph = Bq[i];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) wq[s] += ph * sW[i * 5 + s];
+        }
+        Dual wd[5], ud[5];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) wd[s] = mk(wq[s], s == t ? 1.0 : 0.0);
+        to_conservative(wd, g.form, gam, ud);
+        Dual F[5][3];
+        flux(ud, gam, F);
+        const double vw = sQW[q] * sGeo[0];
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
+#pragma unroll
+          for (int s = 0; s < 5; ++s)
+            C[kk * 25 + s * 5 + t] = -(vw * ((j0 * F[s][0].d + j1 * F[s][1].d) + j2 * F[s][2].d));
+        }
+#pragma unroll
+        for (int s = 0; s < 5; ++s) C[75 + s * 5 + t] = weight * (vw * ud[s].d);
+      }
+      __syncthreads();
+      const int qn = (D::NQ - q0) < QC ? (D::NQ - q0) : QC;
+      for (int o = tid; o < NM * NM; o += NT) {
+        const int r = o / NM, c = o % NM;
+        const int i = r / 5, s = r % 5, j = c / 5, t = c % 5;
+        double acc = 0.0;
+        for (int qq = 0; qq < qn; ++qq) {
+          const double* Bq = sB + (q0 + qq) * D::QS;
+          const double* C = sC + qq * 100 + s * 5 + t;
+          const double dd = ((Bq[i] * C[0] + Bq[D::NN + i] * C[25]) + Bq[2 * D::NN + i] * C[50]) +
+                            Bq[3 * D::NN + i] * C[75];
+          acc += dd * Bq[3 * D::NN + j];
+        }
+        S[o] += acc;
+      }
+    }
+
+    // ---- face tiles: hw, hhat, hh tensors and the S face blocks
+    for (int k = 0; k < 4; ++k) {
+      __syncthreads();
+      const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
+      for (int it = tid; it < D::NQF * 10; it += NT) {
+        const int q = it / 10, t = (it % 10) % 5, which = (it % 10) / 5;
+        const double* pf = sPF + (k * D::NQF + q) * D::FS;
+        const double* fp = sFP + q * D::FS;
+        double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
+        for (int j = 0; j < D::NFN; ++j) {
+          const double a = pf[j], b = fp[j];
+          const int row = sRows[k * D::NFN + j];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) {
+            wq[s] += a * sW[row * 5 + s];
+            whq[s] += b * sTR[(k * D::NFN + j) * 5 + s];
+          }
+        }
+        Dual wd[5], whd[5], ud[5], uhd[5], fd[5];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          wd[s] = mk(wq[s], (which == 0 && s == t) ? 1.0 : 0.0);
+          whd[s] = mk(whq[s], (which == 1 && s == t) ? 1.0 : 0.0);
+        }
+        to_conservative(wd, g.form, gam, ud);
+        to_conservative(whd, g.form, gam, uhd);
+        numerical_flux(g.kind, ud, uhd, n, gam, fd);
+        const size_t base = (((size_t)e * 4 + k) * D::NQF + q) * 25;
+        if (which == 0) {
+#pragma unroll
+          for (int s = 0; s < 5; ++s) {
+            hw_out[base + s * 5 + t] = fd[s].d;
+            sHW[q * 25 + s * 5 + t] = fd[s].d;
+          }
+        } else {
+          double hh[5];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) {
+            hhat_out[base + s * 5 + t] = fd[s].d;
+            hh[s] = fd[s].d;
+          }
+          if (sBnd[k] && g.has_uinf) {
+            Dual ui[5], gd[5];
+#pragma unroll
+            for (int s = 0; s < 5; ++s) ui[s] = mk(g.uinf[s], 0.0);
+            const double mn[3] = {-n[0], -n[1], -n[2]};
+            numerical_flux(g.kind, ui, uhd, mn, gam, gd);
+#pragma unroll
+            for (int s = 0; s < 5; ++s) hh[s] = hh[s] + gd[s].d;
+          }
+          if (ptc != 0.0) {
+#pragma unroll
+            for (int s = 0; s < 5; ++s) hh[s] = hh[s] + (-ptc * uhd[s].d);
+          }
+#pragma unroll
+          for (int s = 0; s < 5; ++s) hh_out[base + s * 5 + t] = hh[s];
+        }
+      }
+      __syncthreads();
+      const double ar = sGeo[22 + k];
+      for (int o = tid; o < D::NFN * D::NFN * 25; o += NT) {
+        const int ij = o / 25, st = o % 25;
+        const int i = ij / D::NFN, j = ij % D::NFN, s = st / 5, t = st % 5;
+        double acc = 0.0;
+        for (int q = 0; q < D::NQF; ++q) {
+          const double* pf = sPF + (k * D::NQF + q) * D::FS;
+          acc += (((sFW[q] * ar) * pf[i]) * sHW[q * 25 + st]) * pf[j];
+        }
+        const int r = sRows[k * D::NFN + i] * 5 + s, c = sRows[k * D::NFN + j] * 5 + t;
+        S[r * NM + c] += acc;
+      }
+    }
+    __syncthreads();
+
+    // ---- S^-1 (Gauss-Jordan) and column-major store
+    bool ok = gj_inverse(S, NM, NM, sPerm, sCol, sFlag);
+    int bad = 0;
+    for (int o = tid; o < NM * NM; o += NT) bad |= !isfinite(S[o]);
+    bad = __syncthreads_or(bad);
+    if ((!ok || bad) && tid == 0) report(status, 0, 0, e);
+    double* out = sinv + (size_t)e * NM * NM;
+    for (int o = tid; o < NM * NM; o += NT) {
+      const int c = o / NM, r = o % NM;
+      out[o] = S[r * NM + c];
+    }
+  }
+}
+
+// ===========================================================================
+// K4 (factor): face-block preconditioner  (assembly.py:994-1026, 736-752)
+// ===========================================================================
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_precond_factor(Geo g, const double* __restrict__ hh, double* __restrict__ pinv,
+                 unsigned long long* status, int* n_unsym) {
+  using D = Dims<P>;
+  constexpr int NB = D::NB;
+  extern __shared__ double smem[];
+  double* A = smem;                      // NB*NB
+  double* sHH = A + NB * NB;             // NQF*25
+  double* sFP = sHH + D::NQF * 25;       // NQF*NFN
+  double* sCol = sFP + D::NQF * D::NFN;  // NB
+  double* sFw = sCol + NB;               // NQF
+  int* sT = (int*)(sFw + D::NQF);        // NFN
+  int* sPerm = sT + D::NFN;              // NB
+  int* sFlag = sPerm + NB;               // 2
+  const int tid = threadIdx.x;
+  for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[i] = g.fphi[i];
+  for (int f = blockIdx.x; f < g.F; f += gridDim.x) {
+    __syncthreads();
+    for (int i = tid; i < NB * NB; i += NT) A[i] = 0.0;
+    for (int side = 0; side < 2; ++side) {
+      const int st = g.fsides[f * 2 + side];
+      if (st < 0) continue;
+      const int e = st / 4, k = st % 4;
+      __syncthreads();
+      for (int i = tid; i < D::NQF * 25; i += NT) sHH[i] = hh[((size_t)st * D::NQF) * 25 + i];
+      for (int i = tid; i < D::NFN; i += NT) sT[i] = g.tidx[((size_t)e * 4 + k) * D::NFN + i];
+      for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * g.area[(size_t)e * 4 + k];
+      __syncthreads();
+      for (int o = tid; o < D::NFN * D::NFN * 25; o += NT) {
+        const int ij = o / 25, stt = o % 25;
+        const int i = ij / D::NFN, j = ij % D::NFN, s = stt / 5, t = stt % 5;
+        double acc = 0.0;
+        for (int q = 0; q < D::NQF; ++q)
+          acc += ((sFw[q] * sFP[q * D::NFN + i]) * sHH[q * 25 + stt]) * sFP[q * D::NFN + j];
+        A[(sT[i] * 5 + s) * NB + sT[j] * 5 + t] += acc;
+      }
+    }
+    __syncthreads();
+    // symmetry statistic (reference logs the count of non-SPD/non-symmetric blocks)
+    if (tid < 32) {
+      double amax = 0.0, dmax = 0.0;
+      for (int idx = tid; idx < NB * NB; idx += 32) {
+        const int r = idx / NB, c = idx % NB;
+        amax = fmax(amax, fabs(A[idx]));
+        dmax = fmax(dmax, fabs(A[idx] - A[c * NB + r]));
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        amax = fmax(amax, __shfl_down_sync(0xffffffffu, amax, off));
+        dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, off));
+      }
+      if (tid == 0 && !(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
+    }
+    bool ok = gj_inverse(A, NB, NB, sPerm, sCol, sFlag);
+    int bad = 0;
+    for (int o = tid; o < NB * NB; o += NT) bad |= !isfinite(A[o]);
+    bad = __syncthreads_or(bad);
+    if ((!ok || bad) && tid == 0) report(status, 0, 0, f);
+    double* out = pinv + (size_t)f * NB * NB;
+    for (int o = tid; o < NB * NB; o += NT) {
+      const int c = o / NB, r = o % NB;
+      out[o] = A[r * NB + c];
+    }
+  }
+}
+
+// ===========================================================================
+// K3 / K6: condensed matvec, condensed rhs, recovery  (assembly.py:1028-1173)
+//   mode 0 matvec : y += [hh x - (hw S^-1 (hhat x)) scattered]      (y zeroed)
+//   mode 1 rhs    : y += hw S^-1(-r_w) scattered                    (y zeroed)
+//   mode 2 recover: d_w = S^-1(-r_w - hhat x)
+// ===========================================================================
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_condensed(Geo g, int mode, const double* __restrict__ sinv, const double* __restrict__ hw,
+            const double* __restrict__ hhat, const double* __restrict__ hh,
+            const double* __restrict__ x, const double* __restrict__ r_w, double* __restrict__ y,
+            double* __restrict__ d_w) {
+  using D = Dims<P>;
+  constexpr int NM = D::NM;
+  extern __shared__ double smem[];
+  double* sPF = smem;                          // 4*NQF*FS
+  double* sFP = sPF + 4 * D::NQF * D::FS;      // NQF*FS
+  double* sFW = sFP + D::NQF * D::FS;          // NQF
+  double* sX = sFW + D::NQF;                   // 4*NFN*5
+  double* sA1 = sX + 4 * D::NFN * 5;           // 4*NQF*5 (hhat x, weighted)
+  double* sA2 = sA1 + 4 * D::NQF * 5;          // 4*NQF*5 (hh x / hw z, weighted)
+  double* sG = sA2 + 4 * D::NQF * 5;           // NM
+  double* sZ = sG + NM;                        // NM
+  double* sAr = sZ + NM;                       // 4
+  int* sRows = (int*)(sAr + 4);                // 4*NFN
+  int* sNF = sRows + 4 * D::NFN;               // 3*NN
+  int* sFid = sNF + 3 * D::NN;                 // 4
+  int* sTid = sFid + 4;                        // 4*NFN
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 4 * D::NQF * D::NFN; i += NT) sPF[(i / D::NFN) * D::FS + i % D::NFN] = g.pf[i];
+  for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[(i / D::NFN) * D::FS + i % D::NFN] = g.fphi[i];
+  for (int i = tid; i < D::NQF; i += NT) sFW[i] = g.fw[i];
+  for (int i = tid; i < 4 * D::NFN; i += NT) sRows[i] = g.rows[i];
+  for (int i = tid; i < 3 * D::NN; i += NT) sNF[i] = g.nodef[i];
+
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    if (tid < 4) {
+      sFid[tid] = g.fid[e * 4 + tid];
+      sAr[tid] = g.area[(size_t)e * 4 + tid];
+    }
+    for (int i = tid; i < 4 * D::NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * D::NFN + i];
+    __syncthreads();
+    if (mode != 1) {
+      for (int i = tid; i < 4 * D::NFN * 5; i += NT) {
+        int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
+        sX[i] = x[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s];
+      }
+      __syncthreads();
+      // a1 = fw * hhat xq ; a2 = fw * hh xq
+      for (int it = tid; it < 4 * D::NQF; it += NT) {
+        const int k = it / D::NQF, q = it % D::NQF;
+        const double* fp = sFP + q * D::FS;
+        double xq[5] = {0, 0, 0, 0, 0};
+        for (int j = 0; j < D::NFN; ++j) {
+          const double b = fp[j];
+#pragma unroll
+          for (int s = 0; s < 5; ++s) xq[s] += b * sX[(k * D::NFN + j) * 5 + s];
+        }
+        const size_t base = (((size_t)e * 4 + k) * D::NQF + q) * 25;
+        const double fwq = sFW[q] * sAr[k];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          double a = 0.0, b = 0.0;
+#pragma unroll
+          for (int t = 0; t < 5; ++t) {
+            a += hhat[base + s * 5 + t] * xq[t];
+            if (mode == 0) b += hh[base + s * 5 + t] * xq[t];
+          }
+          sA1[it * 5 + s] = fwq * a;
+          if (mode == 0) sA2[it * 5 + s] = fwq * b;
+        }
+      }
+      __syncthreads();
+    }
+    // right-hand side of the local solve
+    for (int o = tid; o < NM; o += NT) {
+      const int i = o / 5, s = o % 5;
+      double v = 0.0;
+      if (mode != 1) {
+        for (int c = 0; c < 3; ++c) {
+          const int kj = sNF[i * 3 + c];
+          if (kj < 0) break;
+          const int k = kj / D::NFN, j = kj % D::NFN;
+          double acc = 0.0;
+          for (int q = 0; q < D::NQF; ++q) acc += sPF[(k * D::NQF + q) * D::FS + j] * sA1[(k * D::NQF + q) * 5 + s];
+          v += acc;
+        }
+      }
+      if (mode == 0) sG[o] = -v;
+      else if (mode == 1) sG[o] = -r_w[(size_t)e * NM + o];
+      else sG[o] = -r_w[(size_t)e * NM + o] + (-v);
+    }
+    __syncthreads();
+    // z = S^-1 g : column-major GEMV, rows across threads (coalesced)
+    const double* Si = sinv + (size_t)e * NM * NM;
+    for (int r = tid; r < NM; r += NT) {
+      double acc0 = 0.0, acc1 = 0.0;
+      int c = 0;
+      for (; c + 1 < NM; c += 2) {
+        acc0 += Si[(size_t)c * NM + r] * sG[c];
+        acc1 += Si[(size_t)(c + 1) * NM + r] * sG[c + 1];
+      }
+      if (c < NM) acc0 += Si[(size_t)c * NM + r] * sG[c];
+      sZ[r] = acc0 + acc1;
+    }
+    __syncthreads();
+    if (mode == 2) {
+      for (int o = tid; o < NM; o += NT) d_w[(size_t)e * NM + o] = sZ[o];
+      continue;
+    }
+    // a3 = fw * hw zq (overwrites a1)
+    for (int it = tid; it < 4 * D::NQF; it += NT) {
+      const int k = it / D::NQF, q = it % D::NQF;
+      const double* pf = sPF + (k * D::NQF + q) * D::FS;
+      double zq[5] = {0, 0, 0, 0, 0};
+      for (int j = 0; j < D::NFN; ++j) {
+        const double a = pf[j];
+        const int row = sRows[k * D::NFN + j];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) zq[s] += a * sZ[row * 5 + s];
+      }
+      const size_t base = (((size_t)e * 4 + k) * D::NQF + q) * 25;
+      const double fwq = sFW[q] * sAr[k];
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        double a = 0.0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) a += hw[base + s * 5 + t] * zq[t];
+        sA1[it * 5 + s] = fwq * a;
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < 4 * D::NFN * 5; o += NT) {
+      const int k = o / (D::NFN * 5), j = (o / 5) % D::NFN, s = o % 5;
+      double a = 0.0, b = 0.0;
+      for (int q = 0; q < D::NQF; ++q) {
+        const double fp = sFP[q * D::FS + j];
+        a += fp * sA1[(k * D::NQF + q) * 5 + s];
+        if (mode == 0) b += fp * sA2[(k * D::NQF + q) * 5 + s];
+      }
+      atomicAdd(&y[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s], b + a);
+    }
+  }
+}
+
+// K4 (apply): z_f = P_f^-1 r_f, column-major GEMV per face
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_precond_apply(int F, const double* __restrict__ pinv, const double* __restrict__ r,
+                double* __restrict__ z) {
+  constexpr int NB = Dims<P>::NB;
+  __shared__ double sR[NB];
+  for (int f = blockIdx.x; f < F; f += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < NB; i += NT) sR[i] = r[(size_t)f * NB + i];
+    __syncthreads();
+    const double* A = pinv + (size_t)f * NB * NB;
+    for (int row = threadIdx.x; row < NB; row += NT) {
+      double acc0 = 0.0, acc1 = 0.0;
+      int c = 0;
+      for (; c + 1 < NB; c += 2) {
+        acc0 += A[(size_t)c * NB + row] * sR[c];
+        acc1 += A[(size_t)(c + 1) * NB + row] * sR[c + 1];
+      }
+      if (c < NB) acc0 += A[(size_t)c * NB + row] * sR[c];
+      z[(size_t)f * NB + row] = acc0 + acc1;
+    }
+  }
+}
+
+// ===========================================================================
+// pointwise helpers and monitors
+// ===========================================================================
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_volume_states(Geo g, const double* __restrict__ w, double* __restrict__ out,
+                unsigned long long* status) {
+  using D = Dims<P>;
+  __shared__ double sPhi[D::NQ * D::NN];
+  __shared__ double sW[D::NN * 5];
+  for (int i = threadIdx.x; i < D::NQ * D::NN; i += NT)
+    sPhi[i] = g.B[(i / D::NN) * 4 * D::NN + 3 * D::NN + i % D::NN];
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < D::NN * 5; i += NT) sW[i] = w[(size_t)e * D::NN * 5 + i];
+    __syncthreads();
+    for (int q = threadIdx.x; q < D::NQ; q += NT) {
+      double wq[5] = {0, 0, 0, 0, 0};
+      for (int i = 0; i < D::NN; ++i) {
+        const double ph = sPhi[q * D::NN + i];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) wq[s] += ph * sW[i * 5 + s];
+      }
+      double u[5];
+      if (!to_conservative(wq, g.form, g.gamma, u)) report(status, 0, 0, e);
+#pragma unroll
+      for (int s = 0; s < 5; ++s) out[((size_t)e * D::NQ + q) * 5 + s] = u[s];
+    }
+  }
+}
+
+// monitors: per-block partial sums of the five integrals (assembly.py:595-620)
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_integrals(Geo g, const double* __restrict__ w, double* __restrict__ partial) {
+  using D = Dims<P>;
+  __shared__ double sPhi[D::NQ * D::NN];
+  __shared__ double sW[D::NN * 5];
+  __shared__ double red[5][NT];
+  for (int i = threadIdx.x; i < D::NQ * D::NN; i += NT)
+    sPhi[i] = g.B[(i / D::NN) * 4 * D::NN + 3 * D::NN + i % D::NN];
+  double acc[5] = {0, 0, 0, 0, 0};
+  const double gam = g.gamma;
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < D::NN * 5; i += NT) sW[i] = w[(size_t)e * D::NN * 5 + i];
+    __syncthreads();
+    for (int q = threadIdx.x; q < D::NQ; q += NT) {
+      double wq[5] = {0, 0, 0, 0, 0};
+      for (int i = 0; i < D::NN; ++i) {
+        const double ph = sPhi[q * D::NN + i];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) wq[s] += ph * sW[i * 5 + s];
+      }
+      double u[5];
+      to_conservative(wq, g.form, gam, u);
+      double rho, vel[3], p;
+      primitive(u, gam, rho, vel, p);
+      const double vw = g.qw[q] * g.det[e];
+      const double sp = ::log(p) - gam * ::log(rho);
+      acc[0] += vw * (-rho * sp / (gam - 1.0));
+      acc[1] += vw * rho * sp;
+      acc[2] += vw * 0.5 * rho * ((vel[0] * vel[0] + vel[1] * vel[1]) + vel[2] * vel[2]);
+      acc[3] += vw * rho;
+      acc[4] += vw * u[4];
+    }
+  }
+  for (int c = 0; c < 5; ++c) red[c][threadIdx.x] = acc[c];
+  __syncthreads();
+  for (int sft = NT / 2; sft > 0; sft >>= 1) {
+    if (threadIdx.x < sft)
+      for (int c = 0; c < 5; ++c) red[c][threadIdx.x] += red[c][threadIdx.x + sft];
+    __syncthreads();
+  }
+  if (threadIdx.x < 5) partial[blockIdx.x * 5 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+}  // namespace mhdg

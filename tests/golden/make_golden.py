@@ -1,0 +1,215 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container (the reference is importable there, not on the
+GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  Each file holds the seeded inputs and the
+reference's outputs for one case, plus the reference's own 1-ulp
+self-sensitivity of every output (relative L2 change when w and trace are
+perturbed by +-1 ulp), which sets the attainable parity floor
+(SURVEY.md finding 11).
+
+Cases
+  kat2d_p1_ec      2D two-triangle mesh, p=1, EC flux, seed 13, amp 0.08
+                   (the reference's independent hand-assembly KAT,
+                   test_assembly.py:488-576)
+  sweep_k{1..4}_{flux}
+                   config-5 style: 3D unit box, n=(2,2,2), m=1,
+                   perturbed-uniform states rho~U[.9,1.1], V~U[-.5,.5],
+                   P~U[.9,1.1] per C0 node then per trace node, entropy form;
+                   alpha = d00/dt (dt=0.01), offset = -alpha*u_quad,
+                   ptc_weight = 1, x ~ N(0,1) with seed+1
+  cfg1_*           config 1: vortex on [0,10]^3, n=4, p=2, ES, projected IC;
+                   operator outputs at the first stage, the state after one
+                   DIRK(3,3) step with dt=0.01, and the integral history of
+                   10 steps
+  cons_k2_lf       conservative formulation, LF flux (format coverage)
+  fs_k2_es         free-stream boundary on a non-periodic box (ghost flux)
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+from macrohdg.assembly import Discretization, FieldSet, FreeStream, StageContext  # noqa: E402
+from macrohdg.cases import IsentropicVortex  # noqa: E402
+from macrohdg.fluxes import DissipationSpec  # noqa: E402
+from macrohdg.gas import GasModel  # noqa: E402
+from macrohdg.mesh import build_box_macro_mesh  # noqa: E402
+from macrohdg.time_march import DIRKIntegrator, dirk33_tableau  # noqa: E402
+
+GAS = GasModel(1.4)
+
+
+def perturbed_uniform(disc, seed):
+    """Config-5 generator: per C0 node then per trace node."""
+    rng = np.random.default_rng(seed)
+
+    def states(n):
+        rho = rng.uniform(0.9, 1.1, n)
+        vel = rng.uniform(-0.5, 0.5, (n, 3))
+        p = rng.uniform(0.9, 1.1, n)
+        return GAS.conservative(rho, vel, p)
+
+    E, nc = disc.mesh.n_macros, disc.layout.n_unique
+    F, nt = disc.n_faces, disc.layout.n_face_unique
+    u_w = states(E * nc).reshape(E, nc, 5)
+    u_t = states(F * nt).reshape(F, nt, 5)
+    return FieldSet(w=disc.from_conservative(u_w), trace=disc.from_conservative(u_t))
+
+
+def ulp_perturb(a, rng):
+    return a * (1.0 + np.finfo(float).eps * rng.choice([-1.0, 1.0], size=a.shape))
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def operator_case(disc, fields, alpha, offset, ptc, x):
+    stage = StageContext(alpha=alpha, offset=offset, dt=None)
+    res = disc.residuals(fields, stage)
+    lin = disc.jacobian(fields, stage, ptc_weight=ptc)
+    out = dict(
+        r_w=res.r_w, r_trace=res.r_trace,
+        matvec=lin.matvec(x), rhs=lin.condensed_rhs(res),
+        recover=lin.recover(res, x)[0], precond=lin.apply_preconditioner(x),
+        vqs=disc.volume_quad_states(fields),
+    )
+    return out
+
+
+def sensitivity(disc, fields, alpha, offset, ptc, x, base, seed=99):
+    rng = np.random.default_rng(seed)
+    pf = FieldSet(w=ulp_perturb(fields.w, rng), trace=ulp_perturb(fields.trace, rng))
+    pert = operator_case(disc, pf, alpha, offset, ptc, x)
+    return {f"sens_{k}": rel(pert[k], base[k]) for k in base}
+
+
+def save(name, **arrays):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({os.path.getsize(path) / 1e3:.1f} kB)")
+
+
+def meta(disc, flux, formulation, box, n, m, p, periodic=True):
+    return dict(box=np.asarray(box, float), n_per_dim=np.asarray(n), m=m, p=p,
+                flux=flux, formulation=formulation, periodic=np.asarray(periodic))
+
+
+def main():
+    t0 = time.time()
+    tab = dirk33_tableau()
+    d00 = tab.d[0, 0]
+
+    # -- 2D KAT --------------------------------------------------------------
+    box2 = np.array([[0.0, 1.0]] * 2)
+    mesh = build_box_macro_mesh(box2, 1, 1)
+    disc = Discretization(mesh, p=1, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("ec"))
+    u0 = GAS.conservative(1.0, np.array([0.3, -0.2]), 0.7)
+    f = disc.project(lambda x: np.broadcast_to(u0, x.shape[:-1] + (4,)).copy())
+    rng = np.random.default_rng(13)
+    f.w += 0.08 * rng.standard_normal(f.w.shape)
+    f.trace += 0.08 * rng.standard_normal(f.trace.shape)
+    res = disc.residuals(f)
+    save("kat2d_p1_ec", w=f.w, trace=f.trace, r_w=res.r_w, r_trace=res.r_trace,
+         **meta(disc, "ec", "entropy", box2, 1, 1, 1))
+
+    # -- config-5 style sweep ---------------------------------------------------
+    box3 = np.array([[0.0, 1.0]] * 3)
+    for p in (1, 2, 3, 4):
+        fluxes = ("es", "kepes", "ec") if p in (2, 3) else ("es", "kepes")
+        for flux in fluxes:
+            mesh = build_box_macro_mesh(box3, (2, 2, 2), 1)
+            disc = Discretization(mesh, p=p, gas=GAS, formulation="entropy",
+                                  flux=DissipationSpec(flux))
+            seed = 1000 + 10 * p
+            fields = perturbed_uniform(disc, seed)
+            dt = 0.01
+            alpha = d00 / dt
+            offset = -alpha * disc.volume_quad_states(fields)
+            x = np.random.default_rng(seed + 1).standard_normal(fields.trace.shape)
+            out = operator_case(disc, fields, alpha, offset, 1.0, x)
+            sens = sensitivity(disc, fields, alpha, offset, 1.0, x, out)
+            save(f"sweep_k{p}_{flux}", w=fields.w, trace=fields.trace, offset=offset,
+                 alpha=alpha, ptc=1.0, x=x, **out, **sens,
+                 **meta(disc, flux, "entropy", box3, (2, 2, 2), 1, p))
+
+    # -- conservative formulation, LF -------------------------------------------
+    mesh = build_box_macro_mesh(box3, (1, 2, 1), 1)
+    disc = Discretization(mesh, p=2, gas=GAS, formulation="conservative",
+                          flux=DissipationSpec("lf"))
+    fields = perturbed_uniform(disc, 77)
+    x = np.random.default_rng(78).standard_normal(fields.trace.shape)
+    offset = -50.0 * disc.volume_quad_states(fields)
+    out = operator_case(disc, fields, 50.0, offset, 0.5, x)
+    sens = sensitivity(disc, fields, 50.0, offset, 0.5, x, out)
+    save("cons_k2_lf", w=fields.w, trace=fields.trace, offset=offset, alpha=50.0,
+         ptc=0.5, x=x, **out, **sens, **meta(disc, "lf", "conservative", box3, (1, 2, 1), 1, 2))
+
+    # -- free-stream boundary ----------------------------------------------------
+    mesh = build_box_macro_mesh(box3, 2, 1, periodic=(True, False, False))
+    uinf = GAS.conservative(1.0, np.array([0.3, -0.2, 0.1]), 0.7)
+    disc = Discretization(mesh, p=2, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("es"), boundary=FreeStream(uinf))
+    fields = perturbed_uniform(disc, 88)
+    x = np.random.default_rng(89).standard_normal(fields.trace.shape)
+    offset = -30.0 * disc.volume_quad_states(fields)
+    out = operator_case(disc, fields, 30.0, offset, 1.0, x)
+    sens = sensitivity(disc, fields, 30.0, offset, 1.0, x, out)
+    save("fs_k2_es", w=fields.w, trace=fields.trace, offset=offset, alpha=30.0,
+         ptc=1.0, x=x, uinf=uinf, **out, **sens,
+         **meta(disc, "es", "entropy", box3, 2, 1, 2, (True, False, False)))
+
+    # -- config 1 ------------------------------------------------------------
+    box = np.array([[0.0, 10.0]] * 3)
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          angle=0.0, center=(5.0, 5.0), gas=GAS)
+    mesh = build_box_macro_mesh(box, 4, 1)
+    disc = Discretization(mesh, p=2, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("es"))
+    fields = disc.project(vx.initial)
+    dt = 0.01
+    alpha = d00 / dt
+    offset = -alpha * disc.volume_quad_states(fields)
+    x = np.random.default_rng(4242).standard_normal(fields.trace.shape)
+    out = operator_case(disc, fields, alpha, offset, 1.0, x)
+    sens = sensitivity(disc, fields, alpha, offset, 1.0, x, out)
+    save("cfg1_ops", w=fields.w, trace=fields.trace, offset=offset, alpha=alpha,
+         ptc=1.0, x=x, node_coords=disc.node_coords, trace_coords=disc.trace_coords,
+         **out, **sens, **meta(disc, "es", "entropy", box, 4, 1, 2))
+
+    integ = DIRKIntegrator(disc)
+    hist = [disc.integrals(fields)]
+    states = {}
+    cur = fields
+
+    def on_step(step, t, flds, reports):
+        hist.append(disc.integrals(flds))
+        if step in (1, 10):
+            states[step] = (flds.w.copy(), flds.trace.copy())
+
+    integ.run(cur, t_final=10 * dt, dt=dt, on_step=on_step)
+    keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+    hist_arr = np.array([[h[k] for k in keys] for h in hist])
+    rec = integ.records
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"], r["fgmres_iters"],
+                        r["jacobian_builds"]] for r in rec])
+    save("cfg1_steps", w0=fields.w, trace0=fields.trace, w1=states[1][0],
+         trace1=states[1][1], w10=states[10][0], trace10=states[10][1],
+         integrals=hist_arr, newton=newton, dt=dt, tableau_d=tab.d, tableau_e=tab.e)
+    print(f"done in {time.time() - t0:.1f} s")
+
+
+if __name__ == "__main__":
+    sys.exit(main())
