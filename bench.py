@@ -1,0 +1,401 @@
+"""Benchmark of the B200 HDG operator hot path (BASELINE.json metric:
+"HDG operator DoF-applications/s (fp64) + % of HBM/FP64 roofline").
+
+Workload (N=1): BASELINE config 2 -- isentropic vortex on [0,10]^3, n=16
+(24,576 macro-tets, m=1), k=3, ES flux, entropy variables, fp64.  The state
+is the projected initial condition, linearized at stage 1 of the first DIRK
+step (alpha = d00/dt, dt = 0.01, offset = -alpha u_n, ptc_weight = 1).
+
+One step = one pass of the operator the Newton/FGMRES loop applies:
+  residual      K1   DoFs = E*nc*5 + F*nt*5
+  matvec        K3   DoFs = F*nt*5        (condensed trace operator)
+  precond apply K4   DoFs = F*nt*5
+value = sum of DoF-applications / device time of the K timed steps.
+e2e = the same step through the public Discretization / LinearizedSystem
+API with pinned host inputs copied in and results copied out every step.
+
+--impl reference: the CPU oracle port (oracle/, the numpy restatement of the
+reference) timed on the host cores on a bounded sample of the same workload.
+Under torchrun (N>1) every rank runs an independent replica (weak scaling);
+rank 0 prints the JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HDG operator DoF-applications/s (fp64)"
+UNIT = "DoF-applications/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=16, help="cells per axis (config 2: 16)")
+    ap.add_argument("--p", type=int, default=3)
+    ap.add_argument("--flux", default="es")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=4)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def make_problem(n, p, flux, device=None, host_only=False):
+    from paper_2507_22195_b200.cases import IsentropicVortex
+    from paper_2507_22195_b200.gas import GasModel
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+    from paper_2507_22195_b200.time_march import dirk33_tableau
+
+    gas = GasModel(1.4)
+    mesh = build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), n, 1)
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          center=(5.0, 5.0), gas=gas)
+    alpha = float(dirk33_tableau().d[0, 0] / 0.01)
+    return gas, mesh, vx, alpha
+
+
+def dof_units(E, F, nc, nt):
+    return dict(residual=E * nc * 5 + F * nt * 5, matvec=F * nt * 5, precond=F * nt * 5)
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.out = out
+        return False
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = [r.split(",") for r in getattr(self, "out", "").strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[2:6]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(n_sample, p, flux, threads, repeats=None, budget_s=15.0):
+    """Time the CPU oracle (numpy port of the reference) on a bounded sample
+    of the same workload: residual + condensed matvec + precond apply."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle.hdg_oracle import OracleHDG
+    from paper_2507_22195_b200.tables import HDGTables
+
+    gas, mesh, vx, alpha = make_problem(n_sample, p, flux)
+    tab = HDGTables(mesh, p)
+    with threadpool_limits(threads):
+        op = OracleHDG(tab, flux=flux)
+        w = gas.entropy_vars(vx.initial(tab.node_coords))
+        tr = gas.entropy_vars(vx.initial(tab.trace_coords))
+        off = -alpha * op.volume_quad_states(w)
+        lin = op.linearize(w, tr, alpha, 1.0)
+        x = np.random.default_rng(1).standard_normal(tr.shape)
+        units = dof_units(mesh.n_macros, tab.n_faces, tab.layout.n_unique, tab.n_trace)
+        per_step = sum(units.values())
+        t0 = time.perf_counter()
+        steps = 0
+        while True:
+            op.residuals(w, tr, alpha, off)
+            lin.matvec(x)
+            lin.apply_preconditioner(x)
+            steps += 1
+            el = time.perf_counter() - t0
+            if (repeats is not None and steps >= repeats) or (repeats is None and el >= budget_s):
+                break
+    return dict(value=per_step * steps / el, unit=UNIT, cores=threads, kind="port",
+                sample=f"oracle residual+matvec+precond on the n={n_sample} vortex mesh "
+                       f"({mesh.n_macros} macros, k={p}, {flux}), {steps} steps in {el:.1f} s",
+                seconds_per_step=el / steps, dofs_per_step=per_step)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # bounded sample of the workload: the same case on an n=4 sub-mesh
+    base = cpu_baseline(args.cpu_sample_n, args.p, args.flux, threads, repeats=args.warmup)
+    t0 = time.perf_counter()
+    res = cpu_baseline(args.cpu_sample_n, args.p, args.flux, threads, repeats=args.steps)
+    total = time.perf_counter() - t0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * res["seconds_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config2 vortex k={args.p} {args.flux} (sampled n={args.cpu_sample_n})",
+                   "sample_macros": 6 * args.cpu_sample_n ** 3},
+        "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": total, "warmup_value": base["value"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, local_rank, world):
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2507_22195_b200 import _native as N
+    from paper_2507_22195_b200.assembly import Discretization, FieldSet, StageContext
+    from paper_2507_22195_b200.fluxes import DissipationSpec
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        torch.distributed.init_process_group("nccl", device_id=dev)
+
+    gas, mesh, vx, alpha = make_problem(args.n, args.p, args.flux)
+    disc = Discretization(mesh, p=args.p, gas=gas, formulation="entropy",
+                          flux=DissipationSpec(args.flux), device=dev)
+    t = disc.tables
+    E, F, nc, nt = mesh.n_macros, t.n_faces, t.layout.n_unique, t.n_trace
+    nq, nqf = t.phi.shape[0], t.fphi.shape[0]
+    fields = disc.project(vx.initial)
+    u_n = disc.volume_quad_states(fields)
+    offset = (-alpha * u_n).contiguous()
+    stage = StageContext(alpha=alpha, offset=offset)
+    lin = disc.jacobian(fields, stage, ptc_weight=1.0)
+    x = torch.as_tensor(np.random.default_rng(1).standard_normal((F, nt, 5)), device=dev)
+    torch.cuda.synchronize()
+
+    units = dof_units(E, F, nc, nt)
+    per_step = sum(units.values())
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        res = disc.residuals(fields, stage, sync=False)
+        if ev:
+            ev[1].record(stream)
+        y = lin.matvec(x)
+        if ev:
+            ev[2].record(stream)
+        z = lin.apply_preconditioner(x)
+        if ev:
+            ev[3].record(stream)
+        return res, y, z
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    code = N.load().mhdg_status_fetch(disc._ctx, None, N.stream_handle())
+    assert code == 0, "non-admissible benchmark state"
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    launches0 = disc.launch_count
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = disc.launch_count - launches0
+    ms = start.elapsed_time(end)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    k_ms = {
+        "residual": float(np.mean([e[0].elapsed_time(e[1]) for e in evs])),
+        "matvec": float(np.mean([e[1].elapsed_time(e[2]) for e in evs])),
+        "precond": float(np.mean([e[2].elapsed_time(e[3]) for e in evs])),
+    }
+    value = world * per_step * args.steps / (ms * 1e-3)
+
+    # ---- e2e through the public API with pinned host buffers
+    w_h = fields.w.cpu().pin_memory()
+    tr_h = fields.trace.cpu().pin_memory()
+    off_h = offset.cpu().pin_memory()
+    x_h = x.cpu().pin_memory()
+    out_h = [torch.empty(s, dtype=torch.float64).pin_memory()
+             for s in (fields.w.shape, fields.trace.shape, x.shape, x.shape)]
+    h2d = 8 * (w_h.numel() + tr_h.numel() + off_h.numel() + x_h.numel())
+    d2h = 8 * sum(o.numel() for o in out_h)
+
+    def e2e_step():
+        wd = w_h.to(dev, non_blocking=True)
+        td = tr_h.to(dev, non_blocking=True)
+        od = off_h.to(dev, non_blocking=True)
+        xd = x_h.to(dev, non_blocking=True)
+        res = disc.residuals(FieldSet(wd, td), StageContext(alpha=alpha, offset=od), sync=False)
+        y = lin.matvec(xd)
+        z = lin.apply_preconditioner(xd)
+        for o, src in zip(out_h, (res.r_w, res.r_trace, y, z)):
+            o.copy_(src, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e2.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = s2.elapsed_time(e2)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_value = world * per_step * args.e2e_steps / (e2e_ms * 1e-3)
+
+    # ---- roofline of each kernel; dominant one in the headline
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    fp64_peak = N.fp64_probe(local_rank) / 1e3  # TFLOP/s, measured here (FMA loop)
+    NM, NB = 5 * nc, 5 * nt
+    bytes_matvec = 8 * E * NM * NM + 3 * 8 * E * 4 * nqf * 25 + 2 * 8 * F * nt * 5 + \
+        4 * E * 4 * (1 + nt) + 8 * E * 4
+    bytes_precond = 8 * F * NB * NB + 2 * 8 * F * nt * 5
+    # residual flop count (ES): SURVEY 8d formula with T = 20 flop per exp/log/sqrt
+    T = 20
+    nfn = nt
+    flops_res = E * (nq * (10 * nc * 5 + 150 + 2 * T) + 4 * nqf * (8 * nfn * 5 + 190 + 8 * T))
+    bytes_res = 8 * (2 * E * nc * 5 + 2 * F * nt * 5 + E * nq * 5) + 96 * E + 4 * E * 4 * (1 + nt)
+    kern = {
+        "matvec": {"bound": "hbm", "achieved": bytes_matvec / (k_ms["matvec"] * 1e-3) / 1e9,
+                   "peak": hbm_peak, "unit": "GB/s", "algorithmic_bytes": bytes_matvec,
+                   "ms": k_ms["matvec"]},
+        "precond": {"bound": "hbm", "achieved": bytes_precond / (k_ms["precond"] * 1e-3) / 1e9,
+                    "peak": hbm_peak, "unit": "GB/s", "algorithmic_bytes": bytes_precond,
+                    "ms": k_ms["precond"]},
+        "residual": {"bound": "fp64", "achieved": flops_res / (k_ms["residual"] * 1e-3) / 1e12,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "algorithmic_flops": flops_res,
+                     "hbm_gbs": bytes_res / (k_ms["residual"] * 1e-3) / 1e9,
+                     "ms": k_ms["residual"]},
+    }
+    for v in kern.values():
+        v["frac"] = v["achieved"] / v["peak"]
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(dom)
+    except (OSError, ValueError):
+        pass
+    roofline = {"bound": kern[dom]["bound"], "achieved": kern[dom]["achieved"],
+                "peak": kern[dom]["peak"], "unit": kern[dom]["unit"], "frac": kern[dom]["frac"],
+                "traffic": traffic, "kernel": dom,
+                "peak_source": f"{hbm_src} MEASURED_PEAKS.json hbm_gbs" if kern[dom]["bound"] == "hbm"
+                else "measured FP64 FMA probe (mhdg_fp64_probe)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_sample_n, args.p, args.flux, threads=1)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (projected isentropic-vortex IC, seeded x)",
+            "config": {"workload": f"config2 isentropic vortex n={args.n} ({E} macros) k={args.p} "
+                                   f"{args.flux} entropy m=1; step = residual + condensed "
+                                   "matvec + face-block precond",
+                       "macros": E, "faces": F, "dofs_per_step": per_step,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2: S^-1 (%.2f GB) streamed every step"
+                             % (8 * E * NM * NM / 1e9)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "kernels": kern,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "fp64_peak_tflops": fp64_peak,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, local_rank, world = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_b200(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

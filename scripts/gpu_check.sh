@@ -1,0 +1,10 @@
+set -x
+cd $GRAFT_REPO_ROOT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -20
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -30
+python -c "
+import torch, __graft_entry__ as g; g.build()
+from paper_2507_22195_b200 import _native
+for i in range(3): print('fp64 GFLOP/s', _native.fp64_probe(0))
+"

@@ -1,0 +1,63 @@
+"""GPU step-level parity: DIRK(3,3) steps of config 1 (vortex, n=4, p=2, ES,
+dt=0.01) through the device Newton/FGMRES path against the reference's
+converged states and integral history (tests/golden/cfg1_steps.npz).
+
+Targets (BASELINE north_star): converged state per step within 1e-10
+relative; total-entropy history to 1e-12 relative to |int H| and the sign of
+the per-step entropy change identical."""
+
+import numpy as np
+import pytest
+
+from helpers import load_golden, rel
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+
+
+def cfg1_disc():
+    import math
+
+    from paper_2507_22195_b200 import Discretization, DissipationSpec, GasModel
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    mesh = build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), 4, 1)
+    return Discretization(mesh, p=2, gas=GasModel(1.4), formulation="entropy",
+                          flux=DissipationSpec("es"), device="cuda:0")
+
+
+def test_tableau_bits_match_reference():
+    from paper_2507_22195_b200.time_march import dirk33_tableau
+
+    z = load_golden("cfg1_steps")
+    tab = dirk33_tableau()
+    assert np.array_equal(tab.d, z["tableau_d"]) and np.array_equal(tab.e, z["tableau_e"])
+
+
+def test_cfg1_ten_steps(cuda_ok):
+    from paper_2507_22195_b200.assembly import FieldSet
+    from paper_2507_22195_b200.time_march import DIRKIntegrator
+
+    z = load_golden("cfg1_steps")
+    disc = cfg1_disc()
+    fields = FieldSet(z["w0"], z["trace0"])
+    integ = DIRKIntegrator(disc)
+    hist = [disc.integrals(fields)]
+    snaps = {}
+
+    def on_step(step, t, flds, reports):
+        hist.append(disc.integrals(flds))
+        if step in (1, 10):
+            snaps[step] = (flds.w.clone(), flds.trace.clone())
+
+    integ.run(fields, t_final=10 * float(z["dt"]), dt=float(z["dt"]), on_step=on_step)
+    assert rel(snaps[1][0], z["w1"]) <= 1e-10 and rel(snaps[1][1], z["trace1"]) <= 1e-10
+    assert rel(snaps[10][0], z["w10"]) <= 1e-10 and rel(snaps[10][1], z["trace10"]) <= 1e-10
+    got = np.array([[h[k] for k in KEYS] for h in hist])
+    want = z["integrals"]
+    assert np.all(np.abs(got - want) <= 1e-12 * np.maximum(1.0, np.abs(want)))
+    dh_got, dh_want = np.diff(got[:, 0]), np.diff(want[:, 0])
+    assert np.array_equal(np.sign(dh_got), np.sign(dh_want))
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"]] for r in integ.records])
+    assert np.array_equal(newton, z["newton"][:, :3])
