@@ -330,12 +330,11 @@ extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace,
 template <int P, int NT>
 static int launch_condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x,
                             const double* rw, double* y, double* dw, cudaStream_t s) {
-  using D = Dims<P>;
-  size_t smem = ((size_t)4 * D::NQF * D::FS + D::NQF * D::FS + D::NQF + 4 * D::NFN * 5 + 8 * D::NQF * 5 +
-                 2 * D::NM + 4) * 8 + ((size_t)4 * D::NFN + 3 * D::NN + 4 + 4 * D::NFN) * 4;
+  size_t smem = CondSmem<P>::bytes;
   if (set_smem(k_condensed<P, NT>, smem)) return MHDG_CUDA_ERROR;
-  k_condensed<P, NT><<<grid_for(c, c->E, 16), NT, smem, s>>>(c->geo, mode, L->sinv, L->hw, L->hhat, L->hh, x,
-                                                              rw, y, dw);
+  int per_sm = std::max(1, std::min(16, (int)(225 * 1024 / (smem + 1024))));
+  k_condensed<P, NT><<<grid_for(c, c->E, per_sm), NT, smem, s>>>(c->geo, mode, L->sinv, L->hw, L->hhat, L->hh,
+                                                                  x, rw, y, dw);
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;
@@ -345,9 +344,9 @@ static int condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const dou
                      double* y, double* dw, cudaStream_t s) {
   switch (c->p) {
     case 1: return launch_condensed<1, 64>(c, mode, L, x, rw, y, dw, s);
-    case 2: return launch_condensed<2, 64>(c, mode, L, x, rw, y, dw, s);
-    case 3: return launch_condensed<3, 128>(c, mode, L, x, rw, y, dw, s);
-    default: return launch_condensed<4, 192>(c, mode, L, x, rw, y, dw, s);
+    case 2: return launch_condensed<2, 128>(c, mode, L, x, rw, y, dw, s);
+    case 3: return launch_condensed<3, 256>(c, mode, L, x, rw, y, dw, s);
+    default: return launch_condensed<4, 256>(c, mode, L, x, rw, y, dw, s);
   }
 }
 

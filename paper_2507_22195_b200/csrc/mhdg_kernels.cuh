@@ -17,6 +17,7 @@
 // and independent of order (IEEE addition is commutative).
 #pragma once
 #include "mhdg_math.cuh"
+#include "mhdg_tma.cuh"
 
 namespace mhdg {
 
@@ -602,7 +603,24 @@ k_precond_factor(Geo g, const double* __restrict__ hh, double* __restrict__ pinv
 //   mode 0 matvec : y += [hh x - (hw S^-1 (hhat x)) scattered]      (y zeroed)
 //   mode 1 rhs    : y += hw S^-1(-r_w) scattered                    (y zeroed)
 //   mode 2 recover: d_w = S^-1(-r_w - hhat x)
+// HBM-bound: per macro it streams S^-1 (8 NM^2 B) plus the face tensors.
+// STAGE (NM^2*8 <= 80 KB, P <= 3): S^-1 and hw arrive by TMA bulk copies
+// (cp.async.bulk, mbarrier completion).  The next macro's S^-1 is requested
+// as soon as the GEMV has consumed the buffer and its hw as soon as the a3
+// phase has, so the copy overlaps every other phase of the iteration.
+// Otherwise (P = 4) S^-1 is streamed from HBM, 8 independent loads/thread.
 // ===========================================================================
+template <int P>
+struct CondSmem {
+  using D = Dims<P>;
+  static constexpr bool STAGE = D::NM * D::NM * 8 <= 80 * 1024;
+  static constexpr int stage_doubles = STAGE ? (D::NM * D::NM + 4 * D::NQF * 25) : 0;
+  static constexpr int doubles = 2 /*mbarriers*/ + stage_doubles + 4 * D::NQF * D::FS + D::NQF * D::FS +
+                                 D::NQF + 4 * D::NFN * 5 + 3 * 4 * D::NQF * 5 + 2 * D::NM + 4;
+  static constexpr int ints = 4 * D::NFN + 3 * D::NN + 4 + 4 * D::NFN;
+  static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
+};
+
 template <int P, int NT>
 __global__ void __launch_bounds__(NT)
 k_condensed(Geo g, int mode, const double* __restrict__ sinv, const double* __restrict__ hw,
@@ -610,29 +628,52 @@ k_condensed(Geo g, int mode, const double* __restrict__ sinv, const double* __re
             const double* __restrict__ x, const double* __restrict__ r_w, double* __restrict__ y,
             double* __restrict__ d_w) {
   using D = Dims<P>;
+  using CS = CondSmem<P>;
   constexpr int NM = D::NM;
-  extern __shared__ double smem[];
-  double* sPF = smem;                          // 4*NQF*FS
-  double* sFP = sPF + 4 * D::NQF * D::FS;      // NQF*FS
-  double* sFW = sFP + D::NQF * D::FS;          // NQF
-  double* sX = sFW + D::NQF;                   // 4*NFN*5
-  double* sA1 = sX + 4 * D::NFN * 5;           // 4*NQF*5 (hhat x, weighted)
-  double* sA2 = sA1 + 4 * D::NQF * 5;          // 4*NQF*5 (hh x / hw z, weighted)
-  double* sG = sA2 + 4 * D::NQF * 5;           // NM
-  double* sZ = sG + NM;                        // NM
-  double* sAr = sZ + NM;                       // 4
-  int* sRows = (int*)(sAr + 4);                // 4*NFN
-  int* sNF = sRows + 4 * D::NFN;               // 3*NN
-  int* sFid = sNF + 3 * D::NN;                 // 4
-  int* sTid = sFid + 4;                        // 4*NFN
+  constexpr bool STAGE = CS::STAGE;
+  extern __shared__ __align__(16) double smem[];
+  uint64_t* barS = (uint64_t*)smem;                  // S^-1 landed
+  uint64_t* barH = barS + 1;                         // hw landed
+  double* sS = smem + 2;                             // NM*NM (TMA)
+  double* sHW = sS + (STAGE ? NM * NM : 0);          // 4*NQF*25 (TMA)
+  double* sPF = smem + 2 + CS::stage_doubles;        // 4*NQF*FS
+  double* sFP = sPF + 4 * D::NQF * D::FS;            // NQF*FS
+  double* sFW = sFP + D::NQF * D::FS;                // NQF
+  double* sX = sFW + D::NQF;                         // 4*NFN*5
+  double* sXq = sX + 4 * D::NFN * 5;                 // 4*NQF*5
+  double* sA1 = sXq + 4 * D::NQF * 5;                // 4*NQF*5
+  double* sA2 = sA1 + 4 * D::NQF * 5;                // 4*NQF*5
+  double* sG = sA2 + 4 * D::NQF * 5;                 // NM
+  double* sZ = sG + NM;                              // NM
+  double* sAr = sZ + NM;                             // 4
+  int* sRows = (int*)(sAr + 4);                      // 4*NFN
+  int* sNF = sRows + 4 * D::NFN;                     // 3*NN
+  int* sFid = sNF + 3 * D::NN;                       // 4
+  int* sTid = sFid + 4;                              // 4*NFN
   const int tid = threadIdx.x;
   for (int i = tid; i < 4 * D::NQF * D::NFN; i += NT) sPF[(i / D::NFN) * D::FS + i % D::NFN] = g.pf[i];
   for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[(i / D::NFN) * D::FS + i % D::NFN] = g.fphi[i];
   for (int i = tid; i < D::NQF; i += NT) sFW[i] = g.fw[i];
   for (int i = tid; i < 4 * D::NFN; i += NT) sRows[i] = g.rows[i];
   for (int i = tid; i < 3 * D::NN; i += NT) sNF[i] = g.nodef[i];
+  constexpr uint32_t BYTES_S = NM * NM * 8, BYTES_HW = 4 * D::NQF * 25 * 8;
+  if (STAGE && tid == 0) {
+    mbar_init(barS, 1);
+    mbar_init(barH, 1);
+    if (blockIdx.x < g.E) {
+      mbar_expect_tx(barS, BYTES_S);
+      bulk_g2s(sS, sinv + (size_t)blockIdx.x * NM * NM, BYTES_S, barS);
+      if (mode != 2) {
+        mbar_expect_tx(barH, BYTES_HW);
+        bulk_g2s(sHW, hw + (size_t)blockIdx.x * 4 * D::NQF * 25, BYTES_HW, barH);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t phase = 0;
 
   for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    const int e_next = e + gridDim.x;
     __syncthreads();
     if (tid < 4) {
       sFid[tid] = g.fid[e * 4 + tid];
@@ -642,47 +683,47 @@ k_condensed(Geo g, int mode, const double* __restrict__ sinv, const double* __re
     __syncthreads();
     if (mode != 1) {
       for (int i = tid; i < 4 * D::NFN * 5; i += NT) {
-        int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
+        const int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
         sX[i] = x[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s];
       }
       __syncthreads();
-      // a1 = fw * hhat xq ; a2 = fw * hh xq
-      for (int it = tid; it < 4 * D::NQF; it += NT) {
-        const int k = it / D::NQF, q = it % D::NQF;
+      for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
+        const int kq = it / 5, t = it % 5, k = kq / D::NQF, q = kq % D::NQF;
         const double* fp = sFP + q * D::FS;
-        double xq[5] = {0, 0, 0, 0, 0};
-        for (int j = 0; j < D::NFN; ++j) {
-          const double b = fp[j];
+        double acc = 0.0;
 #pragma unroll
-          for (int s = 0; s < 5; ++s) xq[s] += b * sX[(k * D::NFN + j) * 5 + s];
+        for (int j = 0; j < D::NFN; ++j) acc += fp[j] * sX[(k * D::NFN + j) * 5 + t];
+        sXq[it] = acc;
+      }
+      __syncthreads();
+      for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
+        const int kq = it / 5, s = it % 5, k = kq / D::NQF, q = kq % D::NQF;
+        const size_t base = ((size_t)e * 4 * D::NQF + kq) * 25 + s * 5;
+        const double* xq = sXq + kq * 5;
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          a += __ldg(hhat + base + t) * xq[t];
+          if (mode == 0) b += __ldg(hh + base + t) * xq[t];
         }
-        const size_t base = (((size_t)e * 4 + k) * D::NQF + q) * 25;
         const double fwq = sFW[q] * sAr[k];
-#pragma unroll
-        for (int s = 0; s < 5; ++s) {
-          double a = 0.0, b = 0.0;
-#pragma unroll
-          for (int t = 0; t < 5; ++t) {
-            a += hhat[base + s * 5 + t] * xq[t];
-            if (mode == 0) b += hh[base + s * 5 + t] * xq[t];
-          }
-          sA1[it * 5 + s] = fwq * a;
-          if (mode == 0) sA2[it * 5 + s] = fwq * b;
-        }
+        sA1[it] = fwq * a;
+        if (mode == 0) sA2[it] = fwq * b;
       }
       __syncthreads();
     }
-    // right-hand side of the local solve
     for (int o = tid; o < NM; o += NT) {
       const int i = o / 5, s = o % 5;
       double v = 0.0;
       if (mode != 1) {
+#pragma unroll
         for (int c = 0; c < 3; ++c) {
           const int kj = sNF[i * 3 + c];
           if (kj < 0) break;
           const int k = kj / D::NFN, j = kj % D::NFN;
           double acc = 0.0;
-          for (int q = 0; q < D::NQF; ++q) acc += sPF[(k * D::NQF + q) * D::FS + j] * sA1[(k * D::NQF + q) * 5 + s];
+          for (int q = 0; q < D::NQF; ++q)
+            acc += sPF[(k * D::NQF + q) * D::FS + j] * sA1[(k * D::NQF + q) * 5 + s];
           v += acc;
         }
       }
@@ -691,48 +732,83 @@ k_condensed(Geo g, int mode, const double* __restrict__ sinv, const double* __re
       else sG[o] = -r_w[(size_t)e * NM + o] + (-v);
     }
     __syncthreads();
-    // z = S^-1 g : column-major GEMV, rows across threads (coalesced)
-    const double* Si = sinv + (size_t)e * NM * NM;
-    for (int r = tid; r < NM; r += NT) {
-      double acc0 = 0.0, acc1 = 0.0;
-      int c = 0;
-      for (; c + 1 < NM; c += 2) {
-        acc0 += Si[(size_t)c * NM + r] * sG[c];
-        acc1 += Si[(size_t)(c + 1) * NM + r] * sG[c + 1];
+    if (STAGE) {
+      mbar_wait(barS, phase);
+      for (int r = tid; r < NM; r += NT) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 3 < NM; c += 4) {
+          a0 += sS[(c + 0) * NM + r] * sG[c + 0];
+          a1 += sS[(c + 1) * NM + r] * sG[c + 1];
+          a2 += sS[(c + 2) * NM + r] * sG[c + 2];
+          a3 += sS[(c + 3) * NM + r] * sG[c + 3];
+        }
+        for (; c < NM; ++c) a0 += sS[c * NM + r] * sG[c];
+        sZ[r] = (a0 + a1) + (a2 + a3);
       }
-      if (c < NM) acc0 += Si[(size_t)c * NM + r] * sG[c];
-      sZ[r] = acc0 + acc1;
+    } else {
+      const double* Si = sinv + (size_t)e * NM * NM;
+      for (int r = tid; r < NM; r += NT) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = 0;
+        for (; c + 7 < NM; c += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcs(Si + (size_t)(c + u) * NM + r);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u & 3] += v[u] * sG[c + u];
+        }
+        for (; c < NM; ++c) acc[0] += __ldcs(Si + (size_t)c * NM + r) * sG[c];
+        sZ[r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      }
     }
     __syncthreads();
+    if (STAGE && tid == 0 && e_next < g.E) {
+      fence_proxy_async();
+      mbar_expect_tx(barS, BYTES_S);
+      bulk_g2s(sS, sinv + (size_t)e_next * NM * NM, BYTES_S, barS);
+    }
     if (mode == 2) {
+      phase ^= 1u;
       for (int o = tid; o < NM; o += NT) d_w[(size_t)e * NM + o] = sZ[o];
       continue;
     }
-    // a3 = fw * hw zq (overwrites a1)
-    for (int it = tid; it < 4 * D::NQF; it += NT) {
-      const int k = it / D::NQF, q = it % D::NQF;
+    for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
+      const int kq = it / 5, t = it % 5, k = kq / D::NQF, q = kq % D::NQF;
       const double* pf = sPF + (k * D::NQF + q) * D::FS;
-      double zq[5] = {0, 0, 0, 0, 0};
-      for (int j = 0; j < D::NFN; ++j) {
-        const double a = pf[j];
-        const int row = sRows[k * D::NFN + j];
+      double acc = 0.0;
 #pragma unroll
-        for (int s = 0; s < 5; ++s) zq[s] += a * sZ[row * 5 + s];
+      for (int j = 0; j < D::NFN; ++j) acc += pf[j] * sZ[sRows[k * D::NFN + j] * 5 + t];
+      sXq[it] = acc;
+    }
+    if (STAGE) mbar_wait(barH, phase);
+    phase ^= 1u;
+    __syncthreads();
+    for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
+      const int kq = it / 5, s = it % 5, q = kq % D::NQF, k = kq / D::NQF;
+      const double* zq = sXq + kq * 5;
+      double a = 0.0;
+      if (STAGE) {
+        const double* hr = sHW + kq * 25 + s * 5;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) a += hr[t] * zq[t];
+      } else {
+        const size_t base = ((size_t)e * 4 * D::NQF + kq) * 25 + s * 5;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) a += __ldcs(hw + base + t) * zq[t];
       }
-      const size_t base = (((size_t)e * 4 + k) * D::NQF + q) * 25;
-      const double fwq = sFW[q] * sAr[k];
-#pragma unroll
-      for (int s = 0; s < 5; ++s) {
-        double a = 0.0;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) a += hw[base + s * 5 + t] * zq[t];
-        sA1[it * 5 + s] = fwq * a;
-      }
+      sA1[it] = (sFW[q] * sAr[k]) * a;
     }
     __syncthreads();
+    if (STAGE && tid == 0 && e_next < g.E) {
+      fence_proxy_async();
+      mbar_expect_tx(barH, BYTES_HW);
+      bulk_g2s(sHW, hw + (size_t)e_next * 4 * D::NQF * 25, BYTES_HW, barH);
+    }
     for (int o = tid; o < 4 * D::NFN * 5; o += NT) {
       const int k = o / (D::NFN * 5), j = (o / 5) % D::NFN, s = o % 5;
       double a = 0.0, b = 0.0;
+#pragma unroll 4
       for (int q = 0; q < D::NQF; ++q) {
         const double fp = sFP[q * D::FS + j];
         a += fp * sA1[(k * D::NQF + q) * 5 + s];
