@@ -74,6 +74,8 @@ typedef struct {
   const uint8_t* boundary_st; /* (E, n_st)       */
   const int64_t* face_sides;  /* (F, 2) macro*n_st+tile, -1 if none */
   const double* freestream;   /* (5) conservative far-field state or NULL */
+  int n_owned_faces;          /* faces [0, n_owned) get preconditioner blocks;
+                                 0 = all (single partition)                   */
 } mhdg_tables;
 
 typedef struct mhdg_ctx mhdg_ctx;
@@ -108,6 +110,21 @@ int mhdg_status_fetch(mhdg_ctx* ctx, mhdg_status* st, void* stream);
 int mhdg_linearize(mhdg_ctx* ctx, const double* w, const double* trace,
                    double alpha, double ptc_weight, const mhdg_lin_buffers* lin,
                    mhdg_status* st, void* stream);
+
+/* The two halves of mhdg_linearize, for partitioned runs where the
+ * preconditioner blocks of halo faces need the other rank's side:
+ * mhdg_linearize_local builds S^-1, hw, hhat, hh; mhdg_precond_factor
+ * assembles and inverts the owned face blocks, taking remote sides
+ * (face_sides entries <= -2) from hh_remote (n_remote, nqf, 5, 5),
+ * tidx_remote (n_remote, nfn) and area_remote (n_remote) device arrays. */
+int mhdg_linearize_local(mhdg_ctx* ctx, const double* w, const double* trace,
+                         double alpha, double ptc_weight,
+                         const mhdg_lin_buffers* lin, mhdg_status* st,
+                         void* stream);
+int mhdg_precond_factor(mhdg_ctx* ctx, const mhdg_lin_buffers* lin,
+                        int n_remote, const double* hh_remote,
+                        const int32_t* tidx_remote, const double* area_remote,
+                        mhdg_status* st, void* stream);
 
 /* LinearizedSystem.matvec (assembly.py:1131-1143): y = A^ x */
 int mhdg_matvec(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* x,
@@ -153,6 +170,9 @@ int mhdg_scale(mhdg_ctx* ctx, int64_t n, const double* x, double a,
                const double* a_dev, int invert, double* y, void* stream);
 int mhdg_axpby(mhdg_ctx* ctx, int64_t n, double a, const double* x, double b,
                const double* y, double* z, void* stream);
+/* y -= a_dev[0] * x  (distributed MGS step with an all-reduced scalar) */
+int mhdg_axpy_dev(mhdg_ctx* ctx, int64_t n, const double* a_dev,
+                  const double* x, double* y, void* stream);
 
 /* number of library kernels launched since creation (evidence counter) */
 int64_t mhdg_launch_count(const mhdg_ctx* ctx);

@@ -297,8 +297,8 @@ class OracleHDG:
             np.add.at(r_tr, (t.face_id_st[:, k][:, None], t.trace_idx[:, k]), vals)
         return r_w, r_tr
 
-    def linearize(self, w, trace, alpha=0.0, ptc_weight=0.0):
-        return OracleLin(self, w, trace, alpha, ptc_weight)
+    def linearize(self, w, trace, alpha=0.0, ptc_weight=0.0, precond=True):
+        return OracleLin(self, w, trace, alpha, ptc_weight, precond)
 
     def integrals(self, w):
         """Volume integrals of assembly.py:595-620."""
@@ -324,7 +324,7 @@ class OracleLin:
     inviscid): S per macro (LU), face quadrature tensors hw / hhat / ptc,
     face-block preconditioner (Cholesky if symmetric SPD else LU)."""
 
-    def __init__(self, op, w, trace, alpha, ptc_weight):
+    def __init__(self, op, w, trace, alpha, ptc_weight, precond=True):
         t, gas = op.t, op.gas
         self.op = op
         self.shape = trace.shape
@@ -382,6 +382,13 @@ class OracleLin:
                 raise ArithmeticError(f"singular local matrix on macro {e}")
             self.lu.append(lu)
         self.S = Smat
+        if precond:
+            self._build_precond()
+
+    def _build_precond(self):
+        t = self.op.t
+        ns = t.n_s
+        face_w = t.face_w
         # face-block preconditioner (assembly.py:994-1026)
         F, nt, _ = self.shape
         blocks = np.zeros((F, nt, ns, nt, ns))

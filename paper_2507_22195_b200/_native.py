@@ -46,7 +46,7 @@ class Tables(C.Structure):
         ("fphi", dptr), ("facet_wts", dptr), ("face_rows", dptr), ("sub_det", dptr),
         ("sub_inv_jac", dptr), ("face_normals", dptr), ("face_area", dptr),
         ("face_id_st", dptr), ("trace_idx", dptr), ("boundary_st", dptr),
-        ("face_sides", dptr), ("freestream", dptr),
+        ("face_sides", dptr), ("freestream", dptr), ("n_owned_faces", C.c_int),
     ]
 
 
@@ -63,6 +63,11 @@ _SIGS = {
     "mhdg_status_fetch": (C.c_int, [C.c_void_p, C.POINTER(Status), C.c_void_p]),
     "mhdg_linearize": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, C.c_double,
                                  C.POINTER(LinBuffers), C.POINTER(Status), C.c_void_p]),
+    "mhdg_linearize_local": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, C.c_double,
+                                       C.POINTER(LinBuffers), C.POINTER(Status), C.c_void_p]),
+    "mhdg_precond_factor": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), C.c_int, dptr, dptr, dptr,
+                                      C.POINTER(Status), C.c_void_p]),
+    "mhdg_axpy_dev": (C.c_int, [C.c_void_p, C.c_int64, dptr, dptr, dptr, C.c_void_p]),
     "mhdg_matvec": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, C.c_void_p]),
     "mhdg_condensed_rhs": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr,
                                      C.c_void_p]),

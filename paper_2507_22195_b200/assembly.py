@@ -70,9 +70,9 @@ class ResidualSet:
     _disc: object = None
 
     def norm(self):
-        parts = [self.r_w, self.r_trace] + ([self.r_q] if self.r_q is not None else [])
         if self._disc is not None:
-            return math.sqrt(sum(self._disc.vdot(p, p) for p in parts))
+            return self._disc.residual_norm(self)
+        parts = [self.r_w, self.r_trace] + ([self.r_q] if self.r_q is not None else [])
         return math.sqrt(sum(float((p * p).sum()) for p in parts))
 
     def max_abs(self):
@@ -115,7 +115,7 @@ class Discretization:
 
     def __init__(self, mesh, p, gas=None, formulation="entropy", flux=None,
                  viscosity=None, quad_degree=None, boundary=None, supg=False,
-                 device=None):
+                 device=None, tables=None, n_owned_faces=0):
         if formulation not in ("conservative", "entropy"):
             raise InvalidConfig(f"unknown formulation {formulation!r}")
         if supg:
@@ -123,7 +123,7 @@ class Discretization:
         if viscosity is not None:
             raise InvalidConfig("viscous operator (level-1 q condensation) is not on the "
                                 "B200 path yet")
-        if mesh.has_boundary and boundary is None:
+        if tables is None and mesh.has_boundary and boundary is None:
             raise InvalidConfig("mesh has boundary faces, a boundary treatment is required")
         if mesh.dim != 3 or mesh.m != 1:
             raise InvalidConfig("the B200 operator is 3D with m = 1 macro subdivision")
@@ -145,7 +145,8 @@ class Discretization:
         self.boundary = boundary
         self.d = mesh.dim
         self.n_s = self.d + 2
-        self.tables = t = HDGTables(mesh, p, quad_degree)
+        self.tables = t = HDGTables(mesh, p, quad_degree) if tables is None else tables
+        self.n_owned_faces = int(n_owned_faces) or t.n_faces
         self.basis, self.layout = t.basis, t.layout
         self.n_st, self.n_faces = t.n_st, t.n_faces
         self.phi = t.phi
@@ -154,7 +155,7 @@ class Discretization:
         self._keep = []
         tab = N.Tables()
         tab.dim, tab.p, tab.m = 3, p, mesh.m
-        tab.n_macros, tab.n_faces = mesh.n_macros, t.n_faces
+        tab.n_macros, tab.n_faces = t.mesh.n_macros, t.n_faces
         tab.nn, tab.nq = t.phi.shape[1], t.phi.shape[0]
         tab.nfn, tab.nqf = t.fphi.shape[1], t.fphi.shape[0]
         tab.n_st, tab.n_sub = t.n_st, t.layout.n_sub
@@ -183,6 +184,7 @@ class Discretization:
         tab.boundary_st = keep(t.boundary_st, np.uint8)
         tab.face_sides = keep(t.face_sides, np.int64)
         tab.freestream = keep(boundary.state, np.float64) if boundary is not None else None
+        tab.n_owned_faces = int(n_owned_faces)
         err = C.c_int(0)
         with torch.cuda.device(self.device):
             self._ctx = lib.mhdg_create(C.byref(tab), self.device.index, C.byref(err))
@@ -243,6 +245,10 @@ class Discretization:
     def _fields(self, fields):
         return self._dev(fields.w), self._dev(fields.trace)
 
+    def residual_norm(self, res):
+        parts = [res.r_w, res.r_trace] + ([res.r_q] if res.r_q is not None else [])
+        return math.sqrt(sum(self.vdot(p, p) for p in parts))
+
     def vdot(self, x, y):
         """Deterministic device dot product (float)."""
         self._lib.mhdg_dot(self._ctx, x.numel(), N.ptr(x), N.ptr(y), N.ptr(self._scalar),
@@ -289,7 +295,7 @@ class Discretization:
     def volume_quad_states(self, fields):
         torch = _torch()
         w = self._dev(fields.w)
-        E = self.mesh.n_macros
+        E = self.tables.mesh.n_macros
         out = torch.empty((E, 1, self.phi.shape[0], 5), dtype=torch.float64, device=self.device)
         st = N.Status()
         rc = self._lib.mhdg_volume_quad_states(self._ctx, N.ptr(w), N.ptr(out), C.byref(st),

@@ -19,6 +19,7 @@ using namespace mhdg;
 struct mhdg_ctx {
   int device;
   int p, E, F, nn, nq, nfn, nqf;
+  int n_owned;
   int n_sms;
   Geo geo;
   std::vector<void*> allocs;
@@ -87,6 +88,7 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   c->device = device;
   c->p = P; c->E = t->n_macros; c->F = t->n_faces;
   c->nn = NN; c->nq = NQ; c->nfn = NFN; c->nqf = NQF;
+  c->n_owned = t->n_owned_faces > 0 ? t->n_owned_faces : t->n_faces;
   c->launches = 0;
   c->d_scratch = nullptr;
   c->scratch_bytes = 0;
@@ -125,7 +127,7 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   g.fid = upload_i64(c, t->face_id_st, E * 4, err);
   g.tidx = upload_i64(c, t->trace_idx, E * 4 * NFN, err);
   g.bnd = t->boundary_st ? upload(c, t->boundary_st, E * 4, err) : nullptr;
-  g.fsides = upload_i64(c, t->face_sides, F * 2, err);
+  g.fsides = upload_i64(c, t->face_sides, (size_t)c->n_owned * 2, err);
   g.has_uinf = t->freestream != nullptr;
   if (t->freestream)
     for (int s = 0; s < 5; ++s) g.uinf[s] = t->freestream[s];
@@ -272,41 +274,21 @@ static int launch_linearize(mhdg_ctx* c, const double* w, const double* tr, doub
 }
 
 template <int P, int NT>
-static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, cudaStream_t s) {
+static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* hh_rem,
+                                 const int* tidx_rem, const double* area_rem, cudaStream_t s) {
   using D = Dims<P>;
   size_t smem = ((size_t)D::NB * D::NB + D::NQF * 25 + D::NQF * D::NFN + D::NB + D::NQF) * 8 +
                 ((size_t)D::NFN + D::NB + 2) * 4;
   if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;
   int per_sm = std::max(1, std::min(16, (int)(200 * 1024 / smem)));
-  k_precond_factor<P, NT><<<grid_for(c, c->F, per_sm), NT, smem, s>>>(c->geo, L->hh, L->pinv,
-                                                                       c->d_status + 1, c->d_unsym);
+  k_precond_factor<P, NT><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
+      c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;
 }
 
-extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
-                              const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
-  cudaStream_t s = S(stream);
-  CK(cudaSetDevice(c->device));
-  CK(cudaMemsetAsync(c->d_status, 0xff, 2 * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(c->d_unsym, 0, sizeof(int), s));
-  const double weight = alpha + ptc;
-  int rc;
-  switch (c->p) {
-    case 1: rc = launch_linearize<1, 128>(c, w, trace, weight, ptc, L, s); break;
-    case 2: rc = launch_linearize<2, 256>(c, w, trace, weight, ptc, L, s); break;
-    case 3: rc = launch_linearize<3, 256>(c, w, trace, weight, ptc, L, s); break;
-    default: rc = launch_linearize<4, 512>(c, w, trace, weight, ptc, L, s); break;
-  }
-  if (rc) return rc;
-  switch (c->p) {
-    case 1: rc = launch_precond_factor<1, 64>(c, L, s); break;
-    case 2: rc = launch_precond_factor<2, 64>(c, L, s); break;
-    case 3: rc = launch_precond_factor<3, 128>(c, L, s); break;
-    default: rc = launch_precond_factor<4, 128>(c, L, s); break;
-  }
-  if (rc) return rc;
+static int fetch_lin_status(mhdg_ctx* c, mhdg_status* st, cudaStream_t s) {
   unsigned long long keys[2];
   int unsym = 0;
   CK(cudaMemcpyAsync(keys, c->d_status, sizeof(keys), cudaMemcpyDeviceToHost, s));
@@ -322,6 +304,61 @@ extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace,
   }
   if (st) *st = tmp;
   return tmp.code;
+}
+
+static int linearize_local(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
+                           const mhdg_lin_buffers* L, cudaStream_t s) {
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemsetAsync(c->d_status, 0xff, 2 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(c->d_unsym, 0, sizeof(int), s));
+  const double weight = alpha + ptc;
+  switch (c->p) {
+    case 1: return launch_linearize<1, 128>(c, w, trace, weight, ptc, L, s);
+    case 2: return launch_linearize<2, 256>(c, w, trace, weight, ptc, L, s);
+    case 3: return launch_linearize<3, 256>(c, w, trace, weight, ptc, L, s);
+    default: return launch_linearize<4, 512>(c, w, trace, weight, ptc, L, s);
+  }
+}
+
+static int precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* hh_rem, const int* tidx_rem,
+                          const double* area_rem, cudaStream_t s) {
+  switch (c->p) {
+    case 1: return launch_precond_factor<1, 64>(c, L, hh_rem, tidx_rem, area_rem, s);
+    case 2: return launch_precond_factor<2, 64>(c, L, hh_rem, tidx_rem, area_rem, s);
+    case 3: return launch_precond_factor<3, 128>(c, L, hh_rem, tidx_rem, area_rem, s);
+    default: return launch_precond_factor<4, 128>(c, L, hh_rem, tidx_rem, area_rem, s);
+  }
+}
+
+extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
+                              const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
+  cudaStream_t s = S(stream);
+  int rc = linearize_local(c, w, trace, alpha, ptc, L, s);
+  if (rc) return rc;
+  rc = precond_factor(c, L, nullptr, nullptr, nullptr, s);
+  if (rc) return rc;
+  return fetch_lin_status(c, st, s);
+}
+
+extern "C" int mhdg_linearize_local(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
+                                    const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
+  cudaStream_t s = S(stream);
+  int rc = linearize_local(c, w, trace, alpha, ptc, L, s);
+  if (rc) return rc;
+  return fetch_lin_status(c, st, s);
+}
+
+extern "C" int mhdg_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, int n_remote, const double* hh_remote,
+                                   const int32_t* tidx_remote, const double* area_remote, mhdg_status* st,
+                                   void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemsetAsync(c->d_status, 0xff, 2 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(c->d_unsym, 0, sizeof(int), s));
+  (void)n_remote;
+  int rc = precond_factor(c, L, hh_remote, tidx_remote, area_remote, s);
+  if (rc) return rc;
+  return fetch_lin_status(c, st, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -389,10 +426,10 @@ extern "C" int mhdg_precond(mhdg_ctx* c, const mhdg_lin_buffers* L, const double
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
   switch (c->p) {
-    case 1: k_precond_apply<1, 32><<<grid_for(c, c->F, 32), 32, 0, s>>>(c->F, L->pinv, r, z); break;
-    case 2: k_precond_apply<2, 32><<<grid_for(c, c->F, 32), 32, 0, s>>>(c->F, L->pinv, r, z); break;
-    case 3: k_precond_apply<3, 64><<<grid_for(c, c->F, 24), 64, 0, s>>>(c->F, L->pinv, r, z); break;
-    default: k_precond_apply<4, 96><<<grid_for(c, c->F, 16), 96, 0, s>>>(c->F, L->pinv, r, z); break;
+    case 1: k_precond_apply<1, 32><<<grid_for(c, c->n_owned, 32), 32, 0, s>>>(c->n_owned, L->pinv, r, z); break;
+    case 2: k_precond_apply<2, 32><<<grid_for(c, c->n_owned, 32), 32, 0, s>>>(c->n_owned, L->pinv, r, z); break;
+    case 3: k_precond_apply<3, 64><<<grid_for(c, c->n_owned, 24), 64, 0, s>>>(c->n_owned, L->pinv, r, z); break;
+    default: k_precond_apply<4, 96><<<grid_for(c, c->n_owned, 16), 96, 0, s>>>(c->n_owned, L->pinv, r, z); break;
   }
   c->launches++;
   CK(cudaGetLastError());
@@ -625,6 +662,23 @@ __global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, doubl
                         double* __restrict__ z) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     z[i] = a * x[i] + b * y[i];
+}
+
+__global__ void k_axpy_dev(int64_t n, const double* __restrict__ a_dev, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  const double a = a_dev[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = y[i] - a * x[i];
+}
+
+extern "C" int mhdg_axpy_dev(mhdg_ctx* c, int64_t n, const double* a_dev, const double* x, double* y,
+                             void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  k_axpy_dev<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, a_dev, x, y);
+  c->launches++;
+  CK(cudaGetLastError());
+  return MHDG_OK;
 }
 
 extern "C" int mhdg_scale(mhdg_ctx* c, int64_t n, const double* x, double a, const double* a_dev, int invert,

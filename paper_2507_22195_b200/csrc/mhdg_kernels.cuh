@@ -534,8 +534,9 @@ k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trac
 // ===========================================================================
 template <int P, int NT>
 __global__ void __launch_bounds__(NT)
-k_precond_factor(Geo g, const double* __restrict__ hh, double* __restrict__ pinv,
-                 unsigned long long* status, int* n_unsym) {
+k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double* __restrict__ hh_rem,
+                 const int* __restrict__ tidx_rem, const double* __restrict__ area_rem,
+                 double* __restrict__ pinv, unsigned long long* status, int* n_unsym) {
   using D = Dims<P>;
   constexpr int NB = D::NB;
   extern __shared__ double smem[];
@@ -549,17 +550,24 @@ k_precond_factor(Geo g, const double* __restrict__ hh, double* __restrict__ pinv
   int* sFlag = sPerm + NB;               // 2
   const int tid = threadIdx.x;
   for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[i] = g.fphi[i];
-  for (int f = blockIdx.x; f < g.F; f += gridDim.x) {
+  for (int f = blockIdx.x; f < n_faces; f += gridDim.x) {
     __syncthreads();
     for (int i = tid; i < NB * NB; i += NT) A[i] = 0.0;
     for (int side = 0; side < 2; ++side) {
       const int st = g.fsides[f * 2 + side];
-      if (st < 0) continue;
-      const int e = st / 4, k = st % 4;
+      if (st == -1) continue;
       __syncthreads();
-      for (int i = tid; i < D::NQF * 25; i += NT) sHH[i] = hh[((size_t)st * D::NQF) * 25 + i];
-      for (int i = tid; i < D::NFN; i += NT) sT[i] = g.tidx[((size_t)e * 4 + k) * D::NFN + i];
-      for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * g.area[(size_t)e * 4 + k];
+      if (st >= 0) {
+        const int e = st / 4, k = st % 4;
+        for (int i = tid; i < D::NQF * 25; i += NT) sHH[i] = hh[((size_t)st * D::NQF) * 25 + i];
+        for (int i = tid; i < D::NFN; i += NT) sT[i] = g.tidx[((size_t)e * 4 + k) * D::NFN + i];
+        for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * g.area[(size_t)e * 4 + k];
+      } else {  // remote side of a halo face (partitioned runs)
+        const int r = -2 - st;
+        for (int i = tid; i < D::NQF * 25; i += NT) sHH[i] = hh_rem[(size_t)r * D::NQF * 25 + i];
+        for (int i = tid; i < D::NFN; i += NT) sT[i] = tidx_rem[(size_t)r * D::NFN + i];
+        for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * area_rem[r];
+      }
       __syncthreads();
       for (int o = tid; o < D::NFN * D::NFN * 25; o += NT) {
         const int ij = o / 25, stt = o % 25;

@@ -1,0 +1,206 @@
+"""One rank's share of the HDG operator: macro-range
+partition, trace halo exchange around the local device kernels, and
+all-reduced FGMRES inner products.
+
+Per operator:
+  residuals        local kernel -> reduce_partials (owned halo faces get the
+                   neighbour side's partial sum: 0 + a + b, bit-identical to
+                   one device)
+  matvec           fill_ghosts(x) -> local kernel -> reduce_partials
+  condensed_rhs    local partial of -(A_hv S^-1 (-r_w)) -> reduce -> -r^ + that
+  recover          fill_ghosts(d_trace) -> local kernel (macro-local result)
+  precond factor   remote sides of halo faces gathered once per Jacobian build
+  precond apply    face-local on owned faces
+  dots / norms     owned rows only, then all-reduce (SUM)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _native as N
+from .assembly import Discretization, LinearizedSystem, ResidualSet
+from .partition import LocalPartition, TorchDistExchange
+from .tables import HDGTables
+
+
+class PartitionedDiscretization:
+    def __init__(self, mesh, p, rank, world, exchange=None, device=None, full_tables=None,
+                 **kw):
+        full = full_tables if full_tables is not None else HDGTables(mesh, p)
+        self.part = LocalPartition(full, rank, world)
+        self.local = Discretization(mesh, p, device=device, tables=self.part.tables,
+                                    n_owned_faces=self.part.n_owned, **kw)
+        self.exchange = exchange if exchange is not None else TorchDistExchange(self.part)
+        self.rank, self.world = rank, world
+        self.device = self.local.device
+        self.gas, self.formulation = self.local.gas, self.local.formulation
+        self._full = full
+
+    def _dev(self, a):
+        return self.local._dev(a)
+
+    def _fields(self, fields):
+        """Device fields with ghost traces refreshed from their owners (the
+        ghost rows are a cache of the owner's values; updates computed by
+        the solver only carry meaning on owned rows)."""
+        w, tr = self.local._fields(fields)
+        self.exchange.fill_ghosts(tr)
+        fields.w, fields.trace = w, tr
+        return fields
+
+    # -- global reductions ---------------------------------------------------
+    def allreduce(self, values):
+        torch = __import__("torch")
+        t = torch.tensor(values, dtype=torch.float64, device=self.device)
+        self.exchange.allreduce_sum(t)
+        return t.tolist()
+
+    def residual_norm(self, res):
+        nt = self.part.n_owned * res.r_trace.shape[1] * res.r_trace.shape[2]
+        rt = res.r_trace.reshape(-1)[:nt]
+        local = self.local.vdot(res.r_w, res.r_w) + self.local.vdot(rt, rt)
+        return math.sqrt(self.allreduce([local])[0])
+
+    # -- operators -----------------------------------------------------------
+    def residuals(self, fields, stage=None, check=True):
+        res = self.local.residuals(self._fields(fields), stage, check)
+        self.exchange.reduce_partials(res.r_trace)
+        return ResidualSet(res.r_w, res.r_trace, None, _disc=self)
+
+    def jacobian(self, fields, stage=None, ptc_weight=0.0):
+        return PartitionedLinearizedSystem(self, self._fields(fields), stage, ptc_weight)
+
+    def volume_quad_states(self, fields):
+        return self.local.volume_quad_states(fields)
+
+    def to_conservative(self, w, where=""):
+        return self.local.to_conservative(w, where)
+
+    def from_conservative(self, u):
+        return self.local.from_conservative(u)
+
+    def integrals(self, fields):
+        loc = self.local.integrals(fields)
+        keys = list(loc)
+        vals = self.allreduce([loc[k] for k in keys])
+        return dict(zip(keys, vals))
+
+
+class PartitionedLinearizedSystem:
+    def __init__(self, pdisc, fields, stage, ptc_weight):
+        torch = __import__("torch")
+        self.pdisc = pdisc
+        d = pdisc.local
+        self.disc = d
+        self.vectors = DistVectors(pdisc)
+        self.trace_shape = tuple(d._dev(fields.trace).shape)
+        # local linearization without the preconditioner ...
+        self.lin = LinearizedSystem.__new__(LinearizedSystem)
+        lin = self.lin
+        lin.disc, lin.viscous, lin.trace_shape = d, False, self.trace_shape
+        sz = d.lin_sizes
+        for name, n in zip(("sinv", "hw", "hhat", "hh", "pinv"), sz):
+            setattr(lin, name, torch.empty(n, dtype=torch.float64, device=d.device))
+        lin._buf = N.LinBuffers(N.ptr(lin.sinv), N.ptr(lin.hw), N.ptr(lin.hhat), N.ptr(lin.hh),
+                                N.ptr(lin.pinv))
+        w, tr = d._fields(fields)
+        alpha = float(stage.alpha) if stage is not None else 0.0
+        st = N.Status()
+        rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(w), N.ptr(tr), alpha, float(ptc_weight),
+                                         C.byref(lin._buf), C.byref(st), N.stream_handle())
+        N.raise_for(rc, st)
+        # ... then the owned face blocks, with halo sides from the neighbours
+        hh_r, tidx_r, area_r = gather_remote_sides(pdisc, lin)
+        n_rem = 0 if area_r is None else int(area_r.numel())
+        rc = d._lib.mhdg_precond_factor(d._ctx, C.byref(lin._buf), n_rem,
+                                        N.ptr(hh_r), N.ptr(tidx_r), N.ptr(area_r),
+                                        C.byref(st), N.stream_handle())
+        N.raise_for(rc, st)
+
+    def matvec(self, xh):
+        x = self.disc._dev(xh).reshape(self.trace_shape).clone()
+        self.pdisc.exchange.fill_ghosts(x)
+        y = self.lin.matvec(x)
+        self.pdisc.exchange.reduce_partials(y)
+        return y
+
+    def condensed_rhs(self, res):
+        torch = __import__("torch")
+        zero = torch.zeros(self.trace_shape, dtype=torch.float64, device=self.disc.device)
+        part = self.lin.condensed_rhs(ResidualSet(res.r_w, zero))     # = -(local A_hv z)
+        self.pdisc.exchange.reduce_partials(part)
+        return (-self.disc._dev(res.r_trace)) + part
+
+    def recover(self, res, d_trace):
+        x = self.disc._dev(d_trace).reshape(self.trace_shape).clone()
+        self.pdisc.exchange.fill_ghosts(x)
+        return self.lin.recover(res, x)
+
+    def apply_preconditioner(self, r):
+        return self.lin.apply_preconditioner(r)
+
+
+def gather_remote_sides(pdisc, lin):
+    """hh / trace_idx / area of the remote sides of owned halo faces
+    (face_sides entries <= -2); geometry is static, hh comes from the rank
+    owning the other macro."""
+    torch = __import__("torch")
+    part = pdisc.part
+    if part.n_remote_sides == 0:
+        return None, None, None
+    nqf = pdisc.local.tables.fphi.shape[0]
+    hh_r = pdisc.exchange.gather_sides(lin.hh, nqf).contiguous()
+    dev = pdisc.device
+    tidx = torch.as_tensor(part.remote_tidx, device=dev)
+    area = torch.as_tensor(part.remote_area, device=dev)
+    return hh_r, tidx, area
+
+
+class DistVectors:
+    """FGMRES vector operations for one rank: element-wise work on the whole
+    local vector (ghost rows are carried along and never read), inner
+    products on the owned rows only followed by an all-reduce.  MGS therefore
+    needs one all-reduce per basis vector (the reference's MGS order)."""
+
+    def __init__(self, pdisc, inner=None):
+        from .solver import DeviceVectors
+
+        self.inner = inner if inner is not None else DeviceVectors(pdisc.local)
+        self.torch = self.inner.torch
+        self.exchange = pdisc.exchange
+        t = pdisc.local.tables
+        self.n_owned = pdisc.part.n_owned * t.fphi.shape[1] * 5
+        self.h = self.torch.zeros(256, dtype=self.torch.float64, device=pdisc.device)
+
+    def _dot_dev(self, x, y, out):
+        self.inner.dot_into(x[: self.n_owned], y[: self.n_owned], out)
+        self.exchange.allreduce_sum(out)
+
+    def norm(self, x):
+        self._dot_dev(x, x, self.h[0:1])
+        return math.sqrt(float(self.h[0].item()))
+
+    def div_into(self, x, a, out):
+        self.inner.div_into(x, a, out)
+
+    def axpby(self, a, x, b, y, out):
+        self.inner.axpby(a, x, b, y, out)
+
+    def combine(self, Z, k, y, x):
+        self.inner.combine(Z, k, y, x)
+
+    def mgs(self, V, j, w):
+        h = self.h
+        for i in range(j + 1):
+            self._dot_dev(V[i], w, h[i:i + 1])
+            self.inner.axpy_dev(h[i:i + 1], V[i], w)
+        self._dot_dev(w, w, h[j + 1:j + 2])
+        col = h[: j + 2].cpu().numpy().copy()
+        col[j + 1] = math.sqrt(col[j + 1])
+        if col[j + 1] > 1e-300:
+            self.inner.div_into(w, col[j + 1], V[j + 1])
+        return col

@@ -1,0 +1,272 @@
+"""Macro-element partitioning and trace-halo exchange.
+
+Rank g owns a contiguous macro range (cells are x-major, so ranges are x
+slabs).  A skeleton face belongs to the rank of its owner macro (the lower
+macro index, mesh.py:265-279).  Each rank stores the trace of every face
+touching its macros: owned faces first, then ghost faces (owned elsewhere,
+touched by a local macro), both in ascending global face order and in the
+owner's node order, so a face's trace block has the same bytes on every rank.
+
+Exchanges (both sides enumerate the shared faces in ascending global order):
+  reduce_partials : ghost-face partial sums -> owner, added to the owner's
+                    own side (0 + a + b, bit-identical to the single-device
+                    atomic sum because IEEE addition is commutative)
+  fill_ghosts     : owned-face values -> ghost copies (matvec input)
+  gather_sides    : a side's face tensors -> the face owner (preconditioner
+                    blocks of halo faces, once per Jacobian build)
+Transport: `TorchDistExchange` (torch.distributed batched isend/irecv; NCCL
+on GPUs, gloo on CPU) or `LoopbackExchange` (several partitions in one
+process, used to check the partitioned kernels on a single GPU).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from types import SimpleNamespace
+
+import numpy as np
+
+
+def macro_ranges(E, world):
+    bounds = [round(g * E / world) for g in range(world + 1)]
+    return [(bounds[g], bounds[g + 1]) for g in range(world)]
+
+
+@dataclass
+class HaloPlan:
+    """Per-neighbour lists of local face ids (ascending global face id)."""
+
+    owned_shared: dict = field(default_factory=dict)   # rank -> local ids of my faces it touches
+    ghost: dict = field(default_factory=dict)          # rank -> local ids of its faces I touch
+
+
+class LocalPartition:
+    """Local view of the global tables for one rank."""
+
+    def __init__(self, tables, rank, world):
+        self.rank, self.world = rank, world
+        t = tables
+        mesh = t.mesh
+        E = mesh.n_macros
+        ranges = macro_ranges(E, world)
+        self.ranges = ranges
+        lo, hi = ranges[rank]
+        self.macro_lo, self.macro_hi = lo, hi
+        owner_rank = np.searchsorted(np.array([r[1] for r in ranges]), np.arange(E), side="right")
+        self.rank_of_macro = owner_rank
+        skel = mesh.skel
+        own = skel.owner
+        nb = skel.neighbor
+        own_r = owner_rank[own]
+        nb_r = np.where(nb >= 0, owner_rank[np.maximum(nb, 0)], -1)
+        owned = np.nonzero(own_r == rank)[0]
+        ghost = np.nonzero((own_r != rank) & (nb_r == rank))[0]
+        self.global_faces = np.concatenate([owned, ghost])
+        self.n_owned = len(owned)
+        self.n_local_faces = len(self.global_faces)
+        g2l = np.full(len(skel), -1, dtype=np.int64)
+        g2l[self.global_faces] = np.arange(self.n_local_faces)
+        self.g2l = g2l
+        plan = HaloPlan()
+        for h in range(world):
+            if h == rank:
+                continue
+            mine = owned[nb_r[owned] == h]
+            theirs = ghost[own_r[ghost] == h]
+            if len(mine):
+                plan.owned_shared[h] = g2l[mine]
+            if len(theirs):
+                plan.ghost[h] = g2l[theirs]
+        self.plan = plan
+        self.tables = self._local_tables(t, lo, hi, g2l, nb_r, own_r)
+
+    def _local_tables(self, t, lo, hi, g2l, nb_r, own_r):
+        """HDGTables-shaped namespace restricted to this rank."""
+        sl = slice(lo, hi)
+        E_l = hi - lo
+        lt = SimpleNamespace()
+        for name in ("p", "d", "n_s", "basis", "layout", "n_st", "st_face", "st_sub",
+                     "st_subface", "st_face_scatter", "phi_face", "face_rows", "fphi",
+                     "facet_wts", "phi", "dphi", "quad_wts", "domain_volume", "n_trace"):
+            setattr(lt, name, getattr(t, name))
+        lt.sub_det = t.sub_det[sl]
+        lt.sub_inv_jac = t.sub_inv_jac[sl]
+        lt.sub_jac = t.sub_jac[sl]
+        lt.face_normals = t.face_normals[sl]
+        lt.face_area = t.face_area[sl]
+        lt.trace_idx = t.trace_idx[sl]
+        lt.boundary_st = t.boundary_st[sl]
+        lt.side_st = t.side_st[sl]
+        lt.face_id_st = g2l[t.face_id_st[sl]]
+        assert (lt.face_id_st >= 0).all()
+        lt.n_faces = self.n_local_faces
+        lt.vol_w = lt.quad_wts[None, None, :] * lt.sub_det[:, :, None]
+        lt.dphi_phys = np.einsum("qik,eska->esqia", lt.dphi, lt.sub_inv_jac)
+        lt.face_w = lt.facet_wts[None, None, :] * lt.face_area[:, :, None]
+        lt.mesh = SimpleNamespace(n_macros=E_l, dim=t.mesh.dim, m=t.mesh.m)
+        # preconditioner sides of owned faces: local (e*n_st + k) or a remote
+        # side encoded as -2 - (index into the gathered remote-side list)
+        fs = t.face_sides[self.global_faces[: self.n_owned]].copy()
+        remote_rows = []
+        for col in range(2):
+            st = fs[:, col]
+            has = st >= 0
+            e = np.where(has, st // t.n_st, 0)
+            k = np.where(has, st % t.n_st, 0)
+            local = has & (e >= self.macro_lo) & (e < self.macro_hi)
+            remote = has & ~local
+            fs[local, col] = (e[local] - self.macro_lo) * t.n_st + k[local]
+            idx = np.nonzero(remote)[0]
+            fs[remote, col] = -2 - (len(remote_rows) + np.arange(len(idx)))
+            remote_rows.extend(idx.tolist())
+        lt.face_sides = fs
+        self.n_remote_sides = len(remote_rows)
+        # remote sides of owned halo faces: static geometry from the global
+        # tables; hh tensors arrive from the neighbour (gather_sides)
+        rows = np.array(remote_rows, dtype=np.int64)
+        gf = self.global_faces[rows] if len(rows) else rows
+        skel = t.mesh.skel
+        tile_of = np.empty(t.d + 1, dtype=np.int64)
+        tile_of[t.st_face] = np.arange(t.n_st)
+        rem_e = skel.neighbor[gf] if len(rows) else rows
+        rem_k = tile_of[skel.neighbor_face[gf]] if len(rows) else rows
+        self.remote_tidx = np.ascontiguousarray(t.trace_idx[rem_e, rem_k], dtype=np.int32)
+        self.remote_area = np.ascontiguousarray(t.face_area[rem_e, rem_k])
+        remote_of_row = {int(r): i for i, r in enumerate(remote_rows)}
+        self.recv_remote_idx = {h: np.array([remote_of_row[int(f)] for f in ids], dtype=np.int64)
+                                for h, ids in self.plan.owned_shared.items()}
+        # sides I must send: for ghost faces owned by h, my (neighbour) side
+        self.send_sides = {}
+        for h, ids in self.plan.ghost.items():
+            gfs = self.global_faces[ids]
+            e = skel.neighbor[gfs]
+            k = tile_of[skel.neighbor_face[gfs]]
+            self.send_sides[h] = (e - self.macro_lo) * t.n_st + k
+        return lt
+
+    # -- host helpers --------------------------------------------------------
+    def local_fields(self, w, trace):
+        """Slice global numpy fields into the local layout."""
+        return w[self.macro_lo:self.macro_hi], trace[self.global_faces]
+
+    def owned_mask(self):
+        m = np.zeros(self.n_local_faces, dtype=bool)
+        m[: self.n_owned] = True
+        return m
+
+
+class TorchDistExchange:
+    """Halo transport over torch.distributed (NCCL on GPU, gloo on CPU)."""
+
+    def __init__(self, part, group=None):
+        self.part = part
+        self.group = group
+
+    def _exchange(self, sends, recvs):
+        import torch.distributed as dist
+
+        ops = []
+        for h, buf in sends.items():
+            ops.append(dist.P2POp(dist.isend, buf.contiguous(), h, self.group))
+        for h, buf in recvs.items():
+            ops.append(dist.P2POp(dist.irecv, buf, h, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def reduce_partials(self, trace_like):
+        """owner += neighbour partials on shared faces; returns trace_like."""
+        import torch
+
+        plan = self.part.plan
+        sends = {h: trace_like[torch.as_tensor(ids, device=trace_like.device)]
+                 for h, ids in plan.ghost.items()}
+        recvs = {h: torch.empty((len(ids),) + tuple(trace_like.shape[1:]), dtype=trace_like.dtype,
+                                device=trace_like.device) for h, ids in plan.owned_shared.items()}
+        self._exchange(sends, recvs)
+        for h, ids in plan.owned_shared.items():
+            idx = torch.as_tensor(ids, device=trace_like.device)
+            trace_like[idx] = trace_like[idx] + recvs[h]
+        return trace_like
+
+    def fill_ghosts(self, trace_like):
+        import torch
+
+        plan = self.part.plan
+        sends = {h: trace_like[torch.as_tensor(ids, device=trace_like.device)]
+                 for h, ids in plan.owned_shared.items()}
+        recvs = {h: torch.empty((len(ids),) + tuple(trace_like.shape[1:]), dtype=trace_like.dtype,
+                                device=trace_like.device) for h, ids in plan.ghost.items()}
+        self._exchange(sends, recvs)
+        for h, ids in plan.ghost.items():
+            trace_like[torch.as_tensor(ids, device=trace_like.device)] = recvs[h]
+        return trace_like
+
+    def allreduce_sum(self, t):
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def gather_sides(self, hh_local, nqf):
+        """hh tensors of the remote sides of my owned halo faces."""
+        import torch
+
+        part = self.part
+        dev = hh_local.device
+        blocks = hh_local.view(-1, nqf * 25)
+        sends = {h: blocks[torch.as_tensor(st, device=dev)] for h, st in part.send_sides.items()}
+        recvs = {h: torch.empty((len(idx), nqf * 25), dtype=torch.float64, device=dev)
+                 for h, idx in part.recv_remote_idx.items()}
+        self._exchange(sends, recvs)
+        out = torch.empty((part.n_remote_sides, nqf * 25), dtype=torch.float64, device=dev)
+        for h, idx in part.recv_remote_idx.items():
+            out[torch.as_tensor(idx, device=dev)] = recvs[h]
+        return out
+
+
+class LoopbackExchange:
+    """All partitions in one process: exchanges are direct copies.  Used to
+    run the partitioned device kernels on a single GPU against the
+    single-partition result."""
+
+    def __init__(self, parts):
+        self.parts = parts
+
+    def reduce_partials(self, traces):
+        import torch
+
+        recv = {}
+        for g, p in enumerate(self.parts):
+            for h, ids in p.plan.ghost.items():
+                recv[(h, g)] = traces[g][torch.as_tensor(ids, device=traces[g].device)].clone()
+        for (h, g), buf in recv.items():
+            ids = self.parts[h].plan.owned_shared[g]
+            idx = torch.as_tensor(ids, device=traces[h].device)
+            traces[h][idx] = traces[h][idx] + buf.to(traces[h].device)
+        return traces
+
+    def gather_sides(self, hh_locals, nqf):
+        """Remote-side hh tensors for every partition (list in, list out)."""
+        import torch
+
+        outs = []
+        for g, p in enumerate(self.parts):
+            out = torch.empty((p.n_remote_sides, nqf * 25), dtype=torch.float64,
+                              device=hh_locals[g].device)
+            for h, idx in p.recv_remote_idx.items():
+                src = hh_locals[h].view(-1, nqf * 25)[torch.as_tensor(
+                    self.parts[h].send_sides[g], device=hh_locals[h].device)]
+                out[torch.as_tensor(idx, device=out.device)] = src.to(out.device)
+            outs.append(out)
+        return outs
+
+    def fill_ghosts(self, traces):
+        import torch
+
+        for g, p in enumerate(self.parts):
+            for h, ids in p.plan.owned_shared.items():
+                vals = traces[g][torch.as_tensor(ids, device=traces[g].device)]
+                dst = self.parts[h].plan.ghost[g]
+                traces[h][torch.as_tensor(dst, device=traces[h].device)] = vals.to(traces[h].device)
+        return traces

@@ -1,0 +1,177 @@
+"""Partitioned operator, host side: partition structure, and
+world_size-2 gloo runs where each rank evaluates its macro range with the
+CPU oracle and the halo exchange / all-reduce code of the product
+(`partition.TorchDistExchange`, `distributed.DistVectors`, `solver.fgmres`)
+assembles the global result."""
+
+import os
+import socket
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2507_22195_b200.mesh import build_box_macro_mesh
+from paper_2507_22195_b200.partition import LocalPartition, TorchDistExchange
+from paper_2507_22195_b200.tables import HDGTables
+
+
+def small_tables(n=(4, 2, 2), p=2):
+    return HDGTables(build_box_macro_mesh(np.array([[0.0, 1.0]] * 3), n, 1), p)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_partition_structure(world):
+    t = small_tables()
+    parts = [LocalPartition(t, g, world) for g in range(world)]
+    owned = np.concatenate([p.global_faces[: p.n_owned] for p in parts])
+    assert np.array_equal(np.sort(owned), np.arange(t.n_faces))
+    for g, pg in enumerate(parts):
+        lt = pg.tables
+        assert lt.mesh.n_macros == pg.macro_hi - pg.macro_lo
+        assert (lt.face_id_st < pg.n_local_faces).all()
+        # every local side's face is local, with the global id it had
+        glob = t.face_id_st[pg.macro_lo:pg.macro_hi]
+        assert np.array_equal(pg.global_faces[lt.face_id_st], glob)
+        for h, ids in pg.plan.owned_shared.items():
+            ph = parts[h]
+            assert np.array_equal(pg.global_faces[ids], ph.global_faces[ph.plan.ghost[g]])
+            assert len(pg.recv_remote_idx[h]) == len(ph.send_sides[g])
+        assert sum(len(v) for v in pg.recv_remote_idx.values()) == pg.n_remote_sides
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class CPUVectors:
+    """Test double of the device vector kernels (torch CPU ops)."""
+
+    def __init__(self):
+        self.torch = torch
+
+    def dot_into(self, x, y, out):
+        out[0] = torch.dot(x, y)
+
+    def norm(self, x):
+        return float(torch.linalg.vector_norm(x))
+
+    def div_into(self, x, a, out):
+        out.copy_(x / a)
+
+    def axpby(self, a, x, b, y, out):
+        out.copy_(a * x + b * y)
+
+    def axpy_dev(self, a, x, y):
+        y.sub_(a[0] * x)
+
+    def combine(self, Z, k, yv, x):
+        x.add_(torch.from_numpy(np.ascontiguousarray(yv[:k])) @ Z[:k])
+
+    def mgs(self, V, j, w):
+        h = np.zeros(j + 2)
+        for i in range(j + 1):
+            h[i] = float(V[i] @ w)
+            w.sub_(h[i] * V[i])
+        h[j + 1] = float(torch.linalg.vector_norm(w))
+        if h[j + 1] > 1e-300:
+            V[j + 1].copy_(w / h[j + 1])
+        return h
+
+
+def _states(gas, rng, n):
+    return gas.entropy_vars(gas.conservative(rng.uniform(0.9, 1.1, n), rng.uniform(-0.5, 0.5, (n, 3)),
+                                             rng.uniform(0.9, 1.1, n)))
+
+
+def _worker(rank, world, port, flux, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.hdg_oracle import Gas, OracleHDG, fgmres as ofgmres
+        from paper_2507_22195_b200 import solver
+        from paper_2507_22195_b200.distributed import DistVectors
+
+        gas = Gas(1.4)
+        t = small_tables()
+        E, nc, F, nt = t.mesh.n_macros, t.layout.n_unique, t.n_faces, t.n_trace
+        rng = np.random.default_rng(2024)
+        w = _states(gas, rng, E * nc).reshape(E, nc, 5)
+        tr = _states(gas, rng, F * nt).reshape(F, nt, 5)
+        x = rng.standard_normal(tr.shape)
+        full = OracleHDG(t, flux=flux)
+        alpha = 150.0
+        off = -alpha * full.volume_quad_states(w)
+        rw_ref, rt_ref = full.residuals(w, tr, alpha, off)
+        lin_ref = full.linearize(w, tr, alpha, 1.0, precond=False)
+        y_ref = lin_ref.matvec(x)
+
+        part = LocalPartition(t, rank, world)
+        ex = TorchDistExchange(part)
+        lo, hi = part.macro_lo, part.macro_hi
+        op = OracleHDG(part.tables, flux=flux)
+        wl, trl = part.local_fields(w, tr)
+        rw, rt = op.residuals(wl, trl, alpha, off[lo:hi])
+        rt_t = torch.from_numpy(rt.copy())
+        ex.reduce_partials(rt_t)
+        own = part.global_faces[: part.n_owned]
+        ok_res = (np.array_equal(rw, rw_ref[lo:hi])
+                  and np.array_equal(rt_t.numpy()[: part.n_owned], rt_ref[own]))
+        # ghost fill of a matvec input, then the partitioned matvec
+        xl = torch.from_numpy(x[part.global_faces].copy())
+        xl[part.n_owned:] = 1e300
+        ex.fill_ghosts(xl)
+        ok_fill = np.array_equal(xl.numpy(), x[part.global_faces])
+        lin = op.linearize(wl, trl, alpha, 1.0, precond=False)
+        y = torch.from_numpy(lin.matvec(xl.numpy()))
+        ex.reduce_partials(y)
+        err_mv = float(np.abs(y.numpy()[: part.n_owned] - y_ref[own]).max() / np.abs(y_ref).max())
+
+        # distributed FGMRES (product solver + DistVectors, CPU vector double)
+        pdisc = SimpleNamespace(exchange=ex, local=SimpleNamespace(tables=part.tables), part=part,
+                                device=torch.device("cpu"))
+        vec = DistVectors(pdisc, inner=CPUVectors())
+        shape = trl.shape
+
+        def dop(v):
+            v2 = v.view(shape).clone()
+            ex.fill_ghosts(v2)
+            out = torch.from_numpy(lin.matvec(v2.numpy()))
+            ex.reduce_partials(out)
+            return out.view(-1)
+
+        b = torch.from_numpy(x[part.global_faces].copy()).view(-1)
+        res = solver.fgmres(dop, b, rel_tol=1e-8, restart=15, max_iters=60,
+                            raise_on_stagnation=False, vec=vec)
+        xr, it_ref, _, _ = ofgmres(lin_ref.matvec_flat if hasattr(lin_ref, "matvec_flat")
+                                   else (lambda v: lin_ref.matvec(v.reshape(tr.shape)).ravel()),
+                                   x.ravel(), rel_tol=1e-8, restart=15, max_iters=60)
+        xd = res.x.view(shape).numpy()[: part.n_owned]
+        err_x = float(np.abs(xd - xr.reshape(tr.shape)[own]).max() / np.abs(xr).max())
+        results[rank] = (ok_res, ok_fill, err_mv, res.iterations, it_ref, err_x)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("flux", ["es", "kepes"])
+def test_gloo_world2_partitioned_operator_and_fgmres(flux):
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), flux, results), nprocs=world,
+                       join=True, start_method="spawn")
+    for rank in range(world):
+        ok_res, ok_fill, err_mv, it, it_ref, err_x = results[rank]
+        assert ok_res, "partitioned residual must be bit-identical"
+        assert ok_fill
+        assert err_mv <= 1e-14
+        assert it == it_ref
+        assert err_x <= 1e-10
