@@ -178,6 +178,8 @@ int mhdg_axpy_dev(mhdg_ctx* ctx, int64_t n, const double* a_dev,
 int64_t mhdg_launch_count(const mhdg_ctx* ctx);
 /* FP64 FMA throughput probe (roofline denominator), returns GFLOP/s */
 double mhdg_fp64_probe(int device, void* stream);
+/* FP64 tensor-core (mma.sync m8n8k4 f64, SASS DMMA) probe, GFLOP/s */
+double mhdg_dmma_probe(int device, void* stream);
 const char* mhdg_version(void);
 
 #ifdef __cplusplus

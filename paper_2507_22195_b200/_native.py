@@ -87,6 +87,7 @@ _SIGS = {
                              C.c_void_p]),
     "mhdg_launch_count": (C.c_int64, [C.c_void_p]),
     "mhdg_fp64_probe": (C.c_double, [C.c_int, C.c_void_p]),
+    "mhdg_dmma_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_version": (C.c_char_p, []),
 }
 
@@ -157,6 +158,11 @@ def raise_for(code, st=None, context=""):
     if code == 7:
         raise MemoryError(f"device allocation failed {context}")
     raise RuntimeError(f"CUDA error in libmhdg_b200 ({code}) {context}")
+
+
+def dmma_probe(device=0):
+    lib = require_cuda()
+    return float(lib.mhdg_dmma_probe(device, stream_handle()))
 
 
 def fp64_probe(device=0):

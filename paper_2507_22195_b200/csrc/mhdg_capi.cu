@@ -188,30 +188,16 @@ static void decode_status(unsigned long long key, mhdg_status* st, bool admissib
   }
 }
 
-static size_t residual_smem(int P) {
-  auto f = [](int NN, int NQ, int NFN, int NQF) {
-    int QS = 4 * NN + 1, FS = (NFN % 2) ? NFN : NFN + 1;
-    size_t d = (size_t)NQ * QS + 4 * NQF * FS + NQF * FS + NQ + NQF + NN * 5 + 4 * NFN * 5 + NQ * 21 +
-               8 * NQF * 5 + 26;
-    size_t i = 4 * NFN + 3 * NN + 4 + 4 * NFN + 4;
-    return d * 8 + i * 4;
-  };
-  switch (P) {
-    case 1: return f(4, 8, 3, 4);
-    case 2: return f(10, 27, 6, 9);
-    case 3: return f(20, 64, 10, 16);
-    default: return f(35, 125, 15, 25);
-  }
-}
-
-template <int P, int NT>
+template <int P>
 static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int has_stage, double alpha,
                            const double* off, int check, double* rw, double* rt, cudaStream_t s) {
-  size_t smem = residual_smem(P);
-  if (set_smem(k_residual<P, NT>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = std::max(1, (int)(200 * 1024 / smem));
-  k_residual<P, NT><<<grid_for(c, c->E, per_sm), NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check,
-                                                                 rw, rt, c->d_status);
+  using RC = ResCfg<P>;
+  size_t smem = RC::bytes;
+  if (set_smem(k_residual<P>, smem)) return MHDG_CUDA_ERROR;
+  int per_sm = std::max(1, std::min(4, (int)(220 * 1024 / (smem + 1024))));
+  int blocks = std::min((c->E + RC::EB - 1) / RC::EB, c->n_sms * per_sm);
+  k_residual<P><<<std::max(1, blocks), RC::NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check, rw, rt,
+                                                          c->d_status);
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;
@@ -236,10 +222,10 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
   CK(cudaMemsetAsync(r_trace, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   int rc;
   switch (c->p) {
-    case 1: rc = launch_residual<1, 64>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
-    case 2: rc = launch_residual<2, 64>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
-    case 3: rc = launch_residual<3, 128>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
-    default: rc = launch_residual<4, 256>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
+    case 1: rc = launch_residual<1>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
+    case 2: rc = launch_residual<2>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
+    case 3: rc = launch_residual<3>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
+    default: rc = launch_residual<4>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
   }
   if (rc) return rc;
   if (!sync) return MHDG_OK;
@@ -714,6 +700,48 @@ __global__ void k_fp64_probe(int iters, double* out) {
   }
   double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
   if (r == 12345.678) out[0] = r;
+}
+
+__global__ void k_dmma_probe(int iters, double* out) {
+  double a0 = threadIdx.x * 1e-9, b0 = 0.999999;
+  double c[8][2];
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[i][0]), "+d"(c[i][1])
+                   : "d"(a0), "d"(b0));
+  }
+  double r = 0;
+  for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
+  if (r == 12345.678) out[0] = r;
+}
+
+// FP64 tensor-core (DMMA m8n8k4) throughput probe, GFLOP/s
+extern "C" double mhdg_dmma_probe(int device, void* stream) {
+  cudaStream_t s = S(stream);
+  cudaSetDevice(device);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* d = nullptr;
+  cudaMalloc(&d, sizeof(double));
+  const int blocks = sms * 4, threads = 256, iters = 4000;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_dmma_probe<<<blocks, threads, 0, s>>>(iters / 10, d);
+  cudaEventRecord(e0, s);
+  k_dmma_probe<<<blocks, threads, 0, s>>>(iters, d);
+  cudaEventRecord(e1, s);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double flops = 2.0 * 256.0 * 8.0 * (double)iters * blocks * (threads / 32);
+  return flops / (ms * 1e-3) / 1e9;
 }
 
 extern "C" double mhdg_fp64_probe(int device, void* stream) {

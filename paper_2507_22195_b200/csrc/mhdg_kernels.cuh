@@ -100,158 +100,269 @@ __device__ void load_tables(const Geo& g, double* sB, double* sPF, double* sFP, 
 
 // ===========================================================================
 // K1: residual  (assembly.py:459-549, inviscid)
+//
+// Persistent CTAs, EB macros per iteration.  Phases:
+//  1. pointwise: every thread evaluates one face and one volume quadrature
+//     point per macro (balanced), producing the weighted two-point fluxes
+//     H[k][q][s] and the reference-space flux / temporal rows G[q][kk][s]
+//     (kk = 0..2: -vol_w J^-1 F, kk = 3: vol_w (alpha u + offset));
+//  2. contraction, warp-specialized per macro:
+//     DMMA warps: r_w^T (5 x NN) = G^T (5 x 4NQ) . B (4NQ x NN) on the FP64
+//       tensor cores (mma.sync.m8n8k4.f64, SASS DMMA), K split across warps;
+//     face warps: face tests of r_w (phi_face) and the side contributions to
+//       r_trace (fphi), scattered with fp64 atomics (two sides per trace
+//       node on a zeroed output: 0 + a + b, order independent);
+//  3. r_w = volume part + face parts in tile order.
+// The basis table B (NQ x 4 x NN) is read through L1 (__ldg).
 // ===========================================================================
-template <int P, int NT>
-__global__ void __launch_bounds__(NT)
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int P>
+struct ResCfg {
+  using D = Dims<P>;
+  static constexpr int EB = (P >= 4) ? 1 : 2;      // macros per CTA iteration
+  static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per CTA
+  static constexpr int NT = NW * 32;
+  static constexpr int WPM = NW / EB;              // warps per macro
+  static constexpr int DW = WPM / 2;               // DMMA warps per macro (K split)
+  static constexpr int FW = WPM - DW;              // face warps per macro
+  static constexpr int NTILE = (D::NN + 7) / 8;    // DMMA N tiles over nodes
+  static constexpr int GS = 21;                    // G row stride (odd)
+  static constexpr int W_ = D::NN * 5, TR_ = 4 * D::NFN * 5, G_ = D::NQ * GS, H_ = 4 * D::NQF * 5,
+                       FR_ = 4 * D::NFN * 5, VOL_ = DW * D::NN * 5, GEO_ = 26;
+  static constexpr int per_macro = W_ + TR_ + G_ + 2 * H_ + FR_ + VOL_ + GEO_;
+  static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF;
+  static constexpr int per_macro_int = 4 + 4 * D::NFN + 4;
+  static constexpr int table_int = 4 * D::NFN + 3 * D::NN;
+  static constexpr size_t bytes =
+      (size_t)(tables + EB * per_macro) * 8 + (size_t)(table_int + EB * per_macro_int) * 4;
+};
+
+template <int P>
+__global__ void __launch_bounds__(ResCfg<P>::NT, 512 / ResCfg<P>::NT)
 k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace,
            int has_stage, double alpha, const double* __restrict__ offset, int check,
            double* __restrict__ r_w, double* __restrict__ r_tr, unsigned long long* status) {
   using D = Dims<P>;
-  extern __shared__ double smem[];
-  double* sB = smem;
-  double* sPF = sB + D::NQ * D::QS;
-  double* sFP = sPF + 4 * D::NQF * D::FS;
-  double* sQW = sFP + D::NQF * D::FS;
-  double* sFW = sQW + D::NQ;
-  double* sW = sFW + D::NQF;                 // NN*5
-  double* sTR = sW + D::NN * 5;              // 4*NFN*5
-  double* sG = sTR + 4 * D::NFN * 5;         // NQ*GS
-  double* sH = sG + D::NQ * D::GS;           // 4*NQF*5
-  double* sHg = sH + 4 * D::NQF * 5;         // 4*NQF*5
-  double* sGeo = sHg + 4 * D::NQF * 5;       // 1 + 9 + 12 + 4
-  int* sRows = (int*)(sGeo + 26);
-  int* sNF = sRows + 4 * D::NFN;
-  int* sFid = sNF + 3 * D::NN;               // 4
-  int* sTid = sFid + 4;                      // 4*NFN
-  int* sBnd = sTid + 4 * D::NFN;             // 4
-  load_tables<P>(g, sB, sPF, sFP, sQW, sFW, sRows, sNF);
+  using R = ResCfg<P>;
+  constexpr int NT = R::NT, EB = R::EB, NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF;
+  constexpr int GS = R::GS;
+  extern __shared__ __align__(16) double smem[];
+  double* sPF = smem;                              // 4*NQF*FS
+  double* sFP = sPF + 4 * NQF * D::FS;             // NQF*FS
+  double* sQW = sFP + NQF * D::FS;                 // NQ
+  double* sFW = sQW + NQ;                          // NQF
+  double* mb = sFW + NQF;                          // EB * per_macro
+  int* sRows = (int*)(mb + EB * R::per_macro);     // 4*NFN
+  int* sNF = sRows + 4 * NFN;                      // 3*NN
+  int* ib = sNF + 3 * NN;                          // EB * per_macro_int
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
+  for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
+  for (int i = tid; i < NQ; i += NT) sQW[i] = g.qw[i];
+  for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
+  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
+  for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
   const double gam = g.gamma;
-  const int tid = threadIdx.x;
+  const double* __restrict__ Bt = g.B;
 
-  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+  auto W = [&](int m) { return mb + m * R::per_macro; };
+  auto TR = [&](int m) { return W(m) + R::W_; };
+  auto G = [&](int m) { return TR(m) + R::TR_; };
+  auto H = [&](int m) { return G(m) + R::G_; };
+  auto HG = [&](int m) { return H(m) + R::H_; };
+  auto FR = [&](int m) { return HG(m) + R::H_; };
+  auto VOL = [&](int m) { return FR(m) + R::FR_; };
+  auto GEO = [&](int m) { return VOL(m) + R::VOL_; };
+  auto FID = [&](int m) { return ib + m * R::per_macro_int; };
+  auto TID = [&](int m) { return FID(m) + 4; };
+  auto BND = [&](int m) { return TID(m) + 4 * NFN; };
+
+  for (int e0 = blockIdx.x * EB; e0 < g.E; e0 += gridDim.x * EB) {
+    const int nm = min(EB, g.E - e0);
     __syncthreads();
-    for (int i = tid; i < D::NN * 5; i += NT) sW[i] = w[(size_t)e * D::NN * 5 + i];
-    if (tid < 4) {
-      sFid[tid] = g.fid[e * 4 + tid];
-      sBnd[tid] = g.bnd ? g.bnd[e * 4 + tid] : 0;
+    for (int i = tid; i < nm * NN * 5; i += NT) W(i / (NN * 5))[i % (NN * 5)] = w[(size_t)e0 * NN * 5 + i];
+    for (int i = tid; i < nm * 4; i += NT) {
+      const int m = i / 4, k = i % 4, e = e0 + m;
+      FID(m)[k] = g.fid[e * 4 + k];
+      BND(m)[k] = g.bnd ? g.bnd[e * 4 + k] : 0;
     }
-    for (int i = tid; i < 4 * D::NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * D::NFN + i];
-    if (tid == 0) sGeo[0] = g.det[e];
-    if (tid >= 1 && tid < 10) sGeo[tid] = g.invj[(size_t)e * 9 + tid - 1];
-    if (tid >= 10 && tid < 22) sGeo[tid] = g.nrm[(size_t)e * 12 + tid - 10];
-    if (tid >= 22 && tid < 26) sGeo[tid] = g.area[(size_t)e * 4 + tid - 22];
+    for (int i = tid; i < nm * 4 * NFN; i += NT) {
+      const int m = i / (4 * NFN);
+      TID(m)[i % (4 * NFN)] = g.tidx[(size_t)e0 * 4 * NFN + i];
+    }
+    for (int i = tid; i < nm * 26; i += NT) {
+      const int m = i / 26, c = i % 26, e = e0 + m;
+      double v;
+      if (c == 0) v = g.det[e];
+      else if (c < 10) v = g.invj[(size_t)e * 9 + c - 1];
+      else if (c < 22) v = g.nrm[(size_t)e * 12 + c - 10];
+      else v = g.area[(size_t)e * 4 + c - 22];
+      GEO(m)[c] = v;
+    }
     __syncthreads();
-    for (int i = tid; i < 4 * D::NFN * 5; i += NT) {
-      int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
-      sTR[i] = trace[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s];
+    for (int i = tid; i < nm * 4 * NFN * 5; i += NT) {
+      const int m = i / (4 * NFN * 5), r = i % (4 * NFN * 5);
+      const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
+      TR(m)[r] = trace[((size_t)FID(m)[k] * NFN + TID(m)[k * NFN + j]) * 5 + s];
     }
     __syncthreads();
 
-    // ---- pointwise: volume quadrature points and face quadrature points
-    for (int it = tid; it < D::NQ + 4 * D::NQF; it += NT) {
-      if (it < D::NQ) {
-        const int q = it;
-        const double* Bq = sB + q * D::QS + 3 * D::NN;
-        double wq[5] = {0, 0, 0, 0, 0};
-        for (int i = 0; i < D::NN; ++i) {
-          double ph = Bq[i];
+    // ---- 1a. face quadrature points: two-point flux, weighted
+    for (int it = tid; it < nm * 4 * NQF; it += NT) {
+      const int m = it / (4 * NQF), kq = it % (4 * NQF), k = kq / NQF, q = kq % NQF, e = e0 + m;
+      const double* pf = sPF + kq * D::FS;
+      const double* fp = sFP + q * D::FS;
+      const double* sw = W(m);
+      const double* st = TR(m) + k * NFN * 5;
+      double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-          for (int s = 0; s < 5; ++s) wq[s] += ph * sW[i * 5 + s];
-        }
-        double u[5];
-        if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e);
-        if (check && !admissible(u, gam)) report(status, 0, 2, e);
-        double F[5][3];
-        flux(u, gam, F);
-        const double vw = sQW[q] * sGeo[0];
-        double* G = sG + q * D::GS;
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-          const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
-#pragma unroll
-          for (int s = 0; s < 5; ++s) G[kk * 5 + s] = -(vw * ((j0 * F[s][0] + j1 * F[s][1]) + j2 * F[s][2]));
-        }
+      for (int j = 0; j < NFN; ++j) {
+        const double a = pf[j], b = fp[j];
+        const int row = sRows[k * NFN + j];
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
-          double tmp = 0.0;
-          if (has_stage) {
-            tmp = alpha * u[s];
-            if (offset) tmp = tmp + offset[((size_t)e * D::NQ + q) * 5 + s];
-            tmp = vw * tmp;
-          }
-          G[15 + s] = tmp;
+          wq[s] += a * sw[row * 5 + s];
+          whq[s] += b * st[j * 5 + s];
         }
-      } else {
-        const int fi = it - D::NQ;
-        const int k = fi / D::NQF, q = fi % D::NQF;
-        const double* pf = sPF + (k * D::NQF + q) * D::FS;
-        const double* fp = sFP + q * D::FS;
-        double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
-        for (int j = 0; j < D::NFN; ++j) {
-          const double a = pf[j], b = fp[j];
-          const int row = sRows[k * D::NFN + j];
+      }
+      double u[5], uh[5];
+      if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e);
+      if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e);
+      if (check && !admissible(u, gam)) report(status, 1 + k, 2, e);
+      if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e);
+      const double* geo = GEO(m);
+      const double n[3] = {geo[10 + k * 3], geo[11 + k * 3], geo[12 + k * 3]};
+      double fh[5];
+      numerical_flux(g.kind, u, uh, n, gam, fh);
+      const double fwq = sFW[q] * geo[22 + k];
+      double* h = H(m) + kq * 5;
 #pragma unroll
-          for (int s = 0; s < 5; ++s) {
-            wq[s] += a * sW[row * 5 + s];
-            whq[s] += b * sTR[(k * D::NFN + j) * 5 + s];
-          }
+      for (int s = 0; s < 5; ++s) h[s] = fwq * fh[s];
+      if (BND(m)[k] && g.has_uinf) {
+        const double mn[3] = {-n[0], -n[1], -n[2]};
+        double gh[5];
+        numerical_flux(g.kind, g.uinf, uh, mn, gam, gh);
+#pragma unroll
+        for (int s = 0; s < 5; ++s) HG(m)[kq * 5 + s] = fwq * gh[s];
+      }
+    }
+    // ---- 1b. volume quadrature points: reference-space flux + temporal term
+    for (int it = tid; it < nm * NQ; it += NT) {
+      const int m = it / NQ, q = it % NQ, e = e0 + m;
+      const double* ph = Bt + ((size_t)q * 4 + 3) * NN;
+      const double* sw = W(m);
+      double wq[5] = {0, 0, 0, 0, 0};
+#pragma unroll 4
+      for (int i = 0; i < NN; ++i) {
+        const double a = __ldg(ph + i);
+#pragma unroll
+        for (int s = 0; s < 5; ++s) wq[s] += a * sw[i * 5 + s];
+      }
+      double u[5];
+      if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e);
+      if (check && !admissible(u, gam)) report(status, 0, 2, e);
+      double F[5][3];
+      flux(u, gam, F);
+      const double* geo = GEO(m);
+      const double vw = sQW[q] * geo[0];
+      double* gr = G(m) + q * GS;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) {
+        const double j0 = geo[1 + kk * 3], j1 = geo[2 + kk * 3], j2 = geo[3 + kk * 3];
+#pragma unroll
+        for (int s = 0; s < 5; ++s) gr[kk * 5 + s] = -(vw * ((j0 * F[s][0] + j1 * F[s][1]) + j2 * F[s][2]));
+      }
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        double tmp = 0.0;
+        if (has_stage) {
+          tmp = alpha * u[s];
+          if (offset) tmp = tmp + offset[((size_t)e * NQ + q) * 5 + s];
+          tmp = vw * tmp;
         }
-        double u[5], uh[5];
-        if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e);
-        if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e);
-        if (check && !admissible(u, gam)) report(status, 1 + k, 2, e);
-        if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e);
-        const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
-        double fh[5];
-        numerical_flux(g.kind, u, uh, n, gam, fh);
-        const double fwq = sFW[q] * sGeo[22 + k];
-        double* H = sH + (k * D::NQF + q) * 5;
-#pragma unroll
-        for (int s = 0; s < 5; ++s) H[s] = fwq * fh[s];
-        if (sBnd[k] && g.has_uinf) {
-          const double mn[3] = {-n[0], -n[1], -n[2]};
-          double gh[5];
-          numerical_flux(g.kind, g.uinf, uh, mn, gam, gh);
-#pragma unroll
-          for (int s = 0; s < 5; ++s) sHg[(k * D::NQF + q) * 5 + s] = fwq * gh[s];
-        }
+        gr[15 + s] = tmp;
       }
     }
     __syncthreads();
 
-    // ---- contraction to the macro test functions
-    for (int o = tid; o < D::NN * 5; o += NT) {
-      const int i = o / 5, s = o % 5;
-      double av = 0.0, at = 0.0;
-      for (int q = 0; q < D::NQ; ++q) {
-        const double* Bq = sB + q * D::QS + i;
-        const double* G = sG + q * D::GS + s;
-        av += (Bq[0] * G[0] + Bq[D::NN] * G[5]) + Bq[2 * D::NN] * G[10];
-        at += Bq[3 * D::NN] * G[15];
-      }
-      double r = av + at;
+    // ---- 2. contraction, warp-specialized per macro
+    {
+      const int m = warp / R::WPM, role = warp % R::WPM;
+      if (m < nm) {
+        if (role < R::DW) {
+          // DMMA: C[s][i] += sum_k G^T[s][k] B[k][i], k = (q, kk)
+          const int q0 = role * NQ / R::DW, q1 = (role + 1) * NQ / R::DW;
+          const int s_a = lane >> 2, kk = lane & 3;
+          double c[R::NTILE][2];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int kj = sNF[i * 3 + c];
-        if (kj < 0) break;
-        const int k = kj / D::NFN, j = kj % D::NFN;
-        double acc = 0.0;
-        for (int q = 0; q < D::NQF; ++q) acc += sPF[(k * D::NQF + q) * D::FS + j] * sH[(k * D::NQF + q) * 5 + s];
-        r += acc;
+          for (int t = 0; t < R::NTILE; ++t) c[t][0] = c[t][1] = 0.0;
+          const double* gm = G(m);
+          for (int q = q0; q < q1; ++q) {
+            const double a = s_a < 5 ? gm[q * GS + kk * 5 + s_a] : 0.0;
+            const double* brow = Bt + ((size_t)q * 4 + kk) * NN;
+#pragma unroll
+            for (int t = 0; t < R::NTILE; ++t) {
+              const int i = t * 8 + (lane >> 2);
+              const double b = i < NN ? __ldg(brow + i) : 0.0;
+              dmma_8x8x4(c[t], a, b);
+            }
+          }
+          double* vol = VOL(m) + role * NN * 5;
+          const int s_c = lane >> 2;
+          if (s_c < 5) {
+#pragma unroll
+            for (int t = 0; t < R::NTILE; ++t)
+#pragma unroll
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const int i = t * 8 + (lane & 3) * 2 + h2;
+                if (i < NN) vol[i * 5 + s_c] = c[t][h2];
+              }
+          }
+        } else {
+          const int fr = role - R::DW, fl = fr * 32 + lane, fstride = R::FW * 32;
+          const double* hm = H(m);
+          const int* fid = FID(m);
+          const int* tdx = TID(m);
+          const bool bnd_any = g.has_uinf && (BND(m)[0] | BND(m)[1] | BND(m)[2] | BND(m)[3]);
+          for (int o = fl; o < 4 * NFN * 5; o += fstride) {
+            const int k = o / (NFN * 5), j = (o / 5) % NFN, s = o % 5;
+            double a = 0.0, b = 0.0;
+#pragma unroll 4
+            for (int q = 0; q < NQF; ++q) {
+              const double hv = hm[(k * NQF + q) * 5 + s];
+              a += sPF[(k * NQF + q) * D::FS + j] * hv;
+              b += sFP[q * D::FS + j] * hv;
+            }
+            FR(m)[o] = a;
+            if (bnd_any && BND(m)[k]) {
+              double gsum = 0.0;
+              for (int q = 0; q < NQF; ++q) gsum += sFP[q * D::FS + j] * HG(m)[(k * NQF + q) * 5 + s];
+              b += gsum;
+            }
+            atomicAdd(&r_tr[((size_t)fid[k] * NFN + tdx[k * NFN + j]) * 5 + s], b);
+          }
+        }
       }
-      r_w[(size_t)e * D::NN * 5 + o] = r;
     }
-    // ---- side contributions to the trace equation
-    for (int o = tid; o < 4 * D::NFN * 5; o += NT) {
-      const int k = o / (D::NFN * 5), j = (o / 5) % D::NFN, s = o % 5;
-      double acc = 0.0;
-      for (int q = 0; q < D::NQF; ++q) acc += sFP[q * D::FS + j] * sH[(k * D::NQF + q) * 5 + s];
-      if (sBnd[k] && g.has_uinf) {
-        double ag = 0.0;
-        for (int q = 0; q < D::NQF; ++q) ag += sFP[q * D::FS + j] * sHg[(k * D::NQF + q) * 5 + s];
-        acc += ag;
+    __syncthreads();
+    // ---- 3. r_w = volume part + face parts (tile order)
+    for (int o = tid; o < nm * NN * 5; o += NT) {
+      const int m = o / (NN * 5), is = o % (NN * 5), i = is / 5, s = is % 5;
+      double r = VOL(m)[is];
+#pragma unroll
+      for (int d2 = 1; d2 < R::DW; ++d2) r += VOL(m)[d2 * NN * 5 + is];
+#pragma unroll
+      for (int c2 = 0; c2 < 3; ++c2) {
+        const int kj = sNF[i * 3 + c2];
+        if (kj < 0) break;
+        r += FR(m)[kj * 5 + s];
       }
-      atomicAdd(&r_tr[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s], acc);
+      r_w[(size_t)e0 * NN * 5 + o] = r;
     }
   }
 }
