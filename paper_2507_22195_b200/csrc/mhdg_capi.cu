@@ -29,6 +29,8 @@ struct mhdg_ctx {
   double* d_scratch;   // P = 4 Gauss-Jordan scratch (lazy)
   size_t scratch_bytes;
   double* d_tmp_trace; // F*nt*5 workspace
+  double* d_gbuf;      // E*nm local right-hand sides (condensed operator)
+  double* d_zbuf;      // E*nm local solutions
   int64_t launches;
 };
 
@@ -135,6 +137,8 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   c->d_unsym = (int*)dalloc(c, sizeof(int) * 4, err);
   c->d_partial = (double*)dalloc(c, sizeof(double) * (2 * RED_BLOCKS * 5 + 64), err);
   c->d_tmp_trace = (double*)dalloc(c, sizeof(double) * F * NFN * 5, err);
+  c->d_gbuf = (double*)dalloc(c, sizeof(double) * E * NN * 5, err);
+  c->d_zbuf = (double*)dalloc(c, sizeof(double) * E * NN * 5, err);
   if (*err != MHDG_OK) {
     mhdg_destroy(c);
     return nullptr;
@@ -172,6 +176,14 @@ static int grid_for(mhdg_ctx* c, int items, int per_sm) {
   return std::max(1, std::min(items, c->n_sms * per_sm));
 }
 
+// resident CTAs per SM for a persistent kernel (registers, smem, threads)
+template <class K>
+static int occ(K kernel, int threads, size_t smem, int cap = 32) {
+  int n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess || n < 1) n = 1;
+  return std::min(n, cap);
+}
+
 static void decode_status(unsigned long long key, mhdg_status* st, bool admissibility) {
   if (key == ~0ull) return;
   const int code = (int)(key >> 40);
@@ -194,7 +206,7 @@ static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int h
   using RC = ResCfg<P>;
   size_t smem = RC::bytes;
   if (set_smem(k_residual<P>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = std::max(1, std::min(4, (int)(220 * 1024 / (smem + 1024))));
+  int per_sm = occ(k_residual<P>, RC::NT, smem);
   int blocks = std::min((c->E + RC::EB - 1) / RC::EB, c->n_sms * per_sm);
   k_residual<P><<<std::max(1, blocks), RC::NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check, rw, rt,
                                                           c->d_status);
@@ -241,7 +253,7 @@ static int launch_linearize(mhdg_ctx* c, const double* w, const double* tr, doub
   using LS = LinSmem<P>;
   size_t smem = LS::bytes;
   if (set_smem(k_linearize<P, NT>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = std::max(1, (int)(220 * 1024 / smem));
+  int per_sm = occ(k_linearize<P, NT>, NT, smem);
   int grid = grid_for(c, c->E, per_sm);
   if (!LS::S_IN_SMEM) {
     size_t need = (size_t)grid * Dims<P>::NM * Dims<P>::NM * sizeof(double);
@@ -266,7 +278,7 @@ static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
   size_t smem = ((size_t)D::NB * D::NB + D::NQF * 25 + D::NQF * D::NFN + D::NB + D::NQF) * 8 +
                 ((size_t)D::NFN + D::NB + 2) * 4;
   if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = std::max(1, std::min(16, (int)(200 * 1024 / smem)));
+  int per_sm = occ(k_precond_factor<P, NT>, NT, smem);
   k_precond_factor<P, NT><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
       c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
   c->launches++;
@@ -350,15 +362,30 @@ extern "C" int mhdg_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, int n
 // ---------------------------------------------------------------------------
 // condensed operator
 // ---------------------------------------------------------------------------
-template <int P, int NT>
-static int launch_condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x,
-                            const double* rw, double* y, double* dw, cudaStream_t s) {
-  size_t smem = CondSmem<P>::bytes;
-  if (set_smem(k_condensed<P, NT>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = std::max(1, std::min(16, (int)(225 * 1024 / (smem + 1024))));
-  k_condensed<P, NT><<<grid_for(c, c->E, per_sm), NT, smem, s>>>(c->geo, mode, L->sinv, L->hw, L->hhat, L->hh,
-                                                                  x, rw, y, dw);
+template <int P>
+static int condensed_split(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
+                           double* y, double* dw, cudaStream_t s) {
+  using D = Dims<P>;
+  constexpr int NT = P >= 3 ? 256 : 128;
+  const size_t fsm = FacePipe<P, NT>::bytes;
+  if (set_smem(k_face_pipe<P, NT, 0>, fsm) || set_smem(k_face_pipe<P, NT, 1>, fsm)) return MHDG_CUDA_ERROR;
+  const int per_in = occ(k_face_pipe<P, NT, 0>, NT, fsm), per_out = occ(k_face_pipe<P, NT, 1>, NT, fsm);
+  double* gbuf = c->d_gbuf;
+  double* zbuf = (mode == 2) ? dw : c->d_zbuf;
+  if (mode != 1) {
+    k_face_pipe<P, NT, 0><<<grid_for(c, c->E, per_in), NT, fsm, s>>>(c->geo, mode, L->hhat, nullptr, x, nullptr,
+                                                                       rw, gbuf);
+    c->launches++;
+  }
+  constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
+  k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(c->E, L->sinv, mode == 1 ? rw : gbuf,
+                                                                 mode == 1, zbuf);
   c->launches++;
+  if (mode != 2) {
+    k_face_pipe<P, NT, 1><<<grid_for(c, c->E, per_out), NT, fsm, s>>>(c->geo, mode, L->hw, L->hh, x, zbuf,
+                                                                       nullptr, y);
+    c->launches++;
+  }
   CK(cudaGetLastError());
   return MHDG_OK;
 }
@@ -366,10 +393,10 @@ static int launch_condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, co
 static int condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
                      double* y, double* dw, cudaStream_t s) {
   switch (c->p) {
-    case 1: return launch_condensed<1, 64>(c, mode, L, x, rw, y, dw, s);
-    case 2: return launch_condensed<2, 128>(c, mode, L, x, rw, y, dw, s);
-    case 3: return launch_condensed<3, 256>(c, mode, L, x, rw, y, dw, s);
-    default: return launch_condensed<4, 256>(c, mode, L, x, rw, y, dw, s);
+    case 1: return condensed_split<1>(c, mode, L, x, rw, y, dw, s);
+    case 2: return condensed_split<2>(c, mode, L, x, rw, y, dw, s);
+    case 3: return condensed_split<3>(c, mode, L, x, rw, y, dw, s);
+    default: return condensed_split<4>(c, mode, L, x, rw, y, dw, s);
   }
 }
 

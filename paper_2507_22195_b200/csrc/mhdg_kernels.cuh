@@ -718,222 +718,277 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
 }
 
 // ===========================================================================
-// K3 / K6: condensed matvec, condensed rhs, recovery  (assembly.py:1028-1173)
-//   mode 0 matvec : y += [hh x - (hw S^-1 (hhat x)) scattered]      (y zeroed)
-//   mode 1 rhs    : y += hw S^-1(-r_w) scattered                    (y zeroed)
-//   mode 2 recover: d_w = S^-1(-r_w - hhat x)
-// HBM-bound: per macro it streams S^-1 (8 NM^2 B) plus the face tensors.
-// STAGE (NM^2*8 <= 80 KB, P <= 3): S^-1 and hw arrive by TMA bulk copies
-// (cp.async.bulk, mbarrier completion).  The next macro's S^-1 is requested
-// as soon as the GEMV has consumed the buffer and its hw as soon as the a3
-// phase has, so the copy overlaps every other phase of the iteration.
-// Otherwise (P = 4) S^-1 is streamed from HBM, 8 independent loads/thread.
+// K3 / K6 as three streaming kernels (the operator is HBM-bound; splitting
+// costs ~3% extra traffic -- g and z round trips -- and lets every kernel
+// run many independent CTAs per SM):
+//   k_face_in  : g = -(A_vh x) [matvec] or -r_w - A_vh x [recover]
+//                (hhat at face quadrature points, tested with phi_face)
+//   k_local_solve: z = S^-1 g, batched column-major GEMV (rhs: g = -r_w)
+//   k_face_out : y += A_hh x [matvec] + A_hv z, scattered to the trace with
+//                fp64 atomics (two sides per node on a zeroed output)
 // ===========================================================================
-template <int P>
-struct CondSmem {
+// z_e = S_e^-1 g_e (column-major S^-1); neg: g = -gin (condensed rhs)
+template <int NM, int NT>
+__global__ void __launch_bounds__(NT)
+k_local_solve(int E, const double* __restrict__ sinv, const double* __restrict__ gin, int neg,
+              double* __restrict__ z) {
+  __shared__ double sg[NM];
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < NM; i += NT) sg[i] = neg ? -gin[(size_t)e * NM + i] : gin[(size_t)e * NM + i];
+    __syncthreads();
+    const double* A = sinv + (size_t)e * NM * NM;
+    for (int r = threadIdx.x; r < NM; r += NT) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int c = 0;
+      for (; c + 3 < NM; c += 4) {
+        a0 += __ldcs(A + (size_t)(c + 0) * NM + r) * sg[c + 0];
+        a1 += __ldcs(A + (size_t)(c + 1) * NM + r) * sg[c + 1];
+        a2 += __ldcs(A + (size_t)(c + 2) * NM + r) * sg[c + 2];
+        a3 += __ldcs(A + (size_t)(c + 3) * NM + r) * sg[c + 3];
+      }
+      for (; c < NM; ++c) a0 += __ldcs(A + (size_t)c * NM + r) * sg[c];
+      z[(size_t)e * NM + r] = (a0 + a1) + (a2 + a3);
+    }
+  }
+}
+
+// Software-pipelined face kernels: while macro e is computed from shared
+// memory, every thread already holds in registers its share of macro
+// e+G's face tensors and trace values (G = grid size), and the metadata
+// (face ids, trace permutations, areas) of macro e+2G -- so none of the
+// three dependent global round trips sits on the critical path.
+template <int P, int NT>
+struct FacePipe {
   using D = Dims<P>;
-  static constexpr bool STAGE = D::NM * D::NM * 8 <= 80 * 1024;
-  static constexpr int stage_doubles = STAGE ? (D::NM * D::NM + 4 * D::NQF * 25) : 0;
-  static constexpr int doubles = 2 /*mbarriers*/ + stage_doubles + 4 * D::NQF * D::FS + D::NQF * D::FS +
-                                 D::NQF + 4 * D::NFN * 5 + 3 * 4 * D::NQF * 5 + 2 * D::NM + 4;
-  static constexpr int ints = 4 * D::NFN + 3 * D::NN + 4 + 4 * D::NFN;
+  static constexpr int NI = 4 * D::NQF;
+  static constexpr int NTEN = NI * 25;
+  static constexpr int NX = 4 * D::NFN * 5;
+  static constexpr int TPT = (NTEN + NT - 1) / NT;   // tensor doubles / thread
+  static constexpr int XPT = (NX + NT - 1) / NT;
+  static constexpr int ZPT = (D::NM + NT - 1) / NT;
+  static constexpr int META = 4 + 4 * D::NFN;        // ints: fid, tidx
+  static constexpr int MPT = (META + 4 + NT - 1) / NT;
+  static constexpr int doubles = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQF + NX + 2 * NTEN + D::NM +
+                                 4 * NI * 5 + 3 * 4;
+  static constexpr int ints = 4 * D::NFN + 3 * D::NN + 3 * META;
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
 };
 
-template <int P, int NT>
+template <int P, int NT, int MODE>   // MODE 0: face_in (A_vh x), 1: face_out (A_hh x + A_hv z)
 __global__ void __launch_bounds__(NT)
-k_condensed(Geo g, int mode, const double* __restrict__ sinv, const double* __restrict__ hw,
-            const double* __restrict__ hhat, const double* __restrict__ hh,
-            const double* __restrict__ x, const double* __restrict__ r_w, double* __restrict__ y,
-            double* __restrict__ d_w) {
+k_face_pipe(Geo g, int mode, const double* __restrict__ tenA, const double* __restrict__ tenB,
+            const double* __restrict__ x, const double* __restrict__ zin, const double* __restrict__ r_w,
+            double* __restrict__ out) {
   using D = Dims<P>;
-  using CS = CondSmem<P>;
-  constexpr int NM = D::NM;
-  constexpr bool STAGE = CS::STAGE;
+  using FP = FacePipe<P, NT>;
+  constexpr int NM = D::NM, NFN = D::NFN, NQF = D::NQF, NN = D::NN, NI = FP::NI, NTEN = FP::NTEN,
+                NX = FP::NX, META = FP::META;
+  // face_in : tenA = hhat; needs x.              out = g (E, NM)
+  // face_out: tenA = hw (z side), tenB = hh (x side, matvec only); out = y
+  const bool use_x = (MODE == 0) || mode == 0;
+  const bool use_b = (MODE == 1) && mode == 0;
   extern __shared__ __align__(16) double smem[];
-  uint64_t* barS = (uint64_t*)smem;                  // S^-1 landed
-  uint64_t* barH = barS + 1;                         // hw landed
-  double* sS = smem + 2;                             // NM*NM (TMA)
-  double* sHW = sS + (STAGE ? NM * NM : 0);          // 4*NQF*25 (TMA)
-  double* sPF = smem + 2 + CS::stage_doubles;        // 4*NQF*FS
-  double* sFP = sPF + 4 * D::NQF * D::FS;            // NQF*FS
-  double* sFW = sFP + D::NQF * D::FS;                // NQF
-  double* sX = sFW + D::NQF;                         // 4*NFN*5
-  double* sXq = sX + 4 * D::NFN * 5;                 // 4*NQF*5
-  double* sA1 = sXq + 4 * D::NQF * 5;                // 4*NQF*5
-  double* sA2 = sA1 + 4 * D::NQF * 5;                // 4*NQF*5
-  double* sG = sA2 + 4 * D::NQF * 5;                 // NM
-  double* sZ = sG + NM;                              // NM
-  double* sAr = sZ + NM;                             // 4
-  int* sRows = (int*)(sAr + 4);                      // 4*NFN
-  int* sNF = sRows + 4 * D::NFN;                     // 3*NN
-  int* sFid = sNF + 3 * D::NN;                       // 4
-  int* sTid = sFid + 4;                              // 4*NFN
+  double* sPF = smem;
+  double* sFP = sPF + 4 * NQF * D::FS;
+  double* sFW = sFP + NQF * D::FS;
+  double* sX = sFW + NQF;          // NX
+  double* sTA = sX + NX;           // NTEN
+  double* sTB = sTA + NTEN;        // NTEN
+  double* sZ = sTB + NTEN;         // NM
+  double* sQ1 = sZ + NM;           // NI*5
+  double* sQ2 = sQ1 + NI * 5;      // NI*5
+  double* sQ3 = sQ2 + NI * 5;      // NI*5
+  double* sQ4 = sQ3 + NI * 5;      // NI*5
+  double* sAr = sQ4 + NI * 5;      // 3 x 4
+  int* sRows = (int*)(sAr + 12);
+  int* sNF = sRows + 4 * NFN;
+  int* sMeta = sNF + 3 * NN;       // 3 x META
   const int tid = threadIdx.x;
-  for (int i = tid; i < 4 * D::NQF * D::NFN; i += NT) sPF[(i / D::NFN) * D::FS + i % D::NFN] = g.pf[i];
-  for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[(i / D::NFN) * D::FS + i % D::NFN] = g.fphi[i];
-  for (int i = tid; i < D::NQF; i += NT) sFW[i] = g.fw[i];
-  for (int i = tid; i < 4 * D::NFN; i += NT) sRows[i] = g.rows[i];
-  for (int i = tid; i < 3 * D::NN; i += NT) sNF[i] = g.nodef[i];
-  constexpr uint32_t BYTES_S = NM * NM * 8, BYTES_HW = 4 * D::NQF * 25 * 8;
-  if (STAGE && tid == 0) {
-    mbar_init(barS, 1);
-    mbar_init(barH, 1);
-    if (blockIdx.x < g.E) {
-      mbar_expect_tx(barS, BYTES_S);
-      bulk_g2s(sS, sinv + (size_t)blockIdx.x * NM * NM, BYTES_S, barS);
-      if (mode != 2) {
-        mbar_expect_tx(barH, BYTES_HW);
-        bulk_g2s(sHW, hw + (size_t)blockIdx.x * 4 * D::NQF * 25, BYTES_HW, barH);
+  for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
+  for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
+  for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
+  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
+  for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
+  const int G = gridDim.x;
+  // metadata element i of macro e: i < 4 fid, < META tidx, else area (double)
+  auto meta_load = [&](int e, int i, int& iv, double& dv) {
+    if (i < 4) iv = g.fid[e * 4 + i];
+    else if (i < META) iv = g.tidx[(size_t)e * 4 * NFN + i - 4];
+    else if (i < META + 4) dv = g.area[(size_t)e * 4 + i - META];
+  };
+  auto meta_store = [&](int slot, int i, int iv, double dv) {
+    if (i < META) sMeta[slot * META + i] = iv;
+    else if (i < META + 4) sAr[slot * 4 + i - META] = dv;
+  };
+  // prologue: metadata of e0 and e0+G in slots 0, 1
+  const int e0 = blockIdx.x;
+  for (int c = 0; c < 2; ++c) {
+    const int e = e0 + c * G;
+    if (e < g.E)
+      for (int i = tid; i < META + 4; i += NT) {
+        int iv = 0;
+        double dv = 0.0;
+        meta_load(e, i, iv, dv);
+        meta_store(c, i, iv, dv);
       }
-    }
   }
   __syncthreads();
-  uint32_t phase = 0;
-
-  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
-    const int e_next = e + gridDim.x;
-    __syncthreads();
-    if (tid < 4) {
-      sFid[tid] = g.fid[e * 4 + tid];
-      sAr[tid] = g.area[(size_t)e * 4 + tid];
-    }
-    for (int i = tid; i < 4 * D::NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * D::NFN + i];
-    __syncthreads();
-    if (mode != 1) {
-      for (int i = tid; i < 4 * D::NFN * 5; i += NT) {
-        const int k = i / (D::NFN * 5), j = (i / 5) % D::NFN, s = i % 5;
-        sX[i] = x[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s];
+  double rA[FP::TPT], rB[FP::TPT], rX[FP::XPT], rZ[FP::ZPT], rMd[FP::MPT];
+  int rMi[FP::MPT];
+  auto prefetch = [&](int e, int slot) {  // tensors / x / z of macro e (meta in slot)
+    const int* mt = sMeta + slot * META;
+#pragma unroll
+    for (int c = 0; c < FP::TPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < NTEN) {
+        rA[c] = __ldcs(tenA + (size_t)e * NTEN + i);
+        if (use_b) rB[c] = __ldcs(tenB + (size_t)e * NTEN + i);
       }
-      __syncthreads();
-      for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
-        const int kq = it / 5, t = it % 5, k = kq / D::NQF, q = kq % D::NQF;
+    }
+    if (use_x) {
+#pragma unroll
+      for (int c = 0; c < FP::XPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < NX) {
+          const int k = i / (NFN * 5), j = (i / 5) % NFN, s = i % 5;
+          rX[c] = x[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s];
+        }
+      }
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int c = 0; c < FP::ZPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < NM) rZ[c] = zin[(size_t)e * NM + i];
+      }
+    }
+  };
+  if (e0 < g.E) prefetch(e0, 0);
+  int slot = 0;
+  for (int e = e0; e < g.E; e += G, slot = (slot + 1) % 3) {
+    const int e1 = e + G, e2 = e + 2 * G;
+    const int s1 = (slot + 1) % 3, s2 = (slot + 2) % 3;
+    __syncthreads();   // previous macro's compute finished with the buffers
+#pragma unroll
+    for (int c = 0; c < FP::TPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < NTEN) {
+        sTA[i] = rA[c];
+        if (use_b) sTB[i] = rB[c];
+      }
+    }
+    if (use_x) {
+#pragma unroll
+      for (int c = 0; c < FP::XPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < NX) sX[i] = rX[c];
+      }
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int c = 0; c < FP::ZPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < NM) sZ[i] = rZ[c];
+      }
+    }
+    __syncthreads();
+    // requests for the next macros (consumed one iteration later)
+    if (e1 < g.E) prefetch(e1, s1);
+    if (e2 < g.E) {
+#pragma unroll
+      for (int c = 0; c < FP::MPT; ++c) {
+        const int i = tid + c * NT;
+        rMi[c] = 0;
+        rMd[c] = 0.0;
+        if (i < META + 4) meta_load(e2, i, rMi[c], rMd[c]);
+      }
+    }
+    const int* mt = sMeta + slot * META;
+    const double* ar = sAr + slot * 4;
+    // ---- compute macro e from shared memory
+    for (int it = tid; it < NI * 5; it += NT) {
+      const int kq = it / 5, t = it % 5, k = kq / NQF, q = kq % NQF;
+      if (use_x) {
         const double* fp = sFP + q * D::FS;
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < D::NFN; ++j) acc += fp[j] * sX[(k * D::NFN + j) * 5 + t];
-        sXq[it] = acc;
+        for (int j = 0; j < NFN; ++j) acc += fp[j] * sX[(k * NFN + j) * 5 + t];
+        sQ1[it] = acc;
       }
-      __syncthreads();
-      for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
-        const int kq = it / 5, s = it % 5, k = kq / D::NQF, q = kq % D::NQF;
-        const size_t base = ((size_t)e * 4 * D::NQF + kq) * 25 + s * 5;
-        const double* xq = sXq + kq * 5;
+      if (MODE == 1) {
+        const double* pf = sPF + kq * D::FS;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < NFN; ++j) acc += pf[j] * sZ[sRows[k * NFN + j] * 5 + t];
+        sQ2[it] = acc;
+      }
+    }
+    __syncthreads();
+    for (int it = tid; it < NI * 5; it += NT) {
+      const int kq = it / 5, s = it % 5, k = kq / NQF, q = kq % NQF;
+      const double fwq = sFW[q] * ar[k];
+      const double* xq = sQ1 + kq * 5;
+      const double* ta = sTA + kq * 25 + s * 5;
+      if (MODE == 0) {
+        double a = 0.0;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) a += ta[t] * xq[t];
+        sQ3[it] = fwq * a;
+      } else {
+        const double* zq = sQ2 + kq * 5;
+        const double* tb = sTB + kq * 25 + s * 5;
         double a = 0.0, b = 0.0;
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
-          a += __ldg(hhat + base + t) * xq[t];
-          if (mode == 0) b += __ldg(hh + base + t) * xq[t];
+          a += ta[t] * zq[t];
+          if (use_b) b += tb[t] * xq[t];
         }
-        const double fwq = sFW[q] * sAr[k];
-        sA1[it] = fwq * a;
-        if (mode == 0) sA2[it] = fwq * b;
+        sQ3[it] = fwq * a;
+        if (use_b) sQ4[it] = fwq * b;
+      }
+    }
+    __syncthreads();
+    if (MODE == 0) {
+      for (int o = tid; o < NX; o += NT) {
+        const int k = o / (NFN * 5), j = (o / 5) % NFN, s = o % 5;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int q = 0; q < NQF; ++q) acc += sPF[(k * NQF + q) * D::FS + j] * sQ3[(k * NQF + q) * 5 + s];
+        sQ2[o] = acc;
       }
       __syncthreads();
-    }
-    for (int o = tid; o < NM; o += NT) {
-      const int i = o / 5, s = o % 5;
-      double v = 0.0;
-      if (mode != 1) {
+      for (int o = tid; o < NM; o += NT) {
+        const int i = o / 5, s = o % 5;
+        double v = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const int kj = sNF[i * 3 + c];
           if (kj < 0) break;
-          const int k = kj / D::NFN, j = kj % D::NFN;
-          double acc = 0.0;
-          for (int q = 0; q < D::NQF; ++q)
-            acc += sPF[(k * D::NQF + q) * D::FS + j] * sA1[(k * D::NQF + q) * 5 + s];
-          v += acc;
+          v += sQ2[kj * 5 + s];
         }
-      }
-      if (mode == 0) sG[o] = -v;
-      else if (mode == 1) sG[o] = -r_w[(size_t)e * NM + o];
-      else sG[o] = -r_w[(size_t)e * NM + o] + (-v);
-    }
-    __syncthreads();
-    if (STAGE) {
-      mbar_wait(barS, phase);
-      for (int r = tid; r < NM; r += NT) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int c = 0;
-        for (; c + 3 < NM; c += 4) {
-          a0 += sS[(c + 0) * NM + r] * sG[c + 0];
-          a1 += sS[(c + 1) * NM + r] * sG[c + 1];
-          a2 += sS[(c + 2) * NM + r] * sG[c + 2];
-          a3 += sS[(c + 3) * NM + r] * sG[c + 3];
-        }
-        for (; c < NM; ++c) a0 += sS[c * NM + r] * sG[c];
-        sZ[r] = (a0 + a1) + (a2 + a3);
+        out[(size_t)e * NM + o] = (mode == 0) ? -v : (-r_w[(size_t)e * NM + o] + (-v));
       }
     } else {
-      const double* Si = sinv + (size_t)e * NM * NM;
-      for (int r = tid; r < NM; r += NT) {
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = 0;
-        for (; c + 7 < NM; c += 8) {
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = __ldcs(Si + (size_t)(c + u) * NM + r);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u & 3] += v[u] * sG[c + u];
-        }
-        for (; c < NM; ++c) acc[0] += __ldcs(Si + (size_t)c * NM + r) * sG[c];
-        sZ[r] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      }
-    }
-    __syncthreads();
-    if (STAGE && tid == 0 && e_next < g.E) {
-      fence_proxy_async();
-      mbar_expect_tx(barS, BYTES_S);
-      bulk_g2s(sS, sinv + (size_t)e_next * NM * NM, BYTES_S, barS);
-    }
-    if (mode == 2) {
-      phase ^= 1u;
-      for (int o = tid; o < NM; o += NT) d_w[(size_t)e * NM + o] = sZ[o];
-      continue;
-    }
-    for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
-      const int kq = it / 5, t = it % 5, k = kq / D::NQF, q = kq % D::NQF;
-      const double* pf = sPF + (k * D::NQF + q) * D::FS;
-      double acc = 0.0;
-#pragma unroll
-      for (int j = 0; j < D::NFN; ++j) acc += pf[j] * sZ[sRows[k * D::NFN + j] * 5 + t];
-      sXq[it] = acc;
-    }
-    if (STAGE) mbar_wait(barH, phase);
-    phase ^= 1u;
-    __syncthreads();
-    for (int it = tid; it < 4 * D::NQF * 5; it += NT) {
-      const int kq = it / 5, s = it % 5, q = kq % D::NQF, k = kq / D::NQF;
-      const double* zq = sXq + kq * 5;
-      double a = 0.0;
-      if (STAGE) {
-        const double* hr = sHW + kq * 25 + s * 5;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) a += hr[t] * zq[t];
-      } else {
-        const size_t base = ((size_t)e * 4 * D::NQF + kq) * 25 + s * 5;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) a += __ldcs(hw + base + t) * zq[t];
-      }
-      sA1[it] = (sFW[q] * sAr[k]) * a;
-    }
-    __syncthreads();
-    if (STAGE && tid == 0 && e_next < g.E) {
-      fence_proxy_async();
-      mbar_expect_tx(barH, BYTES_HW);
-      bulk_g2s(sHW, hw + (size_t)e_next * 4 * D::NQF * 25, BYTES_HW, barH);
-    }
-    for (int o = tid; o < 4 * D::NFN * 5; o += NT) {
-      const int k = o / (D::NFN * 5), j = (o / 5) % D::NFN, s = o % 5;
-      double a = 0.0, b = 0.0;
+      for (int o = tid; o < NX; o += NT) {
+        const int k = o / (NFN * 5), j = (o / 5) % NFN, s = o % 5;
+        double a = 0.0, b = 0.0;
 #pragma unroll 4
-      for (int q = 0; q < D::NQF; ++q) {
-        const double fp = sFP[q * D::FS + j];
-        a += fp * sA1[(k * D::NQF + q) * 5 + s];
-        if (mode == 0) b += fp * sA2[(k * D::NQF + q) * 5 + s];
+        for (int q = 0; q < NQF; ++q) {
+          const double fp = sFP[q * D::FS + j];
+          a += fp * sQ3[(k * NQF + q) * 5 + s];
+          if (use_b) b += fp * sQ4[(k * NQF + q) * 5 + s];
+        }
+        atomicAdd(&out[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s], b + a);
       }
-      atomicAdd(&y[((size_t)sFid[k] * D::NFN + sTid[k * D::NFN + j]) * 5 + s], b + a);
+    }
+    // metadata of e+2G lands in the slot freed two iterations ago
+    if (e2 < g.E) {
+#pragma unroll
+      for (int c = 0; c < FP::MPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < META + 4) meta_store(s2, i, rMi[c], rMd[c]);
+      }
     }
   }
 }
