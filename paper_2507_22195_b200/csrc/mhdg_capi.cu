@@ -247,6 +247,26 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 // ---------------------------------------------------------------------------
 // linearization
 // ---------------------------------------------------------------------------
+template <int P>
+static int launch_linearize2(mhdg_ctx* c, const double* w, const double* tr, double weight, double ptc,
+                             const mhdg_lin_buffers* L, cudaStream_t s) {
+  size_t smem = Lin2<P>::bytes;
+  if (set_smem(k_linearize2<P>, smem)) return MHDG_CUDA_ERROR;
+  int grid = grid_for(c, c->E, occ(k_linearize2<P>, 256, smem));
+  k_linearize2<P><<<grid, 256, smem, s>>>(c->geo, w, tr, weight, ptc, L->sinv, L->hw, L->hhat, L->hh,
+                                          c->d_status);
+  c->launches++;
+  constexpr int NM = Dims<P>::NM;
+  constexpr int TR = NM >= 64 ? 16 : 8, TC = NM >= 64 ? 16 : 8;
+  const size_t gsm = GJBatch<NM, TR, TC>::bytes;
+  if (set_smem(k_gj_batched<NM, TR, TC>, gsm)) return MHDG_CUDA_ERROR;
+  k_gj_batched<NM, TR, TC><<<grid_for(c, c->E, occ(k_gj_batched<NM, TR, TC>, TR * TC, gsm)), TR * TC, gsm, s>>>(
+      c->E, L->sinv, c->d_status);
+  c->launches++;
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
 template <int P, int NT>
 static int launch_linearize(mhdg_ctx* c, const double* w, const double* tr, double weight, double ptc,
                             const mhdg_lin_buffers* L, cudaStream_t s) {
@@ -274,9 +294,7 @@ static int launch_linearize(mhdg_ctx* c, const double* w, const double* tr, doub
 template <int P, int NT>
 static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* hh_rem,
                                  const int* tidx_rem, const double* area_rem, cudaStream_t s) {
-  using D = Dims<P>;
-  size_t smem = ((size_t)D::NB * D::NB + D::NQF * 25 + D::NQF * D::NFN + D::NB + D::NQF) * 8 +
-                ((size_t)D::NFN + D::NB + 2) * 4;
+  size_t smem = PreSmem<P, NT>::bytes;
   if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;
   int per_sm = occ(k_precond_factor<P, NT>, NT, smem);
   k_precond_factor<P, NT><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
@@ -311,9 +329,9 @@ static int linearize_local(mhdg_ctx* c, const double* w, const double* trace, do
   CK(cudaMemsetAsync(c->d_unsym, 0, sizeof(int), s));
   const double weight = alpha + ptc;
   switch (c->p) {
-    case 1: return launch_linearize<1, 128>(c, w, trace, weight, ptc, L, s);
-    case 2: return launch_linearize<2, 256>(c, w, trace, weight, ptc, L, s);
-    case 3: return launch_linearize<3, 256>(c, w, trace, weight, ptc, L, s);
+    case 1: return launch_linearize2<1>(c, w, trace, weight, ptc, L, s);
+    case 2: return launch_linearize2<2>(c, w, trace, weight, ptc, L, s);
+    case 3: return launch_linearize2<3>(c, w, trace, weight, ptc, L, s);
     default: return launch_linearize<4, 512>(c, w, trace, weight, ptc, L, s);
   }
 }

@@ -641,8 +641,452 @@ k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trac
 }
 
 // ===========================================================================
+// Register-blocked Gauss-Jordan inverse with implicit partial pivoting.
+// The N x N row-major matrix in shared memory A is distributed over a
+// TR x TC thread grid (thread (tr, tc) owns rows tr + TR a, columns
+// tc + TC b).  Step k: the pivot is the unused row with the largest |a_rk|
+// (first on ties, LAPACK idamax semantics), found redundantly by every warp;
+// no rows are swapped.  The result Y is written back to A with the pivot
+// sequence q (q[k] = pivot row of step k); then A^-1[r][c] = Y[q[r]][q^-1[c]]
+// (checked in numpy, tests/test_tables.py::test_implicit_pivot_gauss_jordan).
+// Returns false if a pivot is zero / non-finite.
+// ===========================================================================
+template <int N, int TR, int TC>
+struct GJDims {
+  static constexpr int RA = (N + TR - 1) / TR, CB = (N + TC - 1) / TC;
+  static constexpr int NPR = TR * RA, NPC = TC * CB;   // padded extents
+  static constexpr int NI = (N + 31) / 32;
+};
+
+// w: this thread's register tile, loaded by the caller (padding = 0).
+// colbuf: 2*NPR doubles, rowbuf: 2*NPC doubles (shared).  Writes q[N].
+template <int N, int TR, int TC>
+__device__ bool gj_inverse_reg(double (&w)[GJDims<N, TR, TC>::RA][GJDims<N, TR, TC>::CB], double* colbuf,
+                               double* rowbuf, int* q, int* sflag) {
+  using G = GJDims<N, TR, TC>;
+  constexpr int RA = G::RA, CB = G::CB, NI = G::NI;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool act = tid < TR * TC;
+  const int tr = act ? tid / TC : 0, tc = act ? tid % TC : 0;
+  for (int i = tid; i < 2 * G::NPR; i += blockDim.x) colbuf[i] = 0.0;
+  for (int i = tid; i < 2 * G::NPC; i += blockDim.x) rowbuf[i] = 0.0;
+  __syncthreads();
+  unsigned used = 0u;
+  bool ok = true;
+  for (int k = 0; k < N; ++k) {
+    const int cb = (k & 1) * G::NPR, rb = (k & 1) * G::NPC;
+    // 1. owners of column k publish it and clear their copy (the new column
+    //    k is -pinv * col for r != p and pinv on the pivot row)
+    if (act && tc == k % TC) {
+      const int kb = k / TC;
+#pragma unroll
+      for (int a = 0; a < RA; ++a) {
+        double v = 0.0;
+#pragma unroll
+        for (int b2 = 0; b2 < CB; ++b2)
+          if (b2 == kb) { v = w[a][b2]; w[a][b2] = 0.0; }
+        colbuf[cb + tr + TR * a] = v;
+      }
+    }
+    __syncthreads();
+    // 2. pivot: unused row with the largest |a_rk|, first on ties (every warp)
+    double best = -1.0;
+    int bi = N;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int r = lane + 32 * i;
+      if (r < N && !((used >> i) & 1u)) {
+        const double v = fabs(colbuf[cb + r]);
+        if (v > best) { best = v; bi = r; }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int p = bi < N ? bi : 0;
+    if ((p & 31) == lane) used |= 1u << (p >> 5);
+    const double piv = colbuf[cb + p];
+    if (!(fabs(piv) > 0.0) || !isfinite(piv)) ok = false;
+    if (tid == 0) q[k] = p;
+    // 3. pivot row owners scale the row and publish it
+    if (act && tr == p % TR) {
+      const int pa = p / TR;
+      const double pinv = 1.0 / piv;
+#pragma unroll
+      for (int b2 = 0; b2 < CB; ++b2) {
+        const int c = tc + TC * b2;
+        double v = 0.0;
+#pragma unroll
+        for (int a = 0; a < RA; ++a)
+          if (a == pa) v = w[a][b2];
+        v = (c == k ? 1.0 : v) * pinv;
+#pragma unroll
+        for (int a = 0; a < RA; ++a)
+          if (a == pa) w[a][b2] = v;
+        rowbuf[rb + c] = v;
+      }
+    }
+    __syncthreads();
+    // 4. rank-1 update of every other row: pure FMAs
+    if (act) {
+      double rv[CB];
+#pragma unroll
+      for (int b2 = 0; b2 < CB; ++b2) rv[b2] = rowbuf[rb + tc + TC * b2];
+#pragma unroll
+      for (int a = 0; a < RA; ++a) {
+        const int r = tr + TR * a;
+        const double cr = (r == p) ? 0.0 : colbuf[cb + r];
+#pragma unroll
+        for (int b2 = 0; b2 < CB; ++b2) w[a][b2] -= rv[b2] * cr;
+      }
+    }
+  }
+  if (tid == 0) *sflag = ok ? 0 : 1;
+  __syncthreads();
+  return *sflag == 0;
+}
+
+// store A^-1 column-major from the implicit-pivot result Y in shared memory:
+// out[c*N + r] = Y[q[r]][qinv[c]]; also reports non-finite entries
+template <int N, int NT>
+__device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, double* out) {
+  for (int k = threadIdx.x; k < N; k += NT) qinv[q[k]] = k;
+  __syncthreads();
+  int bad = 0;
+  for (int o = threadIdx.x; o < N * N; o += NT) {
+    const int c = o / N, r = o % N;
+    const double v = Y[q[r] * N + qinv[c]];
+    bad |= !isfinite(v);
+    out[o] = v;
+  }
+  return __syncthreads_or(bad) == 0;
+}
+
+// Batched in-place inverse: mats[e] holds S_e row-major on entry and
+// S_e^-1 column-major on exit (register Gauss-Jordan, implicit pivoting).
+template <int N, int TR, int TC>
+struct GJBatch {
+  using G = GJDims<N, TR, TC>;
+  static constexpr size_t bytes = (size_t)(N * N + 2 * G::NPR + 2 * G::NPC) * 8 + (size_t)(2 * N + 2) * 4;
+};
+
+template <int N, int TR, int TC>
+__global__ void __launch_bounds__(TR * TC, 2)
+k_gj_batched(int nmat, double* __restrict__ mats, unsigned long long* status) {
+  using G = GJDims<N, TR, TC>;
+  extern __shared__ __align__(16) double smem[];
+  double* Y = smem;
+  double* colbuf = Y + N * N;
+  double* rowbuf = colbuf + 2 * G::NPR;
+  int* q = (int*)(rowbuf + 2 * G::NPC);
+  int* qi = q + N;
+  int* flag = qi + N;
+  const int tid = threadIdx.x;
+  const int tr = tid / TC, tc = tid % TC;
+  for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
+    double* M = mats + (size_t)m * N * N;
+    double w[G::RA][G::CB];
+#pragma unroll
+    for (int a = 0; a < G::RA; ++a)
+#pragma unroll
+      for (int b = 0; b < G::CB; ++b) {
+        const int r = tr + TR * a, c = tc + TC * b;
+        w[a][b] = (r < N && c < N) ? M[r * N + c] : 0.0;
+      }
+    bool ok = gj_inverse_reg<N, TR, TC>(w, colbuf, rowbuf, q, flag);
+#pragma unroll
+    for (int a = 0; a < G::RA; ++a)
+#pragma unroll
+      for (int b = 0; b < G::CB; ++b) {
+        const int r = tr + TR * a, c = tc + TC * b;
+        if (r < N && c < N) Y[r * N + c] = w[a][b];
+      }
+    __syncthreads();
+    ok = gj_store_colmajor<N, TR * TC>(Y, q, qi, M) && ok;
+    if (!ok && tid == 0) report(status, 0, 0, m);
+    __syncthreads();
+  }
+}
+
+// ===========================================================================
+// K2 v2 (P <= 3): linearization with the S assembly on the FP64 tensor cores.
+//   pointwise : C[q][kk][st] (kk=0..2: -vol_w J^-1 dF/dw, kk=3: weight vol_w du/dw)
+//               by forward-mode duals, st = s*5 + t
+//   stage 1   : D[q][i][st] = sum_kk B[q][kk][i] C[q][kk][st]        (DMMA, K = 4)
+//   stage 2   : S_st[i][j] += sum_q D[q][i][st] phi[q][j]            (DMMA, per q chunk)
+//               accumulated in registers across chunks
+//   faces     : hw/hhat/hh tensors + face blocks of S (as in v1)
+//   inverse   : register-blocked Gauss-Jordan, implicit pivoting
+// ===========================================================================
+template <int P>
+struct Lin2 {
+  using D = Dims<P>;
+  static constexpr int NW = 8, NT = 256;
+  static constexpr int NNP = (D::NN + 7) / 8 * 8;      // padded nodes
+  static constexpr int IT = NNP / 8;                    // node tiles
+  static constexpr int QC = 8;                          // q chunk (2 k-steps)
+  static constexpr int NCH = (D::NQ + QC - 1) / QC;
+  static constexpr int CS = 32;                          // C row (st padded)
+  static constexpr int NPAIR = 25 * IT;                  // (st, i-tile) pairs
+  static constexpr int PPW = (NPAIR + NW - 1) / NW;      // pairs per warp
+  // shared memory (doubles)
+  static constexpr int S_ = D::NM * D::NM;
+  static constexpr int C_ = D::NQ * 4 * CS;
+  static constexpr int DD_ = QC * 25 * NNP;
+  static constexpr int doubles = S_ + C_ + DD_ + D::NN * 5 + 4 * D::NFN * 5 + 4 * D::NQF * D::FS +
+                                 D::NQF * D::FS + D::NQ + D::NQF + D::NQF * 25 + 4 * D::NM + 32;
+  static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + 2 * D::NM + 4;
+  static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256, 1)
+k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ trace, double weight,
+             double ptc, double* __restrict__ sinv, double* __restrict__ hw_out,
+             double* __restrict__ hhat_out, double* __restrict__ hh_out, unsigned long long* status) {
+  using D = Dims<P>;
+  using L = Lin2<P>;
+  constexpr int NN = D::NN, NQ = D::NQ, NM = D::NM, NFN = D::NFN, NQF = D::NQF, NNP = L::NNP;
+  constexpr int NT = L::NT, QC = L::QC, CS = L::CS, IT = L::IT;
+  extern __shared__ __align__(16) double smem[];
+  double* S = smem;                          // NM*NM
+  double* sC = S + L::S_;                    // NQ*4*CS
+  double* sD = sC + L::C_;                   // QC*25*NNP   [qq][st][i]
+  double* sW = sD + L::DD_;                  // NN*5
+  double* sTR = sW + NN * 5;                 // 4*NFN*5
+  double* sPF = sTR + 4 * NFN * 5;           // 4*NQF*FS
+  double* sFP = sPF + 4 * NQF * D::FS;       // NQF*FS
+  double* sQW = sFP + NQF * D::FS;           // NQ
+  double* sFW = sQW + NQ;                    // NQF
+  double* sHW = sFW + NQF;                   // NQF*25
+  double* sCol = sHW + NQF * 25;             // 2*NM
+  double* sRow = sCol + 2 * NM;              // 2*NM
+  double* sGeo = sRow + 2 * NM;              // 32
+  int* sRows = (int*)(sGeo + 32);
+  int* sFid = sRows + 4 * NFN;
+  int* sTid = sFid + 4;
+  int* sBnd = sTid + 4 * NFN;
+  int* sQ = sBnd + 4;                        // NM
+  int* sQi = sQ + NM;                        // NM
+  int* sFlag = sQi + NM;
+  const double* __restrict__ Bt = g.B;
+  const double gam = g.gamma;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
+  for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
+  for (int i = tid; i < NQ; i += NT) sQW[i] = g.qw[i];
+  for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
+  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
+  // padding lanes of C (st >= 25) stay zero
+  for (int i = tid; i < L::C_; i += NT) sC[i] = 0.0;
+
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
+    if (tid < 4) {
+      sFid[tid] = g.fid[e * 4 + tid];
+      sBnd[tid] = g.bnd ? g.bnd[e * 4 + tid] : 0;
+    }
+    for (int i = tid; i < 4 * NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * NFN + i];
+    if (tid == 32) sGeo[0] = g.det[e];
+    if (tid >= 33 && tid < 42) sGeo[tid - 32] = g.invj[(size_t)e * 9 + tid - 33];
+    if (tid >= 42 && tid < 54) sGeo[tid - 32] = g.nrm[(size_t)e * 12 + tid - 42];
+    if (tid >= 54 && tid < 58) sGeo[tid - 32] = g.area[(size_t)e * 4 + tid - 54];
+    __syncthreads();
+    for (int i = tid; i < 4 * NFN * 5; i += NT) {
+      const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
+      sTR[i] = trace[((size_t)sFid[k] * NFN + sTid[k * NFN + j]) * 5 + s2];
+    }
+    // ---- pointwise duals for all volume quadrature points
+    for (int it = tid; it < NQ * 5; it += NT) {
+      const int q = it / 5, t = it % 5;
+      const double* ph = Bt + ((size_t)q * 4 + 3) * NN;
+      double wq[5] = {0, 0, 0, 0, 0};
+      for (int i = 0; i < NN; ++i) {
+        const double a = __ldg(ph + i);
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) wq[s2] += a * sW[i * 5 + s2];
+      }
+      Dual wd[5], ud[5];
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) wd[s2] = mk(wq[s2], s2 == t ? 1.0 : 0.0);
+      to_conservative(wd, g.form, gam, ud);
+      Dual F[5][3];
+      flux(ud, gam, F);
+      const double vw = sQW[q] * sGeo[0];
+      double* C = sC + (size_t)q * 4 * CS;
+#pragma unroll
+      for (int kk = 0; kk < 3; ++kk) {
+        const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2)
+          C[kk * CS + s2 * 5 + t] = -(vw * ((j0 * F[s2][0].d + j1 * F[s2][1].d) + j2 * F[s2][2].d));
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) C[3 * CS + s2 * 5 + t] = weight * (vw * ud[s2].d);
+    }
+    __syncthreads();
+    // ---- S volume blocks on the tensor cores
+    double acc[L::PPW][IT][2];
+#pragma unroll
+    for (int c = 0; c < L::PPW; ++c)
+#pragma unroll
+      for (int jt = 0; jt < IT; ++jt) acc[c][jt][0] = acc[c][jt][1] = 0.0;
+    for (int ch = 0; ch < L::NCH; ++ch) {
+      const int q0 = ch * QC;
+      // stage 1: warp w -> chunk point qq = w: D[qq][st][i]
+      if (warp < QC) {
+        const int qq = warp, q = q0 + qq;
+        const int kk = lane & 3, r8 = lane >> 2;
+#pragma unroll
+        for (int itl = 0; itl < IT; ++itl) {
+          const int i = itl * 8 + r8;
+          const double a = (q < NQ && i < NN) ? __ldg(Bt + ((size_t)q * 4 + kk) * NN + i) : 0.0;
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            const double b = q < NQ ? sC[(size_t)q * 4 * CS + kk * CS + nt * 8 + r8] : 0.0;
+            double c2[2] = {0.0, 0.0};
+            dmma_8x8x4(c2, a, b);
+            const int ii = itl * 8 + r8, st0 = nt * 8 + (lane & 3) * 2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (st0 + h < 25) sD[((size_t)qq * 25 + st0 + h) * NNP + ii] = c2[h];
+          }
+        }
+      }
+      __syncthreads();
+      // stage 2: pairs (st, i-tile) owned by this warp, j-tiles in registers
+#pragma unroll
+      for (int ks = 0; ks < QC / 4; ++ks) {
+        const int qq = ks * 4 + (lane & 3), q = q0 + qq;
+        double bf[IT];
+#pragma unroll
+        for (int jt = 0; jt < IT; ++jt) {
+          const int j = jt * 8 + (lane >> 2);
+          bf[jt] = (q < NQ && j < NN) ? __ldg(Bt + ((size_t)q * 4 + 3) * NN + j) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < L::PPW; ++c) {
+          const int pr = warp + L::NW * c;
+          if (pr < L::NPAIR) {
+            const int st = pr / IT, itl = pr % IT;
+            const double a = sD[((size_t)qq * 25 + st) * NNP + itl * 8 + (lane >> 2)];
+#pragma unroll
+            for (int jt = 0; jt < IT; ++jt) dmma_8x8x4(acc[c][jt], a, bf[jt]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // scatter the accumulators into S[(i,s)][(j,t)]
+#pragma unroll
+    for (int c = 0; c < L::PPW; ++c) {
+      const int pr = warp + L::NW * c;
+      if (pr < L::NPAIR) {
+        const int st = pr / IT, itl = pr % IT, s2 = st / 5, t = st % 5;
+        const int i = itl * 8 + (lane >> 2);
+#pragma unroll
+        for (int jt = 0; jt < IT; ++jt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = jt * 8 + (lane & 3) * 2 + h;
+            if (i < NN && j < NN) S[(i * 5 + s2) * NM + j * 5 + t] = acc[c][jt][h];
+          }
+      }
+    }
+    // ---- face tiles: hw, hhat, hh tensors and the S face blocks
+    for (int k = 0; k < 4; ++k) {
+      __syncthreads();
+      const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
+      for (int it = tid; it < NQF * 10; it += NT) {
+        const int q = it / 10, t = (it % 10) % 5, which = (it % 10) / 5;
+        const double* pf = sPF + (k * NQF + q) * D::FS;
+        const double* fp = sFP + q * D::FS;
+        double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
+        for (int j = 0; j < NFN; ++j) {
+          const double a = pf[j], b = fp[j];
+          const int row = sRows[k * NFN + j];
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) {
+            wq[s2] += a * sW[row * 5 + s2];
+            whq[s2] += b * sTR[(k * NFN + j) * 5 + s2];
+          }
+        }
+        Dual wd[5], whd[5], ud[5], uhd[5], fd[5];
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) {
+          wd[s2] = mk(wq[s2], (which == 0 && s2 == t) ? 1.0 : 0.0);
+          whd[s2] = mk(whq[s2], (which == 1 && s2 == t) ? 1.0 : 0.0);
+        }
+        to_conservative(wd, g.form, gam, ud);
+        to_conservative(whd, g.form, gam, uhd);
+        numerical_flux(g.kind, ud, uhd, n, gam, fd);
+        const size_t base = (((size_t)e * 4 + k) * NQF + q) * 25;
+        if (which == 0) {
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) {
+            hw_out[base + s2 * 5 + t] = fd[s2].d;
+            sHW[q * 25 + s2 * 5 + t] = fd[s2].d;
+          }
+        } else {
+          double hv[5];
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) {
+            hhat_out[base + s2 * 5 + t] = fd[s2].d;
+            hv[s2] = fd[s2].d;
+          }
+          if (sBnd[k] && g.has_uinf) {
+            Dual ui[5], gd[5];
+#pragma unroll
+            for (int s2 = 0; s2 < 5; ++s2) ui[s2] = mk(g.uinf[s2], 0.0);
+            const double mn[3] = {-n[0], -n[1], -n[2]};
+            numerical_flux(g.kind, ui, uhd, mn, gam, gd);
+#pragma unroll
+            for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + gd[s2].d;
+          }
+          if (ptc != 0.0) {
+#pragma unroll
+            for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + (-ptc * uhd[s2].d);
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) hh_out[base + s2 * 5 + t] = hv[s2];
+        }
+      }
+      __syncthreads();
+      const double ar = sGeo[22 + k];
+      for (int o = tid; o < NFN * NFN * 25; o += NT) {
+        const int ij = o / 25, st = o % 25;
+        const int i = ij / NFN, j = ij % NFN, s2 = st / 5, t = st % 5;
+        double acc2 = 0.0;
+        for (int q = 0; q < NQF; ++q) {
+          const double* pf = sPF + (k * NQF + q) * D::FS;
+          acc2 += (((sFW[q] * ar) * pf[i]) * sHW[q * 25 + st]) * pf[j];
+        }
+        const int r = sRows[k * NFN + i] * 5 + s2, c = sRows[k * NFN + j] * 5 + t;
+        S[r * NM + c] += acc2;
+      }
+    }
+    __syncthreads();
+    // ---- S (row-major) to the S^-1 buffer; k_gj_batched inverts in place
+    double* out = sinv + (size_t)e * NM * NM;
+    for (int o = tid; o < NM * NM; o += NT) out[o] = S[o];
+  }
+}
+
+// ===========================================================================
 // K4 (factor): face-block preconditioner  (assembly.py:994-1026, 736-752)
 // ===========================================================================
+template <int P, int NT>
+struct PreSmem {
+  using D = Dims<P>;
+  static constexpr int NB = D::NB;
+  static constexpr size_t bytes = ((size_t)NB * NB + D::NQF * 25 + D::NQF * D::NFN + 4 * (NB + 16) + D::NQF) * 8 +
+                                  ((size_t)D::NFN + 2 * NB + 2) * 4;
+};
+
 template <int P, int NT>
 __global__ void __launch_bounds__(NT)
 k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double* __restrict__ hh_rem,
@@ -650,15 +1094,18 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
                  double* __restrict__ pinv, unsigned long long* status, int* n_unsym) {
   using D = Dims<P>;
   constexpr int NB = D::NB;
-  extern __shared__ double smem[];
+  constexpr int TR = NT >= 128 ? 16 : 8, TC = NT / TR;
+  extern __shared__ __align__(16) double smem[];
   double* A = smem;                      // NB*NB
   double* sHH = A + NB * NB;             // NQF*25
   double* sFP = sHH + D::NQF * 25;       // NQF*NFN
-  double* sCol = sFP + D::NQF * D::NFN;  // NB
-  double* sFw = sCol + NB;               // NQF
+  double* sCol = sFP + D::NQF * D::NFN;  // 2*NPR
+  double* sRow = sCol + 2 * (NB + 16);   // 2*NPC
+  double* sFw = sRow + 2 * (NB + 16);    // NQF
   int* sT = (int*)(sFw + D::NQF);        // NFN
-  int* sPerm = sT + D::NFN;              // NB
-  int* sFlag = sPerm + NB;               // 2
+  int* sQ = sT + D::NFN;                 // NB
+  int* sQi = sQ + NB;                    // NB
+  int* sFlag = sQi + NB;                 // 2
   const int tid = threadIdx.x;
   for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[i] = g.fphi[i];
   for (int f = blockIdx.x; f < n_faces; f += gridDim.x) {
@@ -690,7 +1137,7 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
       }
     }
     __syncthreads();
-    // symmetry statistic (reference logs the count of non-SPD/non-symmetric blocks)
+    // symmetry statistic (the reference logs the count of non-SPD/non-symmetric blocks)
     if (tid < 32) {
       double amax = 0.0, dmax = 0.0;
       for (int idx = tid; idx < NB * NB; idx += 32) {
@@ -704,16 +1151,32 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
       }
       if (tid == 0 && !(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
     }
-    bool ok = gj_inverse(A, NB, NB, sPerm, sCol, sFlag);
-    int bad = 0;
-    for (int o = tid; o < NB * NB; o += NT) bad |= !isfinite(A[o]);
-    bad = __syncthreads_or(bad);
-    if ((!ok || bad) && tid == 0) report(status, 0, 0, f);
-    double* out = pinv + (size_t)f * NB * NB;
-    for (int o = tid; o < NB * NB; o += NT) {
-      const int c = o / NB, r = o % NB;
-      out[o] = A[r * NB + c];
+    __syncthreads();
+    using G = GJDims<NB, TR, TC>;
+    double wr[G::RA][G::CB];
+    {
+      const int tr = tid / TC, tc = tid % TC;
+#pragma unroll
+      for (int a = 0; a < G::RA; ++a)
+#pragma unroll
+        for (int b = 0; b < G::CB; ++b) {
+          const int r = tr + TR * a, c = tc + TC * b;
+          wr[a][b] = (tid < TR * TC && r < NB && c < NB) ? A[r * NB + c] : 0.0;
+        }
+      __syncthreads();
+      bool ok0 = gj_inverse_reg<NB, TR, TC>(wr, sCol, sRow, sQ, sFlag);
+#pragma unroll
+      for (int a = 0; a < G::RA; ++a)
+#pragma unroll
+        for (int b = 0; b < G::CB; ++b) {
+          const int r = tr + TR * a, c = tc + TC * b;
+          if (tid < TR * TC && r < NB && c < NB) A[r * NB + c] = wr[a][b];
+        }
+      __syncthreads();
+      sFlag[1] = ok0;
     }
+    bool ok = gj_store_colmajor<NB, NT>(A, sQ, sQi, pinv + (size_t)f * NB * NB) && (sFlag[1] != 0);
+    if (!ok && tid == 0) report(status, 0, 0, f);
   }
 }
 

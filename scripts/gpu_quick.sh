@@ -12,3 +12,6 @@ for k,v in d['kernels'].items(): print(k, '%.3f ms'%v['ms'], '%.1f %s'%(v['achie
 print(d['clocks'])
 "
 tail -3 gpurun_out/bench.err
+python scripts/implicit_step.py --n 16 --p 3 > gpurun_out/step_cfg2.json 2> gpurun_out/step_cfg2.err; python -c "
+import json; d=json.load(open('gpurun_out/step_cfg2.json')); print('implicit step', {k:v for k,v in d.items() if k!='records'})
+" || tail -3 gpurun_out/step_cfg2.err
