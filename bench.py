@@ -356,6 +356,30 @@ def run_b200(args, rank, local_rank, world):
                 "peak_source": f"{hbm_src} MEASURED_PEAKS.json hbm_gbs" if kern[dom]["bound"] == "hbm"
                 else "measured FP64 FMA probe (mhdg_fp64_probe)"}
 
+    # ---- time per implicit step (one DIRK(3,3) step, dt = 0.01) and one
+    # Jacobian build, measured after the operator timing (not part of value)
+    from paper_2507_22195_b200.time_march import DIRKIntegrator
+
+    torch.cuda.synchronize()
+    jb0 = time.perf_counter()
+    lin2 = disc.jacobian(fields, stage, ptc_weight=1.0)
+    torch.cuda.synchronize()
+    jac_ms = 1e3 * (time.perf_counter() - jb0)
+    del lin2
+    integ = DIRKIntegrator(disc)
+    torch.cuda.synchronize()
+    st0 = time.perf_counter()
+    integ.run(fields, t_final=0.01, dt=0.01)
+    torch.cuda.synchronize()
+    step_s = time.perf_counter() - st0
+    rec = integ.records
+    implicit = {"seconds_per_step": step_s, "jacobian_build_ms": jac_ms,
+                "newton_iters": sum(r["newton_iters"] for r in rec),
+                "fgmres_outer": sum(r["fgmres_iters"] for r in rec),
+                "fgmres_inner": sum(r["inner_iters_total"] for r in rec),
+                "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
+                "dt": 0.01, "tableau": "DIRK(3,3)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_sample_n, args.p, args.flux, threads=1)
@@ -382,6 +406,7 @@ def run_b200(args, rank, local_rank, world):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "fp64_peak_tflops": fp64_peak,
+            "implicit_step": implicit,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
