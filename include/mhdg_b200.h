@@ -76,6 +76,14 @@ typedef struct {
   const double* freestream;   /* (5) conservative far-field state or NULL */
   int n_owned_faces;          /* faces [0, n_owned) get preconditioner blocks;
                                  0 = all (single partition)                   */
+  /* viscous closure (gas.py:48-77) and reference operators of the gradient
+   * equation (assembly.py:326-371), NULL / 0 for inviscid runs            */
+  int has_visc;
+  double reynolds, mach, prandtl, mu;
+  const double* minv_ref;     /* (nn, nn)  inverse reference mass matrix  */
+  const double* pref;         /* (3, nn, nn) Mref^-1 Kref_k               */
+  const double* kref;         /* (3, nn, nn) Kref_k[j][i]                 */
+  const double* eref;         /* (n_st, nfn, nfn) Eref_k[i][j]            */
 } mhdg_tables;
 
 typedef struct mhdg_ctx mhdg_ctx;
@@ -87,29 +95,35 @@ typedef struct {
   double* hhat; /* (E, n_st, nqf, 5, 5) dF^/dw^                        */
   double* hh;   /* (E, n_st, nqf, 5, 5) hhat + ghost + trace ptc       */
   double* pinv; /* (F, 5nt, 5nt) face-block inverse, column-major      */
+  double* wlin; /* (E, nc, 5) state of the linearization (viscous)      */
 } mhdg_lin_buffers;
 
 /* Discretization.__init__ (assembly.py:120-153): upload tables. */
 mhdg_ctx* mhdg_create(const mhdg_tables* tables, int device, int* err);
 void mhdg_destroy(mhdg_ctx* ctx);
-/* element counts of the five mhdg_lin_buffers arrays */
-void mhdg_lin_sizes(const mhdg_ctx* ctx, int64_t sizes[5]);
+/* element counts of the six mhdg_lin_buffers arrays */
+void mhdg_lin_sizes(const mhdg_ctx* ctx, int64_t sizes[6]);
 
 /* Discretization.residuals (assembly.py:459-549).  offset may be NULL;
  * has_stage = 0 means stage None.  check = 0 skips the rho/P checks
  * (residuals(check=False)).  sync = 0 leaves the status on the device
- * (retrieve with mhdg_status_fetch). */
+ * (retrieve with mhdg_status_fetch).  q / r_q: (E, nc, 5, 3) gradient
+ * unknowns and their residual, NULL for inviscid runs. */
 int mhdg_residual(mhdg_ctx* ctx, const double* w, const double* trace,
-                  int has_stage, double alpha, const double* offset, int check,
-                  double* r_w, double* r_trace, int sync, mhdg_status* st,
+                  const double* q, int has_stage, double alpha,
+                  const double* offset, int check, double* r_w,
+                  double* r_trace, double* r_q, int sync, mhdg_status* st,
                   void* stream);
+/* Discretization.solve_gradient (assembly.py:398-411): q = M^-1 (E w^ - K w) */
+int mhdg_solve_gradient(mhdg_ctx* ctx, const double* w, const double* trace,
+                        double* q, void* stream);
 int mhdg_status_fetch(mhdg_ctx* ctx, mhdg_status* st, void* stream);
 
 /* Discretization.jacobian / LinearizedSystem.__init__ (assembly.py:697-1026):
  * linearization tensors, S assembly, per-macro S^-1, face-block inverses. */
 int mhdg_linearize(mhdg_ctx* ctx, const double* w, const double* trace,
-                   double alpha, double ptc_weight, const mhdg_lin_buffers* lin,
-                   mhdg_status* st, void* stream);
+                   const double* q, double alpha, double ptc_weight,
+                   const mhdg_lin_buffers* lin, mhdg_status* st, void* stream);
 
 /* The two halves of mhdg_linearize, for partitioned runs where the
  * preconditioner blocks of halo faces need the other rank's side:
@@ -118,7 +132,7 @@ int mhdg_linearize(mhdg_ctx* ctx, const double* w, const double* trace,
  * (face_sides entries <= -2) from hh_remote (n_remote, nqf, 5, 5),
  * tidx_remote (n_remote, nfn) and area_remote (n_remote) device arrays. */
 int mhdg_linearize_local(mhdg_ctx* ctx, const double* w, const double* trace,
-                         double alpha, double ptc_weight,
+                         const double* q, double alpha, double ptc_weight,
                          const mhdg_lin_buffers* lin, mhdg_status* st,
                          void* stream);
 int mhdg_precond_factor(mhdg_ctx* ctx, const mhdg_lin_buffers* lin,
@@ -131,11 +145,12 @@ int mhdg_matvec(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* x,
                 double* y, void* stream);
 /* LinearizedSystem.condensed_rhs (assembly.py:1145-1157) */
 int mhdg_condensed_rhs(mhdg_ctx* ctx, const mhdg_lin_buffers* lin,
-                       const double* r_w, const double* r_trace, double* b,
-                       void* stream);
-/* LinearizedSystem.recover (assembly.py:1159-1173): d_w */
+                       const double* r_w, const double* r_trace,
+                       const double* r_q, double* b, void* stream);
+/* LinearizedSystem.recover (assembly.py:1159-1173): d_w (and d_q if viscous) */
 int mhdg_recover(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* r_w,
-                 const double* d_trace, double* d_w, void* stream);
+                 const double* r_q, const double* d_trace, double* d_w,
+                 double* d_q, void* stream);
 /* LinearizedSystem.apply_preconditioner (assembly.py:1175-1180) */
 int mhdg_precond(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* r,
                  double* z, void* stream);

@@ -107,6 +107,45 @@ class Gas:
         rho, vel, p = self.primitive(u)
         return _rabs(np.sum(vel * n, axis=-1)) + np.sqrt(self.g * p / rho)
 
+    # -- diffusive terms (gas.py:229-280) ------------------------------------
+    def grads_conservative(self, u, gu):
+        rho, vel, p = self.primitive(u)
+        grho, gmom, gre = gu[..., 0, :], gu[..., 1:-1, :], gu[..., -1, :]
+        gvel = (gmom - vel[..., None] * grho[..., None, :]) / rho[..., None, None]
+        ke = 0.5 * np.sum(vel * vel, axis=-1)
+        conv = np.sum(u[..., 1:-1, None] * gvel, axis=-2)
+        gp = (self.g - 1) * (gre - ke[..., None] * grho - conv)
+        gt = self.g * (rho[..., None] * gp - p[..., None] * grho) / rho[..., None] ** 2
+        return gvel, gt
+
+    def grads_entropy(self, v, gv):
+        ve = v[..., -1]
+        gve = gv[..., -1, :]
+        gvm = gv[..., 1:-1, :]
+        gvel = (v[..., 1:-1, None] * gve[..., None, :] - ve[..., None, None] * gvm) \
+            / ve[..., None, None] ** 2
+        return gvel, self.g * gve / ve[..., None] ** 2
+
+    def viscous_flux(self, visc, vel, gvel, gt):
+        mu = visc.mu / visc.reynolds
+        kappa = visc.mu / (visc.reynolds * (self.g - 1) * visc.mach ** 2 * visc.prandtl)
+        d = vel.shape[-1]
+        div = np.trace(gvel, axis1=-2, axis2=-1)
+        tau = mu * (gvel + np.swapaxes(gvel, -1, -2))
+        for a in range(d):
+            tau[..., a, a] -= (2.0 / 3.0) * mu * div
+        g = np.zeros(vel.shape[:-1] + (d + 2, d), dtype=gvel.dtype)
+        g[..., 1:-1, :] = -tau
+        g[..., -1, :] = -(np.sum(tau * vel[..., :, None], axis=-2) + kappa * gt)
+        return g
+
+    def penalty(self, visc, d):
+        diag = np.empty(d + 2)
+        diag[0] = 0.0
+        diag[1:-1] = visc.mu / visc.reynolds
+        diag[-1] = visc.mu / (visc.reynolds * (self.g - 1) * visc.mach ** 2 * visc.prandtl)
+        return diag
+
 
 class OracleInadmissible(FloatingPointError):
     def __init__(self, kind, where=None):
@@ -201,6 +240,14 @@ def numerical_flux(gas, kind, u, uh, n):
     return f - 0.5 * np.einsum("...ij,...j->...i", R, lam_abs * T * proj)
 
 
+def _cs_jacobian_q(fn, q):
+    """Complex-step Jacobian over the (state, direction) axes of q."""
+    shape = q.shape
+    flat = q.reshape(shape[:-2] + (-1,))
+    jac = cs_jacobian(lambda qf: fn(qf.reshape(qf.shape[:-1] + shape[-2:])), flat)
+    return jac.reshape(jac.shape[:-1] + shape[-2:])
+
+
 def cs_jacobian(fn, x):
     """Complex-step Jacobian over the last axis (gas.py:32-45)."""
     x = np.asarray(x, dtype=float)
@@ -222,12 +269,64 @@ class OracleHDG:
     periodic or with a free-stream state on boundary faces)."""
 
     def __init__(self, tables, flux="es", formulation="entropy", gamma=1.4,
-                 freestream=None):
+                 freestream=None, viscosity=None):
         self.t = tables
         self.gas = Gas(gamma)
         self.kind = flux
         self.form = formulation
         self.freestream = None if freestream is None else np.asarray(freestream, float)
+        self.visc = viscosity
+        if viscosity is not None:
+            self._gradient_operators()
+
+    # -- viscous level-1 operators (assembly.py:326-371) ----------------------
+    def _gradient_operators(self):
+        t = self.t
+        E, nc, d = t.mesh.n_macros, t.layout.n_unique, t.d
+        vol_w, dphi_phys = t.vol_w, t.dphi_phys
+        mass = np.zeros((E, nc, nc))
+        stiff = np.zeros((E, d, nc, nc))
+        for s in range(t.layout.n_sub):
+            ids = t.layout.scatter[s]
+            mloc = np.einsum("eq,qi,qj->eij", vol_w[:, s], t.phi, t.phi)
+            kloc = np.einsum("eq,eqjb,qi->ebji", vol_w[:, s], dphi_phys[:, s], t.phi)
+            np.add.at(mass, (slice(None), ids[:, None], ids[None, :]), mloc)
+            np.add.at(stiff, (slice(None), slice(None), ids[:, None], ids[None, :]), kloc)
+        self.mass, self.stiff = mass, stiff
+        self.mass_factor = [cho_factor(mass[e]) for e in range(E)]
+        self.minvk = np.stack([np.stack([cho_solve(self.mass_factor[e], stiff[e, b])
+                                         for b in range(d)]) for e in range(E)])
+        self.edge = np.stack([np.einsum("eq,qi,qj,eb->eijb", t.face_w[:, k], t.phi_face[k], t.fphi,
+                                        t.face_normals[:, k]) for k in range(t.n_st)], axis=1)
+
+    def mass_solve(self, y):
+        out = np.empty_like(y)
+        nc = y.shape[1]
+        for e in range(y.shape[0]):
+            out[e] = cho_solve(self.mass_factor[e], y[e].reshape(nc, -1),
+                               check_finite=False).reshape(y[e].shape)
+        return out
+
+    def solve_gradient(self, w, trace):
+        """M q_b = E_b w^ - K_b w (assembly.py:398-411)."""
+        t = self.t
+        rhs = -np.einsum("ebji,eit->ejtb", self.stiff, w)
+        for k in range(t.n_st):
+            contrib = np.einsum("eijb,ejt->eitb", self.edge[:, k], self._gather(trace, k))
+            np.add.at(rhs, (slice(None), t.face_rows[k]), contrib)
+        return self.mass_solve(rhs)
+
+    def _grads(self, wq, qq):
+        return (self.gas.grads_entropy(wq, qq) if self.form == "entropy"
+                else self.gas.grads_conservative(wq, qq))
+
+    def viscous_volume_flux(self, wq, qq, uq):
+        gv, gt = self._grads(wq, qq)
+        return self.gas.viscous_flux(self.visc, self.gas.primitive(uq)[1], gv, gt)
+
+    def viscous_face_flux(self, wq, qq, uq, nrm):
+        g = self.viscous_volume_flux(wq, qq, uq)
+        return np.einsum("...sa,...a->...s", g, nrm)
 
     # working variables <-> conservative
     def to_u(self, w):
@@ -259,20 +358,28 @@ class OracleHDG:
             out[:, s] = self.to_u(wq)
         return out
 
-    def residuals(self, w, trace, alpha=None, offset=None):
-        """(r_w, r_trace) of assembly.py:459-549 (inviscid)."""
+    def residuals(self, w, trace, alpha=None, offset=None, q=None):
+        """(r_w, r_trace[, r_q]) of assembly.py:459-549."""
         t, gas = self.t, self.gas
+        visc = self.visc is not None
         dtype = np.result_type(w, trace, float)
         r_w = np.zeros(w.shape, dtype=dtype)
         r_tr = np.zeros(trace.shape, dtype=dtype)
+        r_q = np.zeros(w.shape + (t.d,), dtype=dtype) if visc else None
         vol_w = t.vol_w
         dphi_phys = t.dphi_phys
         for s in range(t.layout.n_sub):
             ids = t.layout.scatter[s]
             wq = np.einsum("qi,eis->eqs", t.phi, w[:, ids])
             uq = self._checked_u(wq, f"volume sub {s}")
+            fl = gas.flux(uq)
+            if visc:
+                qq = np.einsum("qi,eitb->eqtb", t.phi, q[:, ids])
+                fl = fl + self.viscous_volume_flux(wq, qq, uq)
+                r_q[:, ids] += np.einsum("eq,qi,eqtb->eitb", vol_w[:, s], t.phi, qq)
+                r_q[:, ids] += np.einsum("eq,eqib,eqt->eitb", vol_w[:, s], dphi_phys[:, s], wq)
             r_w[:, ids] -= np.einsum("eq,eqia,eqsa->eis", vol_w[:, s],
-                                     dphi_phys[:, s], gas.flux(uq))
+                                     dphi_phys[:, s], fl)
             if alpha is not None:
                 tmp = alpha * uq
                 if offset is not None:
@@ -287,18 +394,29 @@ class OracleHDG:
             uhq = self._checked_u(whq, f"trace tile {k}")
             nrm = t.face_normals[:, k][:, None, :]
             fl = numerical_flux(gas, self.kind, uq, uhq, nrm)
+            if visc:
+                qq = np.einsum("qi,eitb->eqtb", t.phi_face[k], q[:, rows])
+                gn = self.viscous_face_flux(wq, qq, uq, nrm)
+                fl = fl + (gn - 0.5 * gas.penalty(self.visc, t.d) * (whq - wq))
+                r_q[:, rows] -= np.einsum("eq,qi,eqt,eb->eitb", face_w[:, k], t.phi_face[k], whq,
+                                          t.face_normals[:, k])
             r_w[:, rows] += np.einsum("eq,qi,eqs->eis", face_w[:, k], t.phi_face[k], fl)
             vals = np.einsum("eq,qi,eqs->eis", face_w[:, k], t.fphi, fl)
             mask = t.boundary_st[:, k]
             if self.freestream is not None and mask.any():
                 uinf = np.broadcast_to(self.freestream, uhq[mask].shape)
                 ghost = numerical_flux(gas, self.kind, uinf, uhq[mask], -nrm[mask])
+                if visc:
+                    winf = np.broadcast_to(self.from_u(self.freestream), whq[mask].shape)
+                    ghost = ghost + (0.0 - 0.5 * gas.penalty(self.visc, t.d) * (whq[mask] - winf))
                 vals[mask] += np.einsum("eq,qi,eqs->eis", face_w[mask][:, k], t.fphi, ghost)
             np.add.at(r_tr, (t.face_id_st[:, k][:, None], t.trace_idx[:, k]), vals)
+        if visc:
+            return r_w, r_tr, r_q
         return r_w, r_tr
 
-    def linearize(self, w, trace, alpha=0.0, ptc_weight=0.0, precond=True):
-        return OracleLin(self, w, trace, alpha, ptc_weight, precond)
+    def linearize(self, w, trace, alpha=0.0, ptc_weight=0.0, precond=True, q=None):
+        return OracleLin(self, w, trace, alpha, ptc_weight, precond, q)
 
     def integrals(self, w):
         """Volume integrals of assembly.py:595-620."""
@@ -324,19 +442,31 @@ class OracleLin:
     inviscid): S per macro (LU), face quadrature tensors hw / hhat / ptc,
     face-block preconditioner (Cholesky if symmetric SPD else LU)."""
 
-    def __init__(self, op, w, trace, alpha, ptc_weight, precond=True):
+    def __init__(self, op, w, trace, alpha, ptc_weight, precond=True, q=None):
         t, gas = op.t, op.gas
         self.op = op
         self.shape = trace.shape
+        self.viscous = op.visc is not None
         E, nc, ns = w.shape
+        d = t.d
         weight = alpha + ptc_weight
         S = np.zeros((E, nc, ns, nc, ns))
         vol_w = t.vol_w
         dphi_phys = t.dphi_phys
+        self.avq_sub, self.avq_face, self.avhatq = [], [], []
         for s in range(t.layout.n_sub):
             ids = t.layout.scatter[s]
             wq = np.einsum("qi,eis->eqs", t.phi, w[:, ids])
-            fgw = cs_jacobian(lambda wc: gas.flux(op.to_u(wc)), wq)   # (E,q,s,a,t)
+            qq = np.einsum("qi,eitb->eqtb", t.phi, q[:, ids]) if self.viscous else None
+
+            def transport(wc, qf=qq):
+                u = op.to_u(wc)
+                f = gas.flux(u)
+                if qf is not None:
+                    f = f + op.viscous_volume_flux(wc, qf, u)
+                return f
+
+            fgw = cs_jacobian(transport, wq)   # (E,q,s,a,t)
             blk = -np.einsum("eq,eqia,eqsat,qj->eisjt", vol_w[:, s], dphi_phys[:, s],
                              fgw, t.phi, optimize=True)
             if weight != 0.0:
@@ -346,6 +476,13 @@ class OracleLin:
                                                tw, t.phi, optimize=True)
             S_view = S.transpose(0, 1, 3, 2, 4)                     # (E, i, j, s, t)
             S_view[:, ids[:, None], ids[None, :]] += blk.transpose(0, 1, 3, 2, 4)
+            if self.viscous:
+                gq = _cs_jacobian_q(lambda qc: op.viscous_volume_flux(wq, qc, op.to_u(wq)), qq)
+                avq = -np.einsum("eq,eqia,eqsatb,ql->eisltb", vol_w[:, s], dphi_phys[:, s], gq,
+                                 t.phi, optimize=True)
+                self.avq_sub.append(avq)
+                corr = np.einsum("eisltb,eblj->eisjt", avq, op.minvk[:, :, ids, :], optimize=True)
+                S[:, ids] -= corr
         self.hw, self.hhat, self.hh = [], [], []
         face_w = t.face_w
         for k in range(t.n_st):
@@ -354,13 +491,31 @@ class OracleLin:
             whq = np.einsum("qi,eis->eqs", t.fphi, op._gather(trace, k))
             nrm = t.face_normals[:, k][:, None, :]
             uhq = op.to_u(whq)
-            hw = cs_jacobian(lambda wc: numerical_flux(gas, op.kind, op.to_u(wc), uhq, nrm), wq)
-            hhat = cs_jacobian(lambda wc: numerical_flux(gas, op.kind, op.to_u(wq), op.to_u(wc), nrm), whq)
+            qq = np.einsum("qi,eitb->eqtb", t.phi_face[k], q[:, rows]) if self.viscous else None
+            pen = gas.penalty(op.visc, d) if self.viscous else None
+
+            def face_total(wc, whc, qf=qq):
+                u, uh = op.to_u(wc), op.to_u(whc)
+                f = numerical_flux(gas, op.kind, u, uh, nrm)
+                if qf is not None:
+                    f = f + (op.viscous_face_flux(wc, qf, u, nrm) - 0.5 * pen * (whc - wc))
+                return f
+
+            hw = cs_jacobian(lambda wc: face_total(wc, whq), wq)
+            hhat = cs_jacobian(lambda wc: face_total(wq, wc), whq)
             hh = hhat.copy()
             mask = t.boundary_st[:, k]
             if op.freestream is not None and mask.any():
                 uinf = np.broadcast_to(op.freestream, uhq.shape)
-                gh = cs_jacobian(lambda wc: numerical_flux(gas, op.kind, uinf, op.to_u(wc), -nrm), whq)
+                winf = np.broadcast_to(op.from_u(op.freestream), whq.shape)
+
+                def ghost_total(wc):
+                    f = numerical_flux(gas, op.kind, uinf, op.to_u(wc), -nrm)
+                    if pen is not None:
+                        f = f + (0.0 - 0.5 * pen * (wc - winf))
+                    return f
+
+                gh = cs_jacobian(ghost_total, whq)
                 gh[~mask] = 0.0
                 hh = hh + gh
             if ptc_weight != 0.0:
@@ -374,6 +529,18 @@ class OracleLin:
                             t.phi_face[k], optimize=True)
             S_view = S.transpose(0, 1, 3, 2, 4)
             S_view[:, rows[:, None], rows[None, :]] += blk.transpose(0, 1, 3, 2, 4)
+            if self.viscous:
+                uq = op.to_u(wq)
+                gqf = _cs_jacobian_q(lambda qc: op.viscous_face_flux(wq, qc, uq, nrm)
+                                     - 0.5 * pen * (whq - wq), qq)
+                avqf = np.einsum("eq,qi,eqstb,ql->eisltb", face_w[:, k], t.phi_face[k], gqf,
+                                 t.phi_face[k], optimize=True)
+                avh = np.einsum("eq,qi,eqstb,ql->eisltb", face_w[:, k], t.fphi, gqf,
+                                t.phi_face[k], optimize=True)
+                self.avq_face.append(avqf)
+                self.avhatq.append(avh)
+                corr = np.einsum("eisltb,eblj->eisjt", avqf, op.minvk[:, :, rows, :], optimize=True)
+                S[:, rows] -= corr
         Smat = S.reshape(E, nc * ns, nc * ns)
         self.lu = []
         for e in range(E):
@@ -454,17 +621,74 @@ class OracleLin:
         return self._tile_apply_to_trace(
             self.hh, lambda k: np.einsum("qi,eis->eqs", t.fphi, self.op._gather(xh, k)))
 
+    # viscous level-1 couplings (assembly.py:1037-1084)
+    def apply_qv(self, x):
+        return np.einsum("ebji,eit->ejtb", self.op.stiff, x)
+
+    def apply_qvhat(self, xh):
+        t = self.op.t
+        out = np.zeros((t.mesh.n_macros, t.layout.n_unique, t.n_s, t.d))
+        for k in range(t.n_st):
+            contrib = np.einsum("eijb,ejt->eitb", self.op.edge[:, k], self.op._gather(xh, k))
+            np.add.at(out, (slice(None), t.face_rows[k]), -contrib)
+        return out
+
+    def apply_vq(self, y):
+        t = self.op.t
+        out = np.zeros((t.mesh.n_macros, t.layout.n_unique, t.n_s))
+        for s in range(t.layout.n_sub):
+            ids = t.layout.scatter[s]
+            out[:, ids] += np.einsum("eisltb,eltb->eis", self.avq_sub[s], y[:, ids])
+        for k in range(t.n_st):
+            rows = t.face_rows[k]
+            out[:, rows] += np.einsum("eisltb,eltb->eis", self.avq_face[k], y[:, rows])
+        return out
+
+    def apply_vhatq(self, y):
+        t = self.op.t
+        out = np.zeros(self.shape)
+        for k in range(t.n_st):
+            vals = np.einsum("eisltb,eltb->eis", self.avhatq[k], y[:, t.face_rows[k]])
+            np.add.at(out, (t.face_id_st[:, k][:, None], t.trace_idx[:, k]), vals)
+        return out
+
     def matvec(self, xh):
         out = self.apply_vhatvhat(xh)
-        z = self.solve_schur(-self.apply_vvhat(xh))
-        return out + self.apply_vhatv(z)
+        g2 = -self.apply_vvhat(xh)
+        if self.viscous:
+            yq = self.op.mass_solve(self.apply_qvhat(xh))
+            g2 += self.apply_vq(yq)
+            out -= self.apply_vhatq(yq)
+        z = self.solve_schur(g2)
+        out += self.apply_vhatv(z)
+        if self.viscous:
+            out -= self.apply_vhatq(self.op.mass_solve(self.apply_qv(z)))
+        return out
 
-    def condensed_rhs(self, r_w, r_trace):
-        z = self.solve_schur(-r_w)
-        return -r_trace - self.apply_vhatv(z)
+    def condensed_rhs(self, r_w, r_trace, r_q=None):
+        rw, rh = -r_w, -r_trace
+        if self.viscous:
+            mq = self.op.mass_solve(r_q)
+            rw = rw + self.apply_vq(mq)
+            rh = rh + self.apply_vhatq(mq)
+        z = self.solve_schur(rw)
+        b = rh - self.apply_vhatv(z)
+        if self.viscous:
+            b += self.apply_vhatq(self.op.mass_solve(self.apply_qv(z)))
+        return b
 
-    def recover(self, r_w, d_trace):
-        return self.solve_schur(-r_w - self.apply_vvhat(d_trace))
+    def recover(self, r_w, d_trace, r_q=None):
+        rw = -r_w
+        if self.viscous:
+            rw = rw + self.apply_vq(self.op.mass_solve(r_q))
+        g2 = -self.apply_vvhat(d_trace)
+        if self.viscous:
+            g2 += self.apply_vq(self.op.mass_solve(self.apply_qvhat(d_trace)))
+        d_w = self.solve_schur(rw + g2)
+        if not self.viscous:
+            return d_w
+        d_q = -self.op.mass_solve(r_q + self.apply_qv(d_w) + self.apply_qvhat(d_trace))
+        return d_w, d_q
 
     def apply_preconditioner(self, r):
         out = np.empty_like(r)

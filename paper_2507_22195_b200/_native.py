@@ -47,31 +47,37 @@ class Tables(C.Structure):
         ("sub_inv_jac", dptr), ("face_normals", dptr), ("face_area", dptr),
         ("face_id_st", dptr), ("trace_idx", dptr), ("boundary_st", dptr),
         ("face_sides", dptr), ("freestream", dptr), ("n_owned_faces", C.c_int),
+        ("has_visc", C.c_int), ("reynolds", C.c_double), ("mach", C.c_double),
+        ("prandtl", C.c_double), ("mu", C.c_double), ("minv_ref", dptr), ("pref", dptr),
+        ("kref", dptr), ("eref", dptr),
     ]
 
 
 class LinBuffers(C.Structure):
-    _fields_ = [("sinv", dptr), ("hw", dptr), ("hhat", dptr), ("hh", dptr), ("pinv", dptr)]
+    _fields_ = [("sinv", dptr), ("hw", dptr), ("hhat", dptr), ("hh", dptr), ("pinv", dptr),
+                ("wlin", dptr)]
 
 
 _SIGS = {
     "mhdg_create": (C.c_void_p, [C.POINTER(Tables), C.c_int, C.POINTER(C.c_int)]),
     "mhdg_destroy": (None, [C.c_void_p]),
     "mhdg_lin_sizes": (None, [C.c_void_p, C.POINTER(C.c_int64)]),
-    "mhdg_residual": (C.c_int, [C.c_void_p, dptr, dptr, C.c_int, C.c_double, dptr, C.c_int,
-                                dptr, dptr, C.c_int, C.POINTER(Status), C.c_void_p]),
+    "mhdg_residual": (C.c_int, [C.c_void_p, dptr, dptr, dptr, C.c_int, C.c_double, dptr, C.c_int,
+                                dptr, dptr, dptr, C.c_int, C.POINTER(Status), C.c_void_p]),
+    "mhdg_solve_gradient": (C.c_int, [C.c_void_p, dptr, dptr, dptr, C.c_void_p]),
     "mhdg_status_fetch": (C.c_int, [C.c_void_p, C.POINTER(Status), C.c_void_p]),
-    "mhdg_linearize": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, C.c_double,
+    "mhdg_linearize": (C.c_int, [C.c_void_p, dptr, dptr, dptr, C.c_double, C.c_double,
                                  C.POINTER(LinBuffers), C.POINTER(Status), C.c_void_p]),
-    "mhdg_linearize_local": (C.c_int, [C.c_void_p, dptr, dptr, C.c_double, C.c_double,
+    "mhdg_linearize_local": (C.c_int, [C.c_void_p, dptr, dptr, dptr, C.c_double, C.c_double,
                                        C.POINTER(LinBuffers), C.POINTER(Status), C.c_void_p]),
     "mhdg_precond_factor": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), C.c_int, dptr, dptr, dptr,
                                       C.POINTER(Status), C.c_void_p]),
     "mhdg_axpy_dev": (C.c_int, [C.c_void_p, C.c_int64, dptr, dptr, dptr, C.c_void_p]),
     "mhdg_matvec": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, C.c_void_p]),
-    "mhdg_condensed_rhs": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr,
+    "mhdg_condensed_rhs": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, dptr,
                                      C.c_void_p]),
-    "mhdg_recover": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, C.c_void_p]),
+    "mhdg_recover": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, dptr, dptr,
+                               C.c_void_p]),
     "mhdg_precond": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, C.c_void_p]),
     "mhdg_volume_quad_states": (C.c_int, [C.c_void_p, dptr, dptr, C.POINTER(Status), C.c_void_p]),
     "mhdg_to_conservative": (C.c_int, [C.c_void_p, C.c_int64, dptr, dptr, C.POINTER(Status),

@@ -57,9 +57,10 @@ class FieldSet:
     q: object = None
 
     def copy(self):
-        return FieldSet(self.w.clone() if hasattr(self.w, "clone") else self.w.copy(),
-                        self.trace.clone() if hasattr(self.trace, "clone") else self.trace.copy(),
-                        None if self.q is None else self.q.clone())
+        def cp(a):
+            return None if a is None else (a.clone() if hasattr(a, "clone") else a.copy())
+
+        return FieldSet(cp(self.w), cp(self.trace), cp(self.q))
 
 
 @dataclass
@@ -107,9 +108,9 @@ def boundary_trace_operator(kind, state=None):
 class Discretization:
     """Spatial operator on a macro mesh at degree p, evaluated on the GPU.
 
-    Supported on the device: d = 3, m = 1, p = 1..4, default quadrature,
-    entropy or conservative formulation, lf/ec/es/kepes fluxes, periodic or
-    free-stream boundaries, inviscid.  Anything else raises InvalidConfig
+    Supported on the device: d = 3, m = 1, p = 1..4 (viscous: 1..3), default
+    quadrature, entropy or conservative formulation, lf/ec/es/kepes fluxes,
+    periodic or free-stream boundaries, Euler or Navier-Stokes (constant mu).  Anything else raises InvalidConfig
     (the reference-only features are listed in DESIGN.md).
     """
 
@@ -120,9 +121,6 @@ class Discretization:
             raise InvalidConfig(f"unknown formulation {formulation!r}")
         if supg:
             raise InvalidConfig("SUPG streamline term is not on the B200 path")
-        if viscosity is not None:
-            raise InvalidConfig("viscous operator (level-1 q condensation) is not on the "
-                                "B200 path yet")
         if tables is None and mesh.has_boundary and boundary is None:
             raise InvalidConfig("mesh has boundary faces, a boundary treatment is required")
         if mesh.dim != 3 or mesh.m != 1:
@@ -140,7 +138,7 @@ class Discretization:
         self.gas = gas or GasModel()
         self.formulation = formulation
         self.flux = flux or DissipationSpec("kepes")
-        self.viscosity = None
+        self.viscosity = viscosity
         self.supg = False
         self.boundary = boundary
         self.d = mesh.dim
@@ -185,6 +183,15 @@ class Discretization:
         tab.face_sides = keep(t.face_sides, np.int64)
         tab.freestream = keep(boundary.state, np.float64) if boundary is not None else None
         tab.n_owned_faces = int(n_owned_faces)
+        if viscosity is not None:
+            if p > 3:
+                raise InvalidConfig("the viscous B200 operator supports p = 1..3")
+            minv, pref, kref, eref = t.viscous_reference()
+            tab.has_visc = 1
+            tab.reynolds, tab.mach = float(viscosity.reynolds), float(viscosity.mach)
+            tab.prandtl, tab.mu = float(viscosity.prandtl), float(viscosity.mu)
+            tab.minv_ref, tab.pref = keep(minv, np.float64), keep(pref, np.float64)
+            tab.kref, tab.eref = keep(kref, np.float64), keep(eref, np.float64)
         err = C.c_int(0)
         with torch.cuda.device(self.device):
             self._ctx = lib.mhdg_create(C.byref(tab), self.device.index, C.byref(err))
@@ -192,7 +199,7 @@ class Discretization:
             N.raise_for(err.value or 6, None, "(mhdg_create)")
         self._keep = []
         self._scalar = torch.zeros(8, dtype=torch.float64, device=self.device)
-        sizes = (C.c_int64 * 5)()
+        sizes = (C.c_int64 * 6)()
         lib.mhdg_lin_sizes(self._ctx, sizes)
         self.lin_sizes = tuple(int(s) for s in sizes)
 
@@ -245,6 +252,13 @@ class Discretization:
     def _fields(self, fields):
         return self._dev(fields.w), self._dev(fields.trace)
 
+    def _q(self, fields):
+        if self.viscosity is None:
+            return None
+        if fields.q is None:
+            raise InvalidConfig("viscous discretization needs fields.q")
+        return self._dev(fields.q)
+
     def residual_norm(self, res):
         parts = [res.r_w, res.r_trace] + ([res.r_q] if res.r_q is not None else [])
         return math.sqrt(sum(self.vdot(p, p) for p in parts))
@@ -290,7 +304,20 @@ class Discretization:
         u_trace = state_fn(self.trace_coords)
         if self.formulation == "entropy":
             u_nodes, u_trace = self.gas.entropy_vars(u_nodes), self.gas.entropy_vars(u_trace)
-        return FieldSet(w=self._dev(u_nodes), trace=self._dev(u_trace))
+        fields = FieldSet(w=self._dev(u_nodes), trace=self._dev(u_trace))
+        if self.viscosity is not None:
+            fields.q = self.solve_gradient(fields)
+        return fields
+
+    def solve_gradient(self, fields):
+        """Discrete gradient q_b = M^-1 (E_b w^ - K_b w) (assembly.py:398-411)."""
+        torch = _torch()
+        w, tr = self._fields(fields)
+        q = torch.empty(tuple(w.shape) + (self.d,), dtype=torch.float64, device=self.device)
+        rc = self._lib.mhdg_solve_gradient(self._ctx, N.ptr(w), N.ptr(tr), N.ptr(q),
+                                           N.stream_handle())
+        N.raise_for(rc)
+        return q
 
     def volume_quad_states(self, fields):
         torch = _torch()
@@ -307,18 +334,20 @@ class Discretization:
     def residuals(self, fields, stage=None, check=True, sync=True):
         torch = _torch()
         w, tr = self._fields(fields)
+        q = self._q(fields)
         r_w = torch.empty_like(w)
         r_tr = torch.empty_like(tr)
+        r_q = torch.empty_like(q) if q is not None else None
         off = None
         if stage is not None and stage.offset is not None:
             off = self._dev(stage.offset)
         st = N.Status()
         rc = self._lib.mhdg_residual(
-            self._ctx, N.ptr(w), N.ptr(tr), int(stage is not None),
+            self._ctx, N.ptr(w), N.ptr(tr), N.ptr(q), int(stage is not None),
             float(stage.alpha) if stage is not None else 0.0, N.ptr(off), int(bool(check)),
-            N.ptr(r_w), N.ptr(r_tr), int(bool(sync)), C.byref(st), N.stream_handle())
+            N.ptr(r_w), N.ptr(r_tr), N.ptr(r_q), int(bool(sync)), C.byref(st), N.stream_handle())
         N.raise_for(rc, st)
-        return ResidualSet(r_w=r_w, r_trace=r_tr, r_q=None, _disc=self)
+        return ResidualSet(r_w=r_w, r_trace=r_tr, r_q=r_q, _disc=self)
 
     def jacobian(self, fields, stage=None, ptc_weight=0.0, sparse_local_threshold=2048):
         return LinearizedSystem(self, fields, stage, ptc_weight)
@@ -355,24 +384,26 @@ class LinearizedSystem:
     def __init__(self, disc, fields, stage, ptc_weight):
         torch = _torch()
         self.disc = disc
-        self.viscous = False
+        self.viscous = disc.viscosity is not None
         w, tr = disc._fields(fields)
+        q = disc._q(fields)
         self.trace_shape = tuple(tr.shape)
-        sz = disc.lin_sizes
-        dev = disc.device
-        self.sinv = torch.empty(sz[0], dtype=torch.float64, device=dev)
-        self.hw = torch.empty(sz[1], dtype=torch.float64, device=dev)
-        self.hhat = torch.empty(sz[2], dtype=torch.float64, device=dev)
-        self.hh = torch.empty(sz[3], dtype=torch.float64, device=dev)
-        self.pinv = torch.empty(sz[4], dtype=torch.float64, device=dev)
-        self._buf = N.LinBuffers(N.ptr(self.sinv), N.ptr(self.hw), N.ptr(self.hhat),
-                                 N.ptr(self.hh), N.ptr(self.pinv))
+        self.alloc(disc)
         alpha = float(stage.alpha) if stage is not None else 0.0
         st = N.Status()
-        rc = disc._lib.mhdg_linearize(disc._ctx, N.ptr(w), N.ptr(tr), alpha, float(ptc_weight),
-                                      C.byref(self._buf), C.byref(st), N.stream_handle())
+        rc = disc._lib.mhdg_linearize(disc._ctx, N.ptr(w), N.ptr(tr), N.ptr(q), alpha,
+                                      float(ptc_weight), C.byref(self._buf), C.byref(st),
+                                      N.stream_handle())
         N.raise_for(rc, st)
         self.n_unsym = int(st.n_unsym)
+
+    def alloc(self, disc):
+        torch = _torch()
+        sz = disc.lin_sizes
+        for name, n in zip(("sinv", "hw", "hhat", "hh", "pinv", "wlin"), sz):
+            setattr(self, name, torch.empty(n, dtype=torch.float64, device=disc.device))
+        self._buf = N.LinBuffers(*(N.ptr(getattr(self, n)) for n in
+                                   ("sinv", "hw", "hhat", "hh", "pinv", "wlin")))
 
     def _out_trace(self):
         return _torch().empty(self.trace_shape, dtype=_torch().float64, device=self.disc.device)
@@ -388,21 +419,24 @@ class LinearizedSystem:
     def condensed_rhs(self, res):
         d = self.disc
         rw, rt = d._dev(res.r_w), d._dev(res.r_trace)
+        rq = d._dev(res.r_q) if self.viscous else None
         b = self._out_trace()
-        rc = d._lib.mhdg_condensed_rhs(d._ctx, C.byref(self._buf), N.ptr(rw), N.ptr(rt), N.ptr(b),
-                                       N.stream_handle())
+        rc = d._lib.mhdg_condensed_rhs(d._ctx, C.byref(self._buf), N.ptr(rw), N.ptr(rt), N.ptr(rq),
+                                       N.ptr(b), N.stream_handle())
         N.raise_for(rc)
         return b
 
     def recover(self, res, d_trace):
         d = self.disc
         rw = d._dev(res.r_w)
+        rq = d._dev(res.r_q) if self.viscous else None
         x = d._dev(d_trace).reshape(self.trace_shape)
         dw = _torch().empty_like(rw)
-        rc = d._lib.mhdg_recover(d._ctx, C.byref(self._buf), N.ptr(rw), N.ptr(x), N.ptr(dw),
-                                 N.stream_handle())
+        dq = _torch().empty_like(rq) if self.viscous else None
+        rc = d._lib.mhdg_recover(d._ctx, C.byref(self._buf), N.ptr(rw), N.ptr(rq), N.ptr(x),
+                                 N.ptr(dw), N.ptr(dq), N.stream_handle())
         N.raise_for(rc)
-        return dw, None
+        return dw, dq
 
     def apply_preconditioner(self, r):
         d = self.disc

@@ -13,6 +13,7 @@
 
 #include "../../include/mhdg_b200.h"
 #include "mhdg_kernels.cuh"
+#include "mhdg_viscous.cuh"
 
 using namespace mhdg;
 
@@ -20,6 +21,8 @@ struct mhdg_ctx {
   int device;
   int p, E, F, nn, nq, nfn, nqf;
   int n_owned;
+  int visc;
+  ViscGeo vg;
   int n_sms;
   Geo geo;
   std::vector<void*> allocs;
@@ -91,6 +94,7 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   c->p = P; c->E = t->n_macros; c->F = t->n_faces;
   c->nn = NN; c->nq = NQ; c->nfn = NFN; c->nqf = NQF;
   c->n_owned = t->n_owned_faces > 0 ? t->n_owned_faces : t->n_faces;
+  c->visc = t->has_visc;
   c->launches = 0;
   c->d_scratch = nullptr;
   c->scratch_bytes = 0;
@@ -133,6 +137,19 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   g.has_uinf = t->freestream != nullptr;
   if (t->freestream)
     for (int s = 0; s < 5; ++s) g.uinf[s] = t->freestream[s];
+  memset(&c->vg, 0, sizeof(c->vg));
+  if (t->has_visc) {
+    const double gm = t->gamma;
+    c->vg.mu_eff = t->mu / t->reynolds;
+    c->vg.kappa = t->mu / (t->reynolds * (gm - 1) * t->mach * t->mach * t->prandtl);
+    c->vg.pdiag[0] = 0.0;
+    for (int s2 = 1; s2 < 4; ++s2) c->vg.pdiag[s2] = c->vg.mu_eff;
+    c->vg.pdiag[4] = c->vg.kappa;
+    c->vg.minv = upload(c, t->minv_ref, (size_t)NN * NN, err);
+    c->vg.pref = upload(c, t->pref, (size_t)3 * NN * NN, err);
+    c->vg.kref = upload(c, t->kref, (size_t)3 * NN * NN, err);
+    c->vg.eref = upload(c, t->eref, (size_t)4 * NFN * NFN, err);
+  }
   c->d_status = (unsigned long long*)dalloc(c, sizeof(unsigned long long) * 4, err);
   c->d_unsym = (int*)dalloc(c, sizeof(int) * 4, err);
   c->d_partial = (double*)dalloc(c, sizeof(double) * (2 * RED_BLOCKS * 5 + 64), err);
@@ -154,11 +171,12 @@ extern "C" void mhdg_destroy(mhdg_ctx* c) {
   delete c;
 }
 
-extern "C" void mhdg_lin_sizes(const mhdg_ctx* c, int64_t sizes[5]) {
+extern "C" void mhdg_lin_sizes(const mhdg_ctx* c, int64_t sizes[6]) {
   const int64_t nm = 5 * c->nn, nb = 5 * c->nfn;
   sizes[0] = (int64_t)c->E * nm * nm;
   sizes[1] = sizes[2] = sizes[3] = (int64_t)c->E * 4 * c->nqf * 25;
   sizes[4] = (int64_t)c->F * nb * nb;
+  sizes[5] = c->visc ? (int64_t)c->E * nm : 1;
 }
 
 extern "C" int64_t mhdg_launch_count(const mhdg_ctx* c) { return c->launches; }
@@ -225,14 +243,54 @@ extern "C" int mhdg_status_fetch(mhdg_ctx* c, mhdg_status* st, void* stream) {
   return tmp.code;
 }
 
-extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, int has_stage, double alpha,
-                             const double* offset, int check, double* r_w, double* r_trace, int sync,
-                             mhdg_status* st, void* stream) {
+template <int P>
+static int launch_residual_visc(mhdg_ctx* c, const double* w, const double* q, const double* tr, int has_stage,
+                                double alpha, const double* off, int check, double* rw, double* rt, double* rq,
+                                cudaStream_t s) {
+  const size_t smem = ResVisc<P>::bytes;
+  if (set_smem(k_residual_visc<P>, smem)) return MHDG_CUDA_ERROR;
+  k_residual_visc<P><<<grid_for(c, c->E, occ(k_residual_visc<P>, 128, smem)), 128, smem, s>>>(
+      c->geo, c->vg, w, q, tr, has_stage, alpha, off, check, rw, rt, rq, c->d_status);
+  c->launches++;
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
+extern "C" int mhdg_solve_gradient(mhdg_ctx* c, const double* w, const double* trace, double* q, void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  if (!c->visc) return MHDG_INVALID_CONFIG;
+  switch (c->p) {
+    case 1: k_solve_gradient<1, 64><<<grid_for(c, c->E, 16), 64, 0, s>>>(c->geo, c->vg, w, trace, q); break;
+    case 2: k_solve_gradient<2, 128><<<grid_for(c, c->E, 8), 128, 0, s>>>(c->geo, c->vg, w, trace, q); break;
+    case 3: k_solve_gradient<3, 128><<<grid_for(c, c->E, 8), 128, 0, s>>>(c->geo, c->vg, w, trace, q); break;
+    default: k_solve_gradient<4, 128><<<grid_for(c, c->E, 8), 128, 0, s>>>(c->geo, c->vg, w, trace, q); break;
+  }
+  c->launches++;
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
+extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, const double* q, int has_stage,
+                             double alpha, const double* offset, int check, double* r_w, double* r_trace,
+                             double* r_q, int sync, mhdg_status* st, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
   CK(cudaMemsetAsync(c->d_status, 0xff, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(r_trace, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   int rc;
+  if (c->visc) {
+    if (!q || !r_q) return MHDG_INVALID_CONFIG;
+    switch (c->p) {
+      case 1: rc = launch_residual_visc<1>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s); break;
+      case 2: rc = launch_residual_visc<2>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s); break;
+      case 3: rc = launch_residual_visc<3>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s); break;
+      default: rc = launch_residual_visc<4>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s); break;
+    }
+    if (rc) return rc;
+    if (!sync) return MHDG_OK;
+    return mhdg_status_fetch(c, st, stream);
+  }
   switch (c->p) {
     case 1: rc = launch_residual<1>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
     case 2: rc = launch_residual<2>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s); break;
@@ -248,20 +306,33 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 // linearization
 // ---------------------------------------------------------------------------
 template <int P>
-static int launch_linearize2(mhdg_ctx* c, const double* w, const double* tr, double weight, double ptc,
-                             const mhdg_lin_buffers* L, cudaStream_t s) {
+static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, const double* tr, double weight,
+                             double ptc, const mhdg_lin_buffers* L, cudaStream_t s) {
   size_t smem = Lin2<P>::bytes;
-  if (set_smem(k_linearize2<P>, smem)) return MHDG_CUDA_ERROR;
-  int grid = grid_for(c, c->E, occ(k_linearize2<P>, 256, smem));
-  k_linearize2<P><<<grid, 256, smem, s>>>(c->geo, w, tr, weight, ptc, L->sinv, L->hw, L->hhat, L->hh,
-                                          c->d_status);
-  c->launches++;
+  if (c->visc) {
+    if (set_smem(k_linearize2<P, true>, smem)) return MHDG_CUDA_ERROR;
+    int grid = grid_for(c, c->E, occ(k_linearize2<P, true>, 256, smem));
+    k_linearize2<P, true><<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat,
+                                                  L->hh, c->d_status);
+    const size_t csm = SCorr<P>::bytes;
+    if (set_smem(k_visc_scorr<P>, csm)) return MHDG_CUDA_ERROR;
+    k_visc_scorr<P><<<grid_for(c, c->E, occ(k_visc_scorr<P>, 256, csm)), 256, csm, s>>>(c->geo, c->vg, w, L->sinv);
+    c->launches += 2;
+    CK(cudaMemcpyAsync(L->wlin, w, sizeof(double) * (size_t)c->E * c->nn * 5, cudaMemcpyDeviceToDevice, s));
+  } else {
+    if (set_smem(k_linearize2<P, false>, smem)) return MHDG_CUDA_ERROR;
+    int grid = grid_for(c, c->E, occ(k_linearize2<P, false>, 256, smem));
+    k_linearize2<P, false><<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw,
+                                                   L->hhat, L->hh, c->d_status);
+    c->launches++;
+  }
   constexpr int NM = Dims<P>::NM;
   constexpr int TR = NM >= 64 ? 16 : 8, TC = NM >= 64 ? 16 : 8;
   const size_t gsm = GJBatch<NM, TR, TC>::bytes;
   if (set_smem(k_gj_batched<NM, TR, TC>, gsm)) return MHDG_CUDA_ERROR;
   k_gj_batched<NM, TR, TC><<<grid_for(c, c->E, occ(k_gj_batched<NM, TR, TC>, TR * TC, gsm)), TR * TC, gsm, s>>>(
       c->E, L->sinv, c->d_status);
+  (void)ptc;
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;
@@ -322,17 +393,19 @@ static int fetch_lin_status(mhdg_ctx* c, mhdg_status* st, cudaStream_t s) {
   return tmp.code;
 }
 
-static int linearize_local(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
-                           const mhdg_lin_buffers* L, cudaStream_t s) {
+static int linearize_local(mhdg_ctx* c, const double* w, const double* q, const double* trace, double alpha,
+                           double ptc, const mhdg_lin_buffers* L, cudaStream_t s) {
   CK(cudaSetDevice(c->device));
   CK(cudaMemsetAsync(c->d_status, 0xff, 2 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(c->d_unsym, 0, sizeof(int), s));
   const double weight = alpha + ptc;
   switch (c->p) {
-    case 1: return launch_linearize2<1>(c, w, trace, weight, ptc, L, s);
-    case 2: return launch_linearize2<2>(c, w, trace, weight, ptc, L, s);
-    case 3: return launch_linearize2<3>(c, w, trace, weight, ptc, L, s);
-    default: return launch_linearize<4, 512>(c, w, trace, weight, ptc, L, s);
+    case 1: return launch_linearize2<1>(c, w, q, trace, weight, ptc, L, s);
+    case 2: return launch_linearize2<2>(c, w, q, trace, weight, ptc, L, s);
+    case 3: return launch_linearize2<3>(c, w, q, trace, weight, ptc, L, s);
+    default:
+      if (c->visc) return MHDG_INVALID_CONFIG;   // viscous k = 4 not on the device yet
+      return launch_linearize<4, 512>(c, w, trace, weight, ptc, L, s);
   }
 }
 
@@ -346,20 +419,23 @@ static int precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* 
   }
 }
 
-extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
-                              const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
+extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace, const double* q, double alpha,
+                              double ptc, const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
   cudaStream_t s = S(stream);
-  int rc = linearize_local(c, w, trace, alpha, ptc, L, s);
+  if (c->visc && !q) return MHDG_INVALID_CONFIG;
+  int rc = linearize_local(c, w, q, trace, alpha, ptc, L, s);
   if (rc) return rc;
   rc = precond_factor(c, L, nullptr, nullptr, nullptr, s);
   if (rc) return rc;
   return fetch_lin_status(c, st, s);
 }
 
-extern "C" int mhdg_linearize_local(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
-                                    const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
+extern "C" int mhdg_linearize_local(mhdg_ctx* c, const double* w, const double* trace, const double* q,
+                                    double alpha, double ptc, const mhdg_lin_buffers* L, mhdg_status* st,
+                                    void* stream) {
   cudaStream_t s = S(stream);
-  int rc = linearize_local(c, w, trace, alpha, ptc, L, s);
+  if (c->visc && !q) return MHDG_INVALID_CONFIG;
+  int rc = linearize_local(c, w, q, trace, alpha, ptc, L, s);
   if (rc) return rc;
   return fetch_lin_status(c, st, s);
 }
@@ -408,8 +484,39 @@ static int condensed_split(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, con
   return MHDG_OK;
 }
 
+template <int P>
+static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
+                          const double* rq, double* y, double* dw, cudaStream_t s) {
+  using D = Dims<P>;
+  const size_t vsm = VOp<P>::bytes;
+  if (set_smem(k_visc_in<P>, vsm) || set_smem(k_visc_out<P>, vsm)) return MHDG_CUDA_ERROR;
+  double* gbuf = c->d_gbuf;
+  double* zbuf = (mode == 2) ? dw : c->d_zbuf;
+  k_visc_in<P><<<grid_for(c, c->E, occ(k_visc_in<P>, 128, vsm)), 128, vsm, s>>>(c->geo, c->vg, mode, L->wlin, L->hhat,
+                                                                              x, rw, rq, gbuf);
+  constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
+  k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(c->E, L->sinv,
+                                                                                                 gbuf, 0, zbuf);
+  c->launches += 2;
+  if (mode != 2) {
+    k_visc_out<P><<<grid_for(c, c->E, occ(k_visc_out<P>, 128, vsm)), 128, vsm, s>>>(c->geo, c->vg, mode, L->wlin, L->hh,
+                                                                                   L->hw, x, zbuf, rq, y);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
 static int condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
-                     double* y, double* dw, cudaStream_t s) {
+                     double* y, double* dw, cudaStream_t s, const double* rq = nullptr) {
+  if (c->visc) {
+    switch (c->p) {
+      case 1: return condensed_visc<1>(c, mode, L, x, rw, rq, y, dw, s);
+      case 2: return condensed_visc<2>(c, mode, L, x, rw, rq, y, dw, s);
+      case 3: return condensed_visc<3>(c, mode, L, x, rw, rq, y, dw, s);
+      default: return MHDG_INVALID_CONFIG;
+    }
+  }
   switch (c->p) {
     case 1: return condensed_split<1>(c, mode, L, x, rw, y, dw, s);
     case 2: return condensed_split<2>(c, mode, L, x, rw, y, dw, s);
@@ -432,12 +539,13 @@ __global__ void k_neg_sub(int64_t n, const double* __restrict__ a, const double*
 }
 
 extern "C" int mhdg_condensed_rhs(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* r_w,
-                                  const double* r_trace, double* b, void* stream) {
+                                  const double* r_trace, const double* r_q, double* b, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->visc && !r_q) return MHDG_INVALID_CONFIG;
   const int64_t nt = (int64_t)c->F * c->nfn * 5;
   CK(cudaMemsetAsync(c->d_tmp_trace, 0, sizeof(double) * nt, s));
-  int rc = condensed(c, 1, L, nullptr, r_w, c->d_tmp_trace, nullptr, s);
+  int rc = condensed(c, 1, L, nullptr, r_w, c->d_tmp_trace, nullptr, s, r_q);
   if (rc) return rc;
   k_neg_sub<<<grid_for(c, (int)std::min<int64_t>((nt + 255) / 256, 1 << 20), 8), 256, 0, s>>>(
       nt, r_trace, c->d_tmp_trace, b);
@@ -446,11 +554,21 @@ extern "C" int mhdg_condensed_rhs(mhdg_ctx* c, const mhdg_lin_buffers* L, const 
   return MHDG_OK;
 }
 
-extern "C" int mhdg_recover(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* r_w, const double* d_trace,
-                            double* d_w, void* stream) {
+extern "C" int mhdg_recover(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* r_w, const double* r_q,
+                            const double* d_trace, double* d_w, double* d_q, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
-  return condensed(c, 2, L, d_trace, r_w, nullptr, d_w, s);
+  if (c->visc && (!r_q || !d_q)) return MHDG_INVALID_CONFIG;
+  int rc = condensed(c, 2, L, d_trace, r_w, nullptr, d_w, s, r_q);
+  if (rc || !c->visc) return rc;
+  switch (c->p) {
+    case 1: k_visc_dq<1><<<grid_for(c, c->E, 16), 128, 0, s>>>(c->geo, c->vg, r_q, d_w, d_trace, d_q); break;
+    case 2: k_visc_dq<2><<<grid_for(c, c->E, 16), 128, 0, s>>>(c->geo, c->vg, r_q, d_w, d_trace, d_q); break;
+    default: k_visc_dq<3><<<grid_for(c, c->E, 16), 128, 0, s>>>(c->geo, c->vg, r_q, d_w, d_trace, d_q); break;
+  }
+  c->launches++;
+  CK(cudaGetLastError());
+  return MHDG_OK;
 }
 
 extern "C" int mhdg_precond(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* r, double* z, void* stream) {

@@ -18,6 +18,7 @@
 #pragma once
 #include "mhdg_math.cuh"
 #include "mhdg_tma.cuh"
+#include "mhdg_visc_math.cuh"
 
 namespace mhdg {
 
@@ -839,12 +840,13 @@ struct Lin2 {
   static constexpr int doubles = S_ + C_ + DD_ + D::NN * 5 + 4 * D::NFN * 5 + 4 * D::NQF * D::FS +
                                  D::NQF * D::FS + D::NQ + D::NQF + D::NQF * 25 + 4 * D::NM + 32;
   static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + 2 * D::NM + 4;
-  static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
+  static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4 + 16 + D::NN * 15 * 8;
 };
 
-template <int P>
+template <int P, bool VISC>
 __global__ void __launch_bounds__(256, 1)
-k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ trace, double weight,
+k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __restrict__ qn,
+             const double* __restrict__ trace, double weight,
              double ptc, double* __restrict__ sinv, double* __restrict__ hw_out,
              double* __restrict__ hhat_out, double* __restrict__ hh_out, unsigned long long* status) {
   using D = Dims<P>;
@@ -872,6 +874,7 @@ k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ tra
   int* sQ = sBnd + 4;                        // NM
   int* sQi = sQ + NM;                        // NM
   int* sFlag = sQi + NM;
+  double* sQn = (double*)(((size_t)(sFlag + 4) + 15) & ~(size_t)15);   // NN*15 (viscous)
   const double* __restrict__ Bt = g.B;
   const double gam = g.gamma;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -886,6 +889,8 @@ k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ tra
   for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
     __syncthreads();
     for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
+    if (VISC)
+      for (int i = tid; i < NN * 15; i += NT) sQn[i] = qn[(size_t)e * NN * 15 + i];
     if (tid < 4) {
       sFid[tid] = g.fid[e * 4 + tid];
       sBnd[tid] = g.bnd ? g.bnd[e * 4 + tid] : 0;
@@ -916,6 +921,24 @@ k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ tra
       to_conservative(wd, g.form, gam, ud);
       Dual F[5][3];
       flux(ud, gam, F);
+      if (VISC) {
+        double qq[5][3];
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
+        for (int i = 0; i < NN; ++i) {
+          const double a = __ldg(ph + i);
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQn[i * 15 + s2 * 3 + b];
+        }
+        Dual Gv[5][3];
+        visc_G(vg, g.form, wd, ud, qq, gam, Gv);
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) F[s2][a] = F[s2][a] + Gv[s2][a];
+      }
       const double vw = sQW[q] * sGeo[0];
       double* C = sC + (size_t)q * 4 * CS;
 #pragma unroll
@@ -1024,6 +1047,26 @@ k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ tra
         to_conservative(wd, g.form, gam, ud);
         to_conservative(whd, g.form, gam, uhd);
         numerical_flux(g.kind, ud, uhd, n, gam, fd);
+        if (VISC) {
+          double qq[5][3];
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
+          for (int j = 0; j < NFN; ++j) {
+            const double a = pf[j];
+            const int row = sRows[k * NFN + j];
+#pragma unroll
+            for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQn[row * 15 + s2 * 3 + b];
+          }
+          Dual Gv[5][3];
+          visc_G(vg, g.form, wd, ud, qq, gam, Gv);
+#pragma unroll
+          for (int s2 = 0; s2 < 5; ++s2) {
+            const Dual gn = (Gv[s2][0] * n[0] + Gv[s2][1] * n[1]) + Gv[s2][2] * n[2];
+            fd[s2] = fd[s2] + (gn - (0.5 * vg.pdiag[s2]) * (whd[s2] - wd[s2]));
+          }
+        }
         const size_t base = (((size_t)e * 4 + k) * NQF + q) * 25;
         if (which == 0) {
 #pragma unroll
@@ -1044,6 +1087,13 @@ k_linearize2(Geo g, const double* __restrict__ w, const double* __restrict__ tra
             for (int s2 = 0; s2 < 5; ++s2) ui[s2] = mk(g.uinf[s2], 0.0);
             const double mn[3] = {-n[0], -n[1], -n[2]};
             numerical_flux(g.kind, ui, uhd, mn, gam, gd);
+            if (VISC) {
+              double winf[5];
+              if (g.form == FORM_ENTROPY) entropy_vars(g.uinf, gam, winf);
+              else for (int s2 = 0; s2 < 5; ++s2) winf[s2] = g.uinf[s2];
+#pragma unroll
+              for (int s2 = 0; s2 < 5; ++s2) gd[s2] = gd[s2] + (0.0 - (0.5 * vg.pdiag[s2]) * (whd[s2] - winf[s2]));
+            }
 #pragma unroll
             for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + gd[s2].d;
           }

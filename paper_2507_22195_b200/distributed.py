@@ -101,17 +101,15 @@ class PartitionedLinearizedSystem:
         # local linearization without the preconditioner ...
         self.lin = LinearizedSystem.__new__(LinearizedSystem)
         lin = self.lin
-        lin.disc, lin.viscous, lin.trace_shape = d, False, self.trace_shape
-        sz = d.lin_sizes
-        for name, n in zip(("sinv", "hw", "hhat", "hh", "pinv"), sz):
-            setattr(lin, name, torch.empty(n, dtype=torch.float64, device=d.device))
-        lin._buf = N.LinBuffers(N.ptr(lin.sinv), N.ptr(lin.hw), N.ptr(lin.hhat), N.ptr(lin.hh),
-                                N.ptr(lin.pinv))
+        lin.disc, lin.viscous, lin.trace_shape = d, d.viscosity is not None, self.trace_shape
+        lin.alloc(d)
         w, tr = d._fields(fields)
+        q = d._q(fields)
         alpha = float(stage.alpha) if stage is not None else 0.0
         st = N.Status()
-        rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(w), N.ptr(tr), alpha, float(ptc_weight),
-                                         C.byref(lin._buf), C.byref(st), N.stream_handle())
+        rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(w), N.ptr(tr), N.ptr(q), alpha,
+                                         float(ptc_weight), C.byref(lin._buf), C.byref(st),
+                                         N.stream_handle())
         N.raise_for(rc, st)
         # ... then the owned face blocks, with halo sides from the neighbours
         hh_r, tidx_r, area_r = gather_remote_sides(pdisc, lin)

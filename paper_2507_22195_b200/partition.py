@@ -100,6 +100,7 @@ class LocalPartition:
         lt.face_id_st = g2l[t.face_id_st[sl]]
         assert (lt.face_id_st >= 0).all()
         lt.n_faces = self.n_local_faces
+        lt.viscous_reference = t.viscous_reference
         lt.vol_w = lt.quad_wts[None, None, :] * lt.sub_det[:, :, None]
         lt.dphi_phys = np.einsum("qik,eska->esqia", lt.dphi, lt.sub_inv_jac)
         lt.face_w = lt.facet_wts[None, None, :] * lt.face_area[:, :, None]

@@ -130,6 +130,20 @@ class HDGTables:
         # so the per-tile factor area*(d-1)! is stored and multiplied on use
         self.face_area = areas * math.factorial(d - 1)      # (E, n_st)
 
+    def viscous_reference(self):
+        """Reference operators of the gradient equation (assembly.py:326-371)
+        on the unit simplex: Mref^-1, Kref_k[j][i] = sum_q w dphi_k[q,j] phi[q,i],
+        Pref_k = Mref^-1 Kref_k, Eref_k[i][j] = sum_q wf phi_face_k[q,i] fphi[q,j].
+        Per macro: M = det Mref, K_b = det sum_k Jinv[k][b] Kref_k,
+        E_k,b = area_k n_b Eref_k."""
+        w = self.quad_wts
+        mref = np.einsum("q,qi,qj->ij", w, self.phi, self.phi)
+        minv = np.linalg.inv(mref)
+        kref = np.einsum("q,qjk,qi->kji", w, self.dphi, self.phi)
+        pref = np.einsum("ij,kjl->kil", minv, kref)
+        eref = np.einsum("q,kqi,qj->kij", self.facet_wts, self.phi_face, self.fphi)
+        return minv, pref, kref, eref
+
     @property
     def face_w(self):
         return (self.facet_wts[None, None, :] * self.face_area[:, :, None])

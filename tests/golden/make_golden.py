@@ -27,6 +27,10 @@ Cases
                    10 steps
   cons_k2_lf       conservative formulation, LF flux (format coverage)
   fs_k2_es         free-stream boundary on a non-periodic box (ghost flux)
+  visc_*           viscous operator (gradient unknowns q, level-1 condensation):
+                   perturbed states with q = solve_gradient + 0.05 N(0,1) at
+                   Re=100, M=0.5; and the config-4 Taylor-Green parameters
+                   (Re=1600/M, M=0.1, Pr=0.71) on the projected TGV field
 """
 
 from __future__ import annotations
@@ -43,7 +47,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 from macrohdg.assembly import Discretization, FieldSet, FreeStream, StageContext  # noqa: E402
 from macrohdg.cases import IsentropicVortex  # noqa: E402
 from macrohdg.fluxes import DissipationSpec  # noqa: E402
-from macrohdg.gas import GasModel  # noqa: E402
+from macrohdg.cases import TaylorGreen  # noqa: E402
+from macrohdg.gas import GasModel, ViscousParams  # noqa: E402
 from macrohdg.mesh import build_box_macro_mesh  # noqa: E402
 from macrohdg.time_march import DIRKIntegrator, dirk33_tableau  # noqa: E402
 
@@ -106,7 +111,64 @@ def meta(disc, flux, formulation, box, n, m, p, periodic=True):
                 flux=flux, formulation=formulation, periodic=np.asarray(periodic))
 
 
+def viscous_case(name, disc, fields, alpha, ptc, x, extra):
+    """Viscous operator outputs (assembly.py:326-411, 459-549, 772-976,
+    1028-1173) on the given fields (with q)."""
+    offset = -alpha * disc.volume_quad_states(fields)
+    stage = StageContext(alpha=alpha, offset=offset, dt=None)
+
+    def run(f):
+        res = disc.residuals(f, stage)
+        lin = disc.jacobian(f, stage, ptc_weight=ptc)
+        d_w, d_q = lin.recover(res, x)
+        return dict(r_w=res.r_w, r_trace=res.r_trace, r_q=res.r_q, matvec=lin.matvec(x),
+                    rhs=lin.condensed_rhs(res), recover=d_w, recover_q=d_q,
+                    precond=lin.apply_preconditioner(x), vqs=disc.volume_quad_states(f),
+                    qgrad=disc.solve_gradient(f))
+
+    out = run(fields)
+    rng = np.random.default_rng(99)
+    pf = FieldSet(w=ulp_perturb(fields.w, rng), trace=ulp_perturb(fields.trace, rng),
+                  q=ulp_perturb(fields.q, rng))
+    pert = run(pf)
+    sens = {f"sens_{k}": rel(pert[k], out[k]) for k in out}
+    save(name, w=fields.w, trace=fields.trace, q=fields.q, offset=offset, alpha=alpha, ptc=ptc,
+         x=x, **out, **sens, **extra)
+
+
+def main_viscous():
+    box3 = np.array([[0.0, 1.0]] * 3)
+    vp = ViscousParams(reynolds=100.0, mach=0.5)
+    for p, flux, form in ((1, "kepes", "entropy"), (2, "kepes", "entropy"), (3, "es", "entropy"),
+                          (2, "lf", "conservative")):
+        mesh = build_box_macro_mesh(box3, (2, 2, 2), 1)
+        disc = Discretization(mesh, p=p, gas=GAS, formulation=form, flux=DissipationSpec(flux),
+                              viscosity=vp)
+        seed = 2000 + 10 * p
+        fields = perturbed_uniform(disc, seed)
+        rng = np.random.default_rng(seed + 5)
+        fields.q = disc.solve_gradient(fields) + 0.05 * rng.standard_normal(
+            fields.w.shape + (3,))
+        x = np.random.default_rng(seed + 1).standard_normal(fields.trace.shape)
+        viscous_case(f"visc_k{p}_{flux}_{form[:4]}", disc, fields, 40.0, 1.0, x,
+                     dict(**meta(disc, flux, form, box3, (2, 2, 2), 1, p), reynolds=100.0,
+                          mach=0.5, prandtl=0.72, mu=1.0))
+    # Taylor-Green parameters of config 4 (Re 1600 convective -> 16000, Pr 0.71)
+    tg = TaylorGreen(mach=0.1, gas=GAS)
+    vp = tg.viscous_params(1600.0, prandtl=0.71)
+    mesh = build_box_macro_mesh(tg.box, 2, 1)
+    disc = Discretization(mesh, p=3, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("kepes"), viscosity=vp)
+    fields = disc.project(tg.initial)
+    x = np.random.default_rng(31).standard_normal(fields.trace.shape)
+    viscous_case("visc_tgv_k3_kepes", disc, fields, 2.29 / 0.57, 1.0, x,
+                 dict(**meta(disc, "kepes", "entropy", tg.box, 2, 1, 3),
+                      reynolds=vp.reynolds, mach=vp.mach, prandtl=vp.prandtl, mu=vp.mu))
+
+
 def main():
+    if "--only-viscous" in sys.argv:
+        return main_viscous()
     t0 = time.time()
     tab = dirk33_tableau()
     d00 = tab.d[0, 0]
@@ -208,6 +270,7 @@ def main():
     save("cfg1_steps", w0=fields.w, trace0=fields.trace, w1=states[1][0],
          trace1=states[1][1], w10=states[10][0], trace10=states[10][1],
          integrals=hist_arr, newton=newton, dt=dt, tableau_d=tab.d, tableau_e=tab.e)
+    main_viscous()
     print(f"done in {time.time() - t0:.1f} s")
 
 

@@ -62,13 +62,10 @@ def test_partitioned_kernels_match_single_device(cuda_ok, world):
         rts.append(res.r_trace)
         lin = LinearizedSystem.__new__(LinearizedSystem)
         lin.disc, lin.viscous, lin.trace_shape = d, False, tuple(trl.shape)
-        for name, n in zip(("sinv", "hw", "hhat", "hh", "pinv"), d.lin_sizes):
-            setattr(lin, name, torch.empty(n, dtype=torch.float64, device=d.device))
-        lin._buf = N.LinBuffers(N.ptr(lin.sinv), N.ptr(lin.hw), N.ptr(lin.hhat), N.ptr(lin.hh),
-                                N.ptr(lin.pinv))
+        lin.alloc(d)
         stt = N.Status()
         wl_d, trl_d = d._fields(FieldSet(wl, trl))
-        rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(wl_d), N.ptr(trl_d), alpha, 1.0,
+        rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(wl_d), N.ptr(trl_d), None, alpha, 1.0,
                                          C.byref(lin._buf), C.byref(stt), N.stream_handle())
         assert rc == 0
         lins.append(lin)
