@@ -167,6 +167,10 @@ int mhdg_from_conservative(mhdg_ctx* ctx, int64_t n, const double* u, double* w,
  * entropy, thermo_entropy, kinetic_energy, mass, total_energy */
 int mhdg_integrals(mhdg_ctx* ctx, const double* w, double* out_host,
                    void* stream);
+/* Discretization.kinetic_energy_dissipation numerator (assembly.py:622-648):
+ * out_host[0] = 2 mu_eff * integral of rho |curl V|^2 / 2 (divide by |Omega|) */
+int mhdg_dissipation(mhdg_ctx* ctx, const double* w, const double* q,
+                     double* out_host, void* stream);
 
 /* FGMRES vector kernels (solver.py:42-118), deterministic reductions.
  * mhdg_dot: out_dev[0] = x . y

@@ -360,6 +360,16 @@ class Discretization:
         keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
         return {k: float(out[i]) for i, k in enumerate(keys)}
 
+    def kinetic_energy_dissipation(self, fields):
+        """eps = (2 mu_eff / |Omega|) int rho |curl V|^2 / 2 (assembly.py:622-648)."""
+        if self.viscosity is None:
+            raise InvalidConfig("dissipation rate needs a viscous setup")
+        out = (C.c_double * 1)()
+        rc = self._lib.mhdg_dissipation(self._ctx, N.ptr(self._dev(fields.w)), N.ptr(self._q(fields)),
+                                        out, N.stream_handle())
+        N.raise_for(rc)
+        return float(out[0]) / self.domain_volume
+
     def total_generalized_entropy(self, fields):
         v = self.integrals(fields)
         return v["entropy"], v["thermo_entropy"]

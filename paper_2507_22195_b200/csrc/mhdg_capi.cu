@@ -657,6 +657,28 @@ __global__ void k_reduce_rows(int nblk, int ncol, const double* __restrict__ par
   }
 }
 
+extern "C" int mhdg_dissipation(mhdg_ctx* c, const double* w, const double* q, double* out_host, void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  if (!c->visc) return MHDG_INVALID_CONFIG;
+  const int nblk = grid_for(c, c->E, 4);
+  double* part = c->d_partial;
+  double* res = c->d_partial + 2 * RED_BLOCKS * 5;
+  switch (c->p) {
+    case 1: k_dissipation<1, 64><<<nblk, 64, 0, s>>>(c->geo, c->vg, w, q, part); break;
+    case 2: k_dissipation<2, 64><<<nblk, 64, 0, s>>>(c->geo, c->vg, w, q, part); break;
+    case 3: k_dissipation<3, 64><<<nblk, 64, 0, s>>>(c->geo, c->vg, w, q, part); break;
+    default: k_dissipation<4, 128><<<nblk, 128, 0, s>>>(c->geo, c->vg, w, q, part); break;
+  }
+  k_reduce_rows<<<1, 32, 0, s>>>(nblk, 1, part, res);
+  c->launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out_host, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out_host[0] = 2.0 * c->vg.mu_eff * out_host[0];
+  return MHDG_OK;
+}
+
 extern "C" int mhdg_integrals(mhdg_ctx* c, const double* w, double* out_host, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));

@@ -763,4 +763,51 @@ k_visc_dq(Geo g, ViscGeo vg, const double* __restrict__ r_q, const double* __res
   }
 }
 
+// kinetic-energy dissipation partial sums: sum vol_w 0.5 rho |curl V|^2
+// (assembly.py:622-648)
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_dissipation(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __restrict__ q,
+              double* __restrict__ partial) {
+  using D = Dims<P>;
+  constexpr int NN = D::NN, NQ = D::NQ;
+  __shared__ double sW[NN * 5], sQ[NN * 15], red[NT];
+  double acc = 0.0;
+  const double gam = g.gamma;
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
+    for (int i = threadIdx.x; i < NN * 15; i += NT) sQ[i] = q[(size_t)e * NN * 15 + i];
+    __syncthreads();
+    for (int qp = threadIdx.x; qp < NQ; qp += NT) {
+      const double* ph = g.B + ((size_t)qp * 4 + 3) * NN;
+      double wq[5] = {0, 0, 0, 0, 0}, qq[5][3];
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
+      for (int i = 0; i < NN; ++i) {
+        const double a = __ldg(ph + i);
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) {
+          wq[s2] += a * sW[i * 5 + s2];
+#pragma unroll
+          for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQ[i * 15 + s2 * 3 + b];
+        }
+      }
+      double u[5], gv[3][3], gt[3];
+      to_conservative(wq, g.form, gam, u);
+      vt_grads(g.form, wq, u, qq, gam, gv, gt);
+      const double wx = gv[2][1] - gv[1][2], wy = gv[0][2] - gv[2][0], wz = gv[1][0] - gv[0][1];
+      const double om2 = (wx * wx + wy * wy) + wz * wz;
+      acc += g.qw[qp] * g.det[e] * 0.5 * u[0] * om2;
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int sft = NT / 2; sft > 0; sft >>= 1) {
+    if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
 }  // namespace mhdg

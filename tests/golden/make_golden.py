@@ -166,9 +166,29 @@ def main_viscous():
                       reynolds=vp.reynolds, mach=vp.mach, prandtl=vp.prandtl, mu=vp.mu))
 
 
+def main_viscous_steps():
+    """One DIRK(3,3) step of the viscous Taylor-Green vortex (config-4
+    parameters, KEPES) on n=2, p=2, dt = 0.057 t_c."""
+    tg = TaylorGreen(mach=0.1, gas=GAS)
+    disc = Discretization(build_box_macro_mesh(tg.box, 2, 1), p=2, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("kepes"), viscosity=tg.viscous_params(1600.0, 0.71))
+    f0 = disc.project(tg.initial)
+    integ = DIRKIntegrator(disc)
+    f1, _ = integ.run(f0, t_final=0.57, dt=0.57)
+    keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"], r["fgmres_iters"],
+                        r["jacobian_builds"]] for r in integ.records])
+    save("visc_tgv_steps", w0=f0.w, trace0=f0.trace, q0=f0.q, w1=f1.w, trace1=f1.trace, q1=f1.q,
+         integrals=np.array([[disc.integrals(f)[k] for k in keys] for f in (f0, f1)]),
+         dissipation=np.array([disc.kinetic_energy_dissipation(f) for f in (f0, f1)]),
+         newton=newton, dt=0.57)
+
+
 def main():
     if "--only-viscous" in sys.argv:
         return main_viscous()
+    if "--only-visc-steps" in sys.argv:
+        return main_viscous_steps()
     t0 = time.time()
     tab = dirk33_tableau()
     d00 = tab.d[0, 0]
@@ -271,6 +291,7 @@ def main():
          trace1=states[1][1], w10=states[10][0], trace10=states[10][1],
          integrals=hist_arr, newton=newton, dt=dt, tableau_d=tab.d, tableau_e=tab.e)
     main_viscous()
+    main_viscous_steps()
     print(f"done in {time.time() - t0:.1f} s")
 
 

@@ -61,3 +61,33 @@ def test_cfg1_ten_steps(cuda_ok):
     assert np.array_equal(np.sign(dh_got), np.sign(dh_want))
     newton = np.array([[r["step"], r["stage"], r["newton_iters"]] for r in integ.records])
     assert np.array_equal(newton, z["newton"][:, :3])
+
+
+def test_viscous_tgv_step(cuda_ok):
+    """One DIRK step of the viscous Taylor-Green vortex (config-4 parameters,
+    KEPES, n=2, p=2, dt=0.57) against the reference: converged state incl. q,
+    Newton iteration counts, integrals and kinetic-energy dissipation."""
+    from paper_2507_22195_b200 import Discretization, DissipationSpec, GasModel, TaylorGreen
+    from paper_2507_22195_b200.assembly import FieldSet
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+    from paper_2507_22195_b200.time_march import DIRKIntegrator
+
+    z = load_golden("visc_tgv_steps")
+    gas = GasModel(1.4)
+    tg = TaylorGreen(mach=0.1, gas=gas)
+    disc = Discretization(build_box_macro_mesh(tg.box, 2, 1), p=2, gas=gas, formulation="entropy",
+                          flux=DissipationSpec("kepes"), viscosity=tg.viscous_params(1600.0, 0.71),
+                          device="cuda:0")
+    f0 = FieldSet(z["w0"], z["trace0"], z["q0"])
+    proj = disc.project(tg.initial)
+    assert rel(proj.q, z["q0"]) <= 1e-12
+    integ = DIRKIntegrator(disc)
+    f1, _ = integ.run(f0, t_final=float(z["dt"]), dt=float(z["dt"]))
+    assert rel(f1.w, z["w1"]) <= 1e-10 and rel(f1.trace, z["trace1"]) <= 1e-10
+    assert rel(f1.q, z["q1"]) <= 1e-10
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"]] for r in integ.records])
+    assert np.array_equal(newton, z["newton"][:, :3])
+    got = np.array([[disc.integrals(f)[k] for k in KEYS] for f in (f0, f1)])
+    assert np.all(np.abs(got - z["integrals"]) <= 1e-12 * np.maximum(1.0, np.abs(z["integrals"])))
+    eps = np.array([disc.kinetic_energy_dissipation(f) for f in (f0, f1)])
+    assert np.all(np.abs(eps - z["dissipation"]) <= 1e-12 * np.abs(z["dissipation"]))
