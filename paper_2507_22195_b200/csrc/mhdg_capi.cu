@@ -457,6 +457,34 @@ extern "C" int mhdg_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, int n
 // condensed operator
 // ---------------------------------------------------------------------------
 template <int P>
+static int condensed_face2(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
+                           double* y, double* dw, cudaStream_t s) {
+  using D = Dims<P>;
+  using F2 = Face2<P>;
+  const size_t fsm = F2::bytes;
+  if (set_smem(k_face2<P, 0>, fsm) || set_smem(k_face2<P, 1>, fsm)) return MHDG_CUDA_ERROR;
+  const int nb = (c->E + F2::EB - 1) / F2::EB;
+  double* gbuf = c->d_gbuf;
+  double* zbuf = (mode == 2) ? dw : c->d_zbuf;
+  if (mode != 1) {
+    k_face2<P, 0><<<grid_for(c, nb, occ(k_face2<P, 0>, 128, fsm)), 128, fsm, s>>>(c->geo, mode, L->hhat, nullptr, x,
+                                                                                  nullptr, rw, gbuf);
+    c->launches++;
+  }
+  constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
+  k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(
+      c->E, L->sinv, mode == 1 ? rw : gbuf, mode == 1, zbuf);
+  c->launches++;
+  if (mode != 2) {
+    k_face2<P, 1><<<grid_for(c, nb, occ(k_face2<P, 1>, 128, fsm)), 128, fsm, s>>>(c->geo, mode, L->hw, L->hh, x,
+                                                                                  zbuf, nullptr, y);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
+template <int P>
 static int condensed_split(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
                            double* y, double* dw, cudaStream_t s) {
   using D = Dims<P>;
@@ -518,10 +546,10 @@ static int condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const dou
     }
   }
   switch (c->p) {
-    case 1: return condensed_split<1>(c, mode, L, x, rw, y, dw, s);
-    case 2: return condensed_split<2>(c, mode, L, x, rw, y, dw, s);
-    case 3: return condensed_split<3>(c, mode, L, x, rw, y, dw, s);
-    default: return condensed_split<4>(c, mode, L, x, rw, y, dw, s);
+    case 1: return condensed_face2<1>(c, mode, L, x, rw, y, dw, s);
+    case 2: return condensed_face2<2>(c, mode, L, x, rw, y, dw, s);
+    case 3: return condensed_face2<3>(c, mode, L, x, rw, y, dw, s);
+    default: return condensed_face2<4>(c, mode, L, x, rw, y, dw, s);
   }
 }
 

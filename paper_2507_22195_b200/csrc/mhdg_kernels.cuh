@@ -1506,6 +1506,241 @@ k_face_pipe(Geo g, int mode, const double* __restrict__ tenA, const double* __re
   }
 }
 
+// Register-blocked face kernels: one thread per (macro slot, tile, face
+// point); its 25-entry tensor rows for the NEXT macro batch are prefetched
+// straight into registers (no shared-memory staging of the 12.8 KB/macro
+// tensors), and every shared-memory read feeds a 5-wide register block.
+template <int P>
+struct Face2 {
+  using D = Dims<P>;
+  static constexpr int NI = 4 * D::NQF;                        // items per macro
+  static constexpr int NT = 128;
+  static constexpr int EB = (NT / NI) > 0 ? (NT / NI) : 1;    // macros per iteration
+  static constexpr int IPT = (EB * NI + NT - 1) / NT;          // items per thread
+  static constexpr int NX = 4 * D::NFN * 5;
+  static constexpr int XPT = (EB * NX + NT - 1) / NT;
+  static constexpr int ZPT = (EB * D::NM + NT - 1) / NT;
+  static constexpr int META = 4 + 4 * D::NFN;
+  static constexpr int MPT = (EB * (META + 4) + NT - 1) / NT;
+  static constexpr int doubles = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQF + EB * (NX + D::NM + 2 * NI * 5 + NX) +
+                                 3 * EB * 4;
+  static constexpr int ints = 4 * D::NFN + 3 * D::NN + 3 * EB * META;
+  static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
+};
+
+template <int P, int MODE>   // MODE 0: g = -A_vh x (+ -r_w); 1: y += A_hh x + A_hv z
+__global__ void __launch_bounds__(128, 3)
+k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restrict__ tenB,
+        const double* __restrict__ x, const double* __restrict__ zin, const double* __restrict__ r_w,
+        double* __restrict__ out) {
+  using D = Dims<P>;
+  using F2 = Face2<P>;
+  constexpr int NM = D::NM, NFN = D::NFN, NQF = D::NQF, NN = D::NN, NI = F2::NI, NX = F2::NX, META = F2::META;
+  constexpr int NT = F2::NT, EB = F2::EB;
+  const bool use_x = (MODE == 0) || mode == 0;
+  const bool use_b = (MODE == 1) && mode == 0;
+  extern __shared__ __align__(16) double smem[];
+  double* sPF = smem;
+  double* sFP = sPF + 4 * NQF * D::FS;
+  double* sFW = sFP + NQF * D::FS;
+  double* sX = sFW + NQF;                 // EB*NX
+  double* sZ = sX + EB * NX;              // EB*NM
+  double* sA = sZ + EB * NM;              // EB*NI*5
+  double* sB = sA + EB * NI * 5;          // EB*NI*5
+  double* sT = sB + EB * NI * 5;          // EB*NX
+  double* sAr = sT + EB * NX;             // 3*EB*4
+  int* sRows = (int*)(sAr + 3 * EB * 4);
+  int* sNF = sRows + 4 * NFN;
+  int* sMeta = sNF + 3 * NN;              // 3*EB*META
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
+  for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
+  for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
+  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
+  for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
+  const int G = gridDim.x * EB;
+  auto meta_elem = [&](int e0, int i, int& iv, double& dv) {   // i over EB*(META+4)
+    const int m = i / (META + 4), r = i % (META + 4), e = e0 + m;
+    if (e >= g.E) return;
+    if (r < 4) iv = g.fid[e * 4 + r];
+    else if (r < META) iv = g.tidx[(size_t)e * 4 * NFN + r - 4];
+    else dv = g.area[(size_t)e * 4 + r - META];
+  };
+  auto meta_put = [&](int slot, int i, int iv, double dv) {
+    const int m = i / (META + 4), r = i % (META + 4);
+    if (r < META) sMeta[(slot * EB + m) * META + r] = iv;
+    else sAr[(slot * EB + m) * 4 + r - META] = dv;
+  };
+  const int e00 = blockIdx.x * EB;
+  for (int c = 0; c < 2; ++c)
+    for (int i = tid; i < EB * (META + 4); i += NT) {
+      int iv = 0;
+      double dv = 0.0;
+      meta_elem(e00 + c * G, i, iv, dv);
+      meta_put(c, i, iv, dv);
+    }
+  __syncthreads();
+  double rA[F2::IPT][25], rB[F2::IPT][25], rX[F2::XPT], rZ[F2::ZPT], rMd[F2::MPT];
+  int rMi[F2::MPT];
+  auto prefetch = [&](int e0, int slot) {
+#pragma unroll
+    for (int c = 0; c < F2::IPT; ++c) {
+      const int it = tid + c * NT, m = it / NI, e = e0 + m;
+      if (it < EB * NI && e < g.E) {
+        const double2* pa = reinterpret_cast<const double2*>(tenA + ((size_t)e * NI + it % NI) * 25);
+        // rows start at 25*8*item bytes: 8-byte aligned only for odd items -> scalar loads
+#pragma unroll
+        for (int u = 0; u < 25; ++u) rA[c][u] = __ldcs(tenA + ((size_t)e * NI + it % NI) * 25 + u);
+        if (use_b)
+#pragma unroll
+          for (int u = 0; u < 25; ++u) rB[c][u] = __ldcs(tenB + ((size_t)e * NI + it % NI) * 25 + u);
+        (void)pa;
+      }
+    }
+    if (use_x) {
+#pragma unroll
+      for (int c = 0; c < F2::XPT; ++c) {
+        const int i = tid + c * NT, m = i / NX, r = i % NX, e = e0 + m;
+        if (i < EB * NX && e < g.E) {
+          const int* mt = sMeta + (slot * EB + m) * META;
+          const int k = r / (NFN * 5), j = (r / 5) % NFN, s2 = r % 5;
+          rX[c] = x[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s2];
+        }
+      }
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int c = 0; c < F2::ZPT; ++c) {
+        const int i = tid + c * NT, m = i / NM, e = e0 + m;
+        if (i < EB * NM && e < g.E) rZ[c] = zin[(size_t)e * NM + i % NM];
+      }
+    }
+  };
+  if (e00 < g.E) prefetch(e00, 0);
+  int slot = 0;
+  for (int e0 = e00; e0 < g.E; e0 += G, slot = (slot + 1) % 3) {
+    const int e1 = e0 + G, e2 = e0 + 2 * G;
+    const int s1 = (slot + 1) % 3, s2s = (slot + 2) % 3;
+    const int nm = min(EB, g.E - e0);
+    __syncthreads();
+    if (use_x) {
+#pragma unroll
+      for (int c = 0; c < F2::XPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < EB * NX) sX[i] = rX[c];
+      }
+    }
+    if (MODE == 1) {
+#pragma unroll
+      for (int c = 0; c < F2::ZPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < EB * NM) sZ[i] = rZ[c];
+      }
+    }
+    __syncthreads();
+    // ---- phase 1: per (slot m, tile k, point q): 5-vectors at the point
+    if (e2 < g.E) {
+#pragma unroll
+      for (int c = 0; c < F2::MPT; ++c) {
+        const int i = tid + c * NT;
+        rMi[c] = 0;
+        rMd[c] = 0.0;
+        if (i < EB * (META + 4)) meta_elem(e2, i, rMi[c], rMd[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < F2::IPT; ++c) {
+      const int it = tid + c * NT, m = it / NI, kq = it % NI, k = kq / NQF, q = kq % NQF;
+      if (it < EB * NI && m < nm) {
+        const double fwq = sFW[q] * sAr[(slot * EB + m) * 4 + k];
+        double xq[5] = {0, 0, 0, 0, 0}, zq[5] = {0, 0, 0, 0, 0};
+        if (use_x) {
+          const double* fp = sFP + q * D::FS;
+          const double* xs = sX + m * NX + k * NFN * 5;
+#pragma unroll
+          for (int j = 0; j < NFN; ++j) {
+            const double f = fp[j];
+#pragma unroll
+            for (int t = 0; t < 5; ++t) xq[t] += f * xs[j * 5 + t];
+          }
+        }
+        if (MODE == 1) {
+          const double* pf = sPF + kq * D::FS;
+          const double* zs = sZ + m * NM;
+#pragma unroll
+          for (int j = 0; j < NFN; ++j) {
+            const double f = pf[j];
+            const int row = sRows[k * NFN + j];
+#pragma unroll
+            for (int t = 0; t < 5; ++t) zq[t] += f * zs[row * 5 + t];
+          }
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) {
+          double a = 0.0, b = 0.0;
+#pragma unroll
+          for (int t = 0; t < 5; ++t) {
+            a += rA[c][s2 * 5 + t] * (MODE == 0 ? xq[t] : zq[t]);
+            if (use_b) b += rB[c][s2 * 5 + t] * xq[t];
+          }
+          sA[it * 5 + s2] = fwq * a;
+          if (use_b) sB[it * 5 + s2] = fwq * b;
+        }
+      }
+    }
+    // next batch: tensor rows / trace values / z into the same registers
+    if (e1 < g.E) prefetch(e1, s1);
+    __syncthreads();
+    // ---- phase 2: per (slot m, tile k, node j): 5 outputs
+    for (int o = tid; o < nm * 4 * NFN; o += NT) {
+      const int m = o / (4 * NFN), kj = o % (4 * NFN), k = kj / NFN, j = kj % NFN;
+      double a[5] = {0, 0, 0, 0, 0}, b[5] = {0, 0, 0, 0, 0};
+      const double* A = sA + (m * NI + k * NQF) * 5;
+      const double* B = sB + (m * NI + k * NQF) * 5;
+#pragma unroll 4
+      for (int q = 0; q < NQF; ++q) {
+        const double f = (MODE == 0) ? sPF[(k * NQF + q) * D::FS + j] : sFP[q * D::FS + j];
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) {
+          a[s2] += f * A[q * 5 + s2];
+          if (use_b) b[s2] += f * B[q * 5 + s2];
+        }
+      }
+      if (MODE == 0) {
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) sT[m * NX + kj * 5 + s2] = a[s2];
+      } else {
+        const int* mt = sMeta + (slot * EB + m) * META;
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2)
+          atomicAdd(&out[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s2], b[s2] + a[s2]);
+      }
+    }
+    if (MODE == 0) {
+      __syncthreads();
+      for (int o = tid; o < nm * NM; o += NT) {
+        const int m = o / NM, r = o % NM, i = r / 5, s2 = r % 5;
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int kj = sNF[i * 3 + c];
+          if (kj < 0) break;
+          v += sT[m * NX + kj * 5 + s2];
+        }
+        const size_t gi = (size_t)(e0 + m) * NM + r;
+        out[gi] = (mode == 0) ? -v : (-r_w[gi] + (-v));
+      }
+    }
+    if (e2 < g.E) {
+#pragma unroll
+      for (int c = 0; c < F2::MPT; ++c) {
+        const int i = tid + c * NT;
+        if (i < EB * (META + 4)) meta_put(s2s, i, rMi[c], rMd[c]);
+      }
+    }
+  }
+}
+
 // K4 (apply): z_f = P_f^-1 r_f, column-major GEMV per face
 template <int P, int NT>
 __global__ void __launch_bounds__(NT)
