@@ -14,6 +14,7 @@
 #include "../../include/mhdg_b200.h"
 #include "mhdg_kernels.cuh"
 #include "mhdg_viscous.cuh"
+#include "mhdg_visc_fast.cuh"
 
 using namespace mhdg;
 
@@ -149,6 +150,61 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
     c->vg.pref = upload(c, t->pref, (size_t)3 * NN * NN, err);
     c->vg.kref = upload(c, t->kref, (size_t)3 * NN * NN, err);
     c->vg.eref = upload(c, t->eref, (size_t)4 * NFN * NFN, err);
+    // point tables: products of the reference matrices evaluated at the
+    // volume and face quadrature points (fewer per-matvec contractions)
+    const int NPT = NQ + 4 * NQF;
+    std::vector<double> phi_pt((size_t)NPT * NN, 0.0);
+    for (int q = 0; q < NQ; ++q)
+      for (int i = 0; i < NN; ++i) phi_pt[(size_t)q * NN + i] = t->phi[(size_t)q * NN + i];
+    for (int it = 0; it < 4 * NQF; ++it) {
+      const int k = it / NQF;
+      for (int j = 0; j < NFN; ++j)
+        phi_pt[(size_t)(NQ + it) * NN + t->face_rows[k * NFN + j]] = t->phi_face[(size_t)it * NFN + j];
+    }
+    std::vector<double> pm((size_t)NPT * NN, 0.0), phit((size_t)NN * NPT), pmt((size_t)NN * NPT);
+    for (int pt = 0; pt < NPT; ++pt)
+      for (int j = 0; j < NN; ++j) {
+        double a = 0.0;
+        for (int l = 0; l < NN; ++l) a += phi_pt[(size_t)pt * NN + l] * t->minv_ref[(size_t)l * NN + j];
+        pm[(size_t)pt * NN + j] = a;
+        pmt[(size_t)j * NPT + pt] = a;
+        phit[(size_t)j * NPT + pt] = phi_pt[(size_t)pt * NN + j];
+      }
+    std::vector<double> cxt((size_t)4 * NFN * NPT), dzt((size_t)3 * NN * NPT), tpp((size_t)3 * NPT * NN);
+    for (int pt = 0; pt < NPT; ++pt) {
+      for (int k = 0; k < 4; ++k)
+        for (int jj = 0; jj < NFN; ++jj) {
+          double a = 0.0;
+          for (int ip = 0; ip < NFN; ++ip)
+            a += pm[(size_t)pt * NN + t->face_rows[k * NFN + ip]] * t->eref[((size_t)k * NFN + ip) * NFN + jj];
+          cxt[((size_t)k * NFN + jj) * NPT + pt] = -a;
+        }
+      for (int k2 = 0; k2 < 3; ++k2)
+        for (int i = 0; i < NN; ++i) {
+          double a = 0.0, b = 0.0;
+          for (int j = 0; j < NN; ++j) {
+            a += pm[(size_t)pt * NN + j] * t->kref[((size_t)k2 * NN + j) * NN + i];
+            b += phi_pt[(size_t)pt * NN + j] * t->pref[((size_t)k2 * NN + j) * NN + i];
+          }
+          dzt[((size_t)k2 * NN + i) * NPT + pt] = a;
+          tpp[((size_t)k2 * NPT + pt) * NN + i] = b;
+        }
+    }
+    const int NK = 3 * NQ + 4 * NQF, NKP = (NK + 3) / 4 * 4, NNP = (NN + 7) / 8 * 8;
+    std::vector<double> tst((size_t)NKP * NNP, 0.0);
+    for (int q = 0; q < NQ; ++q)
+      for (int kk = 0; kk < 3; ++kk)
+        for (int i = 0; i < NN; ++i) tst[(size_t)(q * 3 + kk) * NNP + i] = B[((size_t)q * 4 + kk) * NN + i];
+    for (int it = 0; it < 4 * NQF; ++it)
+      for (int i = 0; i < NN; ++i) tst[(size_t)(3 * NQ + it) * NNP + i] = phi_pt[(size_t)(NQ + it) * NN + i];
+    c->vg.tst = upload(c, tst.data(), tst.size(), err);
+    c->vg.npt = NPT;
+    c->vg.phit = upload(c, phit.data(), phit.size(), err);
+    c->vg.phipt = upload(c, phi_pt.data(), phi_pt.size(), err);
+    c->vg.pmt = upload(c, pmt.data(), pmt.size(), err);
+    c->vg.cxt = upload(c, cxt.data(), cxt.size(), err);
+    c->vg.dzt = upload(c, dzt.data(), dzt.size(), err);
+    c->vg.tpp = upload(c, tpp.data(), tpp.size(), err);
   }
   c->d_status = (unsigned long long*)dalloc(c, sizeof(unsigned long long) * 4, err);
   c->d_unsym = (int*)dalloc(c, sizeof(int) * 4, err);
@@ -314,9 +370,10 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
     int grid = grid_for(c, c->E, occ(k_linearize2<P, true>, 256, smem));
     k_linearize2<P, true><<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat,
                                                   L->hh, c->d_status);
-    const size_t csm = SCorr<P>::bytes;
-    if (set_smem(k_visc_scorr<P>, csm)) return MHDG_CUDA_ERROR;
-    k_visc_scorr<P><<<grid_for(c, c->E, occ(k_visc_scorr<P>, 256, csm)), 256, csm, s>>>(c->geo, c->vg, w, L->sinv);
+    const size_t csm = SCorr2<P>::bytes;
+    if (set_smem(k_visc_scorr2<P>, csm)) return MHDG_CUDA_ERROR;
+    k_visc_scorr2<P><<<grid_for(c, c->E, occ(k_visc_scorr2<P>, 256, csm)), 256, csm, s>>>(c->geo, c->vg, w,
+                                                                                           L->sinv);
     c->launches += 2;
     CK(cudaMemcpyAsync(L->wlin, w, sizeof(double) * (size_t)c->E * c->nn * 5, cudaMemcpyDeviceToDevice, s));
   } else {
@@ -516,19 +573,21 @@ template <int P>
 static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
                           const double* rq, double* y, double* dw, cudaStream_t s) {
   using D = Dims<P>;
-  const size_t vsm = VOp<P>::bytes;
-  if (set_smem(k_visc_in<P>, vsm) || set_smem(k_visc_out<P>, vsm)) return MHDG_CUDA_ERROR;
+  using V = VFast<P>;
+  const size_t ism = sizeof(typename V::In) * V::MBI, osm = sizeof(typename V::Out) * V::MBO;
+  if (set_smem(k_visc_in2<P>, ism) || set_smem(k_visc_out2<P>, osm)) return MHDG_CUDA_ERROR;
   double* gbuf = c->d_gbuf;
   double* zbuf = (mode == 2) ? dw : c->d_zbuf;
-  k_visc_in<P><<<grid_for(c, c->E, occ(k_visc_in<P>, 128, vsm)), 128, vsm, s>>>(c->geo, c->vg, mode, L->wlin, L->hhat,
-                                                                              x, rw, rq, gbuf);
+  const int nbi = (c->E + V::MBI - 1) / V::MBI, nbo = (c->E + V::MBO - 1) / V::MBO;
+  k_visc_in2<P><<<grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s>>>(c->geo, c->vg, mode, L->wlin,
+                                                                                 L->hhat, x, rw, rq, gbuf);
   constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
   k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(c->E, L->sinv,
                                                                                                  gbuf, 0, zbuf);
   c->launches += 2;
   if (mode != 2) {
-    k_visc_out<P><<<grid_for(c, c->E, occ(k_visc_out<P>, 128, vsm)), 128, vsm, s>>>(c->geo, c->vg, mode, L->wlin, L->hh,
-                                                                                   L->hw, x, zbuf, rq, y);
+    k_visc_out2<P><<<grid_for(c, nbo, occ(k_visc_out2<P>, 128, osm)), 128, osm, s>>>(
+        c->geo, c->vg, mode, L->wlin, L->hh, L->hw, x, zbuf, rq, y);
     c->launches++;
   }
   CK(cudaGetLastError());

@@ -11,6 +11,16 @@ struct ViscGeo {
   const double* pref;              // (3, NN, NN) Mref^-1 Kref_k
   const double* kref;              // (3, NN, NN) Kref_k[j][i]
   const double* eref;              // (4, NFN, NFN) Eref_k[i][j]
+  // point tables (built at context creation; pt = NQ volume points, then the
+  // 4 NQF face points k*NQF+qf; phi_pt is dense over the NN macro nodes)
+  int npt;
+  const double* phit;              // (NN, NPT)   phi_pt^T
+  const double* phipt;             // (NPT, NN)   phi_pt
+  const double* pmt;               // (NN, NPT)   (phi_pt Mref^-1)^T
+  const double* cxt;               // (4, NFN, NPT)  -(phi_pt Mref^-1 R_k Eref_k)^T
+  const double* dzt;               // (3, NN, NPT)   (phi_pt Mref^-1 Kref_k)^T
+  const double* tpp;               // (3, NPT, NN)   phi_pt Pref_k
+  const double* tst;               // (NKP, NTI*8)   test rows: dphi_kk at (q,kk), then phi_pt at face pts
 };
 
 // velocity / temperature gradients from the working variables (gas.py:229-262)

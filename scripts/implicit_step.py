@@ -25,6 +25,7 @@ ap.add_argument("--p", type=int, default=3)
 ap.add_argument("--flux", default="es")
 ap.add_argument("--dt", type=float, default=0.01)
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--viscous", action="store_true")
 a = ap.parse_args()
 gas = GasModel(1.4)
 if a.case == "vortex":
@@ -35,7 +36,9 @@ else:
     box = case.box
 t0 = time.time()
 mesh = build_box_macro_mesh(box, a.n, 1)
-disc = Discretization(mesh, p=a.p, gas=gas, flux=DissipationSpec(a.flux), device="cuda:0")
+visc = case.viscous_params(1600.0, prandtl=0.71) if a.viscous else None
+disc = Discretization(mesh, p=a.p, gas=gas, flux=DissipationSpec(a.flux), viscosity=visc,
+                      device="cuda:0")
 fields = disc.project(case.initial)
 setup = time.time() - t0
 integ = DIRKIntegrator(disc)
@@ -47,6 +50,7 @@ wall = time.time() - t1
 keys = ("newton_iters", "fgmres_iters", "inner_iters_total", "jacobian_builds", "condense_seconds",
         "matvec_seconds", "recovery_seconds")
 tot = {k: sum(r[k] for r in integ.records) for k in keys}
-print(json.dumps({"case": a.case, "n": a.n, "p": a.p, "macros": mesh.n_macros, "setup_s": setup,
+print(json.dumps({"case": a.case, "viscous": a.viscous, "n": a.n, "p": a.p, "macros": mesh.n_macros,
+                  "setup_s": setup, "gpu_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
                   "steps": a.steps, "wall_s": wall, "s_per_step": wall / a.steps, "totals": tot,
                   "records": integ.records}))
