@@ -542,34 +542,6 @@ static int condensed_face2(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, con
 }
 
 template <int P>
-static int condensed_split(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
-                           double* y, double* dw, cudaStream_t s) {
-  using D = Dims<P>;
-  constexpr int NT = P >= 3 ? 256 : 128;
-  const size_t fsm = FacePipe<P, NT>::bytes;
-  if (set_smem(k_face_pipe<P, NT, 0>, fsm) || set_smem(k_face_pipe<P, NT, 1>, fsm)) return MHDG_CUDA_ERROR;
-  const int per_in = occ(k_face_pipe<P, NT, 0>, NT, fsm), per_out = occ(k_face_pipe<P, NT, 1>, NT, fsm);
-  double* gbuf = c->d_gbuf;
-  double* zbuf = (mode == 2) ? dw : c->d_zbuf;
-  if (mode != 1) {
-    k_face_pipe<P, NT, 0><<<grid_for(c, c->E, per_in), NT, fsm, s>>>(c->geo, mode, L->hhat, nullptr, x, nullptr,
-                                                                       rw, gbuf);
-    c->launches++;
-  }
-  constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
-  k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(c->E, L->sinv, mode == 1 ? rw : gbuf,
-                                                                 mode == 1, zbuf);
-  c->launches++;
-  if (mode != 2) {
-    k_face_pipe<P, NT, 1><<<grid_for(c, c->E, per_out), NT, fsm, s>>>(c->geo, mode, L->hw, L->hh, x, zbuf,
-                                                                       nullptr, y);
-    c->launches++;
-  }
-  CK(cudaGetLastError());
-  return MHDG_OK;
-}
-
-template <int P>
 static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
                           const double* rq, double* y, double* dw, cudaStream_t s) {
   using D = Dims<P>;

@@ -580,18 +580,18 @@ k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trac
         to_conservative(wd, g.form, gam, ud);
         to_conservative(whd, g.form, gam, uhd);
         numerical_flux(g.kind, ud, uhd, n, gam, fd);
-        const size_t base = (((size_t)e * 4 + k) * D::NQF + q) * 25;
+        const size_t base = ((size_t)e * 4 + k) * 25 * D::NQF + q;   // ten layout (E,4,25,NQF)
         if (which == 0) {
 #pragma unroll
           for (int s = 0; s < 5; ++s) {
-            hw_out[base + s * 5 + t] = fd[s].d;
+            hw_out[base + (s * 5 + t) * D::NQF] = fd[s].d;
             sHW[q * 25 + s * 5 + t] = fd[s].d;
           }
         } else {
           double hh[5];
 #pragma unroll
           for (int s = 0; s < 5; ++s) {
-            hhat_out[base + s * 5 + t] = fd[s].d;
+            hhat_out[base + (s * 5 + t) * D::NQF] = fd[s].d;
             hh[s] = fd[s].d;
           }
           if (sBnd[k] && g.has_uinf) {
@@ -608,7 +608,7 @@ k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trac
             for (int s = 0; s < 5; ++s) hh[s] = hh[s] + (-ptc * uhd[s].d);
           }
 #pragma unroll
-          for (int s = 0; s < 5; ++s) hh_out[base + s * 5 + t] = hh[s];
+          for (int s = 0; s < 5; ++s) hh_out[base + (s * 5 + t) * D::NQF] = hh[s];
         }
       }
       __syncthreads();
@@ -1067,18 +1067,18 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
             fd[s2] = fd[s2] + (gn - (0.5 * vg.pdiag[s2]) * (whd[s2] - wd[s2]));
           }
         }
-        const size_t base = (((size_t)e * 4 + k) * NQF + q) * 25;
+        const size_t base = ((size_t)e * 4 + k) * 25 * NQF + q;   // ten layout (E,4,25,NQF)
         if (which == 0) {
 #pragma unroll
           for (int s2 = 0; s2 < 5; ++s2) {
-            hw_out[base + s2 * 5 + t] = fd[s2].d;
+            hw_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
             sHW[q * 25 + s2 * 5 + t] = fd[s2].d;
           }
         } else {
           double hv[5];
 #pragma unroll
           for (int s2 = 0; s2 < 5; ++s2) {
-            hhat_out[base + s2 * 5 + t] = fd[s2].d;
+            hhat_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
             hv[s2] = fd[s2].d;
           }
           if (sBnd[k] && g.has_uinf) {
@@ -1102,7 +1102,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
             for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + (-ptc * uhd[s2].d);
           }
 #pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) hh_out[base + s2 * 5 + t] = hv[s2];
+          for (int s2 = 0; s2 < 5; ++s2) hh_out[base + (s2 * 5 + t) * NQF] = hv[s2];
         }
       }
       __syncthreads();
@@ -1167,12 +1167,14 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
       __syncthreads();
       if (st >= 0) {
         const int e = st / 4, k = st % 4;
-        for (int i = tid; i < D::NQF * 25; i += NT) sHH[i] = hh[((size_t)st * D::NQF) * 25 + i];
+        for (int i = tid; i < D::NQF * 25; i += NT)   // (25, NQF) per side -> [q][u]
+          sHH[(i % D::NQF) * 25 + i / D::NQF] = hh[((size_t)st * D::NQF) * 25 + i];
         for (int i = tid; i < D::NFN; i += NT) sT[i] = g.tidx[((size_t)e * 4 + k) * D::NFN + i];
         for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * g.area[(size_t)e * 4 + k];
       } else {  // remote side of a halo face (partitioned runs)
         const int r = -2 - st;
-        for (int i = tid; i < D::NQF * 25; i += NT) sHH[i] = hh_rem[(size_t)r * D::NQF * 25 + i];
+        for (int i = tid; i < D::NQF * 25; i += NT)
+          sHH[(i % D::NQF) * 25 + i / D::NQF] = hh_rem[(size_t)r * D::NQF * 25 + i];
         for (int i = tid; i < D::NFN; i += NT) sT[i] = tidx_rem[(size_t)r * D::NFN + i];
         for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * area_rem[r];
       }
@@ -1266,246 +1268,6 @@ k_local_solve(int E, const double* __restrict__ sinv, const double* __restrict__
   }
 }
 
-// Software-pipelined face kernels: while macro e is computed from shared
-// memory, every thread already holds in registers its share of macro
-// e+G's face tensors and trace values (G = grid size), and the metadata
-// (face ids, trace permutations, areas) of macro e+2G -- so none of the
-// three dependent global round trips sits on the critical path.
-template <int P, int NT>
-struct FacePipe {
-  using D = Dims<P>;
-  static constexpr int NI = 4 * D::NQF;
-  static constexpr int NTEN = NI * 25;
-  static constexpr int NX = 4 * D::NFN * 5;
-  static constexpr int TPT = (NTEN + NT - 1) / NT;   // tensor doubles / thread
-  static constexpr int XPT = (NX + NT - 1) / NT;
-  static constexpr int ZPT = (D::NM + NT - 1) / NT;
-  static constexpr int META = 4 + 4 * D::NFN;        // ints: fid, tidx
-  static constexpr int MPT = (META + 4 + NT - 1) / NT;
-  static constexpr int doubles = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQF + NX + 2 * NTEN + D::NM +
-                                 4 * NI * 5 + 3 * 4;
-  static constexpr int ints = 4 * D::NFN + 3 * D::NN + 3 * META;
-  static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
-};
-
-template <int P, int NT, int MODE>   // MODE 0: face_in (A_vh x), 1: face_out (A_hh x + A_hv z)
-__global__ void __launch_bounds__(NT)
-k_face_pipe(Geo g, int mode, const double* __restrict__ tenA, const double* __restrict__ tenB,
-            const double* __restrict__ x, const double* __restrict__ zin, const double* __restrict__ r_w,
-            double* __restrict__ out) {
-  using D = Dims<P>;
-  using FP = FacePipe<P, NT>;
-  constexpr int NM = D::NM, NFN = D::NFN, NQF = D::NQF, NN = D::NN, NI = FP::NI, NTEN = FP::NTEN,
-                NX = FP::NX, META = FP::META;
-  // face_in : tenA = hhat; needs x.              out = g (E, NM)
-  // face_out: tenA = hw (z side), tenB = hh (x side, matvec only); out = y
-  const bool use_x = (MODE == 0) || mode == 0;
-  const bool use_b = (MODE == 1) && mode == 0;
-  extern __shared__ __align__(16) double smem[];
-  double* sPF = smem;
-  double* sFP = sPF + 4 * NQF * D::FS;
-  double* sFW = sFP + NQF * D::FS;
-  double* sX = sFW + NQF;          // NX
-  double* sTA = sX + NX;           // NTEN
-  double* sTB = sTA + NTEN;        // NTEN
-  double* sZ = sTB + NTEN;         // NM
-  double* sQ1 = sZ + NM;           // NI*5
-  double* sQ2 = sQ1 + NI * 5;      // NI*5
-  double* sQ3 = sQ2 + NI * 5;      // NI*5
-  double* sQ4 = sQ3 + NI * 5;      // NI*5
-  double* sAr = sQ4 + NI * 5;      // 3 x 4
-  int* sRows = (int*)(sAr + 12);
-  int* sNF = sRows + 4 * NFN;
-  int* sMeta = sNF + 3 * NN;       // 3 x META
-  const int tid = threadIdx.x;
-  for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
-  for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
-  for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
-  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
-  for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
-  const int G = gridDim.x;
-  // metadata element i of macro e: i < 4 fid, < META tidx, else area (double)
-  auto meta_load = [&](int e, int i, int& iv, double& dv) {
-    if (i < 4) iv = g.fid[e * 4 + i];
-    else if (i < META) iv = g.tidx[(size_t)e * 4 * NFN + i - 4];
-    else if (i < META + 4) dv = g.area[(size_t)e * 4 + i - META];
-  };
-  auto meta_store = [&](int slot, int i, int iv, double dv) {
-    if (i < META) sMeta[slot * META + i] = iv;
-    else if (i < META + 4) sAr[slot * 4 + i - META] = dv;
-  };
-  // prologue: metadata of e0 and e0+G in slots 0, 1
-  const int e0 = blockIdx.x;
-  for (int c = 0; c < 2; ++c) {
-    const int e = e0 + c * G;
-    if (e < g.E)
-      for (int i = tid; i < META + 4; i += NT) {
-        int iv = 0;
-        double dv = 0.0;
-        meta_load(e, i, iv, dv);
-        meta_store(c, i, iv, dv);
-      }
-  }
-  __syncthreads();
-  double rA[FP::TPT], rB[FP::TPT], rX[FP::XPT], rZ[FP::ZPT], rMd[FP::MPT];
-  int rMi[FP::MPT];
-  auto prefetch = [&](int e, int slot) {  // tensors / x / z of macro e (meta in slot)
-    const int* mt = sMeta + slot * META;
-#pragma unroll
-    for (int c = 0; c < FP::TPT; ++c) {
-      const int i = tid + c * NT;
-      if (i < NTEN) {
-        rA[c] = __ldcs(tenA + (size_t)e * NTEN + i);
-        if (use_b) rB[c] = __ldcs(tenB + (size_t)e * NTEN + i);
-      }
-    }
-    if (use_x) {
-#pragma unroll
-      for (int c = 0; c < FP::XPT; ++c) {
-        const int i = tid + c * NT;
-        if (i < NX) {
-          const int k = i / (NFN * 5), j = (i / 5) % NFN, s = i % 5;
-          rX[c] = x[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s];
-        }
-      }
-    }
-    if (MODE == 1) {
-#pragma unroll
-      for (int c = 0; c < FP::ZPT; ++c) {
-        const int i = tid + c * NT;
-        if (i < NM) rZ[c] = zin[(size_t)e * NM + i];
-      }
-    }
-  };
-  if (e0 < g.E) prefetch(e0, 0);
-  int slot = 0;
-  for (int e = e0; e < g.E; e += G, slot = (slot + 1) % 3) {
-    const int e1 = e + G, e2 = e + 2 * G;
-    const int s1 = (slot + 1) % 3, s2 = (slot + 2) % 3;
-    __syncthreads();   // previous macro's compute finished with the buffers
-#pragma unroll
-    for (int c = 0; c < FP::TPT; ++c) {
-      const int i = tid + c * NT;
-      if (i < NTEN) {
-        sTA[i] = rA[c];
-        if (use_b) sTB[i] = rB[c];
-      }
-    }
-    if (use_x) {
-#pragma unroll
-      for (int c = 0; c < FP::XPT; ++c) {
-        const int i = tid + c * NT;
-        if (i < NX) sX[i] = rX[c];
-      }
-    }
-    if (MODE == 1) {
-#pragma unroll
-      for (int c = 0; c < FP::ZPT; ++c) {
-        const int i = tid + c * NT;
-        if (i < NM) sZ[i] = rZ[c];
-      }
-    }
-    __syncthreads();
-    // requests for the next macros (consumed one iteration later)
-    if (e1 < g.E) prefetch(e1, s1);
-    if (e2 < g.E) {
-#pragma unroll
-      for (int c = 0; c < FP::MPT; ++c) {
-        const int i = tid + c * NT;
-        rMi[c] = 0;
-        rMd[c] = 0.0;
-        if (i < META + 4) meta_load(e2, i, rMi[c], rMd[c]);
-      }
-    }
-    const int* mt = sMeta + slot * META;
-    const double* ar = sAr + slot * 4;
-    // ---- compute macro e from shared memory
-    for (int it = tid; it < NI * 5; it += NT) {
-      const int kq = it / 5, t = it % 5, k = kq / NQF, q = kq % NQF;
-      if (use_x) {
-        const double* fp = sFP + q * D::FS;
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < NFN; ++j) acc += fp[j] * sX[(k * NFN + j) * 5 + t];
-        sQ1[it] = acc;
-      }
-      if (MODE == 1) {
-        const double* pf = sPF + kq * D::FS;
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < NFN; ++j) acc += pf[j] * sZ[sRows[k * NFN + j] * 5 + t];
-        sQ2[it] = acc;
-      }
-    }
-    __syncthreads();
-    for (int it = tid; it < NI * 5; it += NT) {
-      const int kq = it / 5, s = it % 5, k = kq / NQF, q = kq % NQF;
-      const double fwq = sFW[q] * ar[k];
-      const double* xq = sQ1 + kq * 5;
-      const double* ta = sTA + kq * 25 + s * 5;
-      if (MODE == 0) {
-        double a = 0.0;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) a += ta[t] * xq[t];
-        sQ3[it] = fwq * a;
-      } else {
-        const double* zq = sQ2 + kq * 5;
-        const double* tb = sTB + kq * 25 + s * 5;
-        double a = 0.0, b = 0.0;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-          a += ta[t] * zq[t];
-          if (use_b) b += tb[t] * xq[t];
-        }
-        sQ3[it] = fwq * a;
-        if (use_b) sQ4[it] = fwq * b;
-      }
-    }
-    __syncthreads();
-    if (MODE == 0) {
-      for (int o = tid; o < NX; o += NT) {
-        const int k = o / (NFN * 5), j = (o / 5) % NFN, s = o % 5;
-        double acc = 0.0;
-#pragma unroll 4
-        for (int q = 0; q < NQF; ++q) acc += sPF[(k * NQF + q) * D::FS + j] * sQ3[(k * NQF + q) * 5 + s];
-        sQ2[o] = acc;
-      }
-      __syncthreads();
-      for (int o = tid; o < NM; o += NT) {
-        const int i = o / 5, s = o % 5;
-        double v = 0.0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int kj = sNF[i * 3 + c];
-          if (kj < 0) break;
-          v += sQ2[kj * 5 + s];
-        }
-        out[(size_t)e * NM + o] = (mode == 0) ? -v : (-r_w[(size_t)e * NM + o] + (-v));
-      }
-    } else {
-      for (int o = tid; o < NX; o += NT) {
-        const int k = o / (NFN * 5), j = (o / 5) % NFN, s = o % 5;
-        double a = 0.0, b = 0.0;
-#pragma unroll 4
-        for (int q = 0; q < NQF; ++q) {
-          const double fp = sFP[q * D::FS + j];
-          a += fp * sQ3[(k * NQF + q) * 5 + s];
-          if (use_b) b += fp * sQ4[(k * NQF + q) * 5 + s];
-        }
-        atomicAdd(&out[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s], b + a);
-      }
-    }
-    // metadata of e+2G lands in the slot freed two iterations ago
-    if (e2 < g.E) {
-#pragma unroll
-      for (int c = 0; c < FP::MPT; ++c) {
-        const int i = tid + c * NT;
-        if (i < META + 4) meta_store(s2, i, rMi[c], rMd[c]);
-      }
-    }
-  }
-}
-
 // Register-blocked face kernels: one thread per (macro slot, tile, face
 // point); its 25-entry tensor rows for the NEXT macro batch are prefetched
 // straight into registers (no shared-memory staging of the 12.8 KB/macro
@@ -1587,14 +1349,14 @@ k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restri
     for (int c = 0; c < F2::IPT; ++c) {
       const int it = tid + c * NT, m = it / NI, e = e0 + m;
       if (it < EB * NI && e < g.E) {
-        const double2* pa = reinterpret_cast<const double2*>(tenA + ((size_t)e * NI + it % NI) * 25);
-        // rows start at 25*8*item bytes: 8-byte aligned only for odd items -> scalar loads
+        // (E, 4, 25, NQF): entry u of consecutive face points is contiguous
+        const int kq = it % NI;
+        const size_t tb = ((size_t)e * 4 + kq / NQF) * 25 * NQF + kq % NQF;
 #pragma unroll
-        for (int u = 0; u < 25; ++u) rA[c][u] = __ldcs(tenA + ((size_t)e * NI + it % NI) * 25 + u);
+        for (int u = 0; u < 25; ++u) rA[c][u] = __ldcs(tenA + tb + u * NQF);
         if (use_b)
 #pragma unroll
-          for (int u = 0; u < 25; ++u) rB[c][u] = __ldcs(tenB + ((size_t)e * NI + it % NI) * 25 + u);
-        (void)pa;
+          for (int u = 0; u < 25; ++u) rB[c][u] = __ldcs(tenB + tb + u * NQF);
       }
     }
     if (use_x) {

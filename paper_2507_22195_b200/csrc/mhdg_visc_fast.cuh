@@ -1,7 +1,7 @@
 // Viscous condensed-operator kernels in point form (K7, second generation).
 //
-// Same operators as k_visc_in / k_visc_out / k_visc_scorr (mhdg_viscous.cuh,
-// reference assembly.py:772-976 and :1037-1173), reorganised so that every
+// Viscous couplings of the condensed operator and the S correction
+// (reference assembly.py:772-976 and :1037-1173), organised so that every
 // chain "trace / local unknowns -> Y (NN x 15) -> M^-1 -> value at a point"
 // is a single contraction with a precomputed point table (ViscGeo::cxt,
 // dzt, pmt, tpp; built once at context creation):
@@ -115,7 +115,8 @@ MHDG_DEV void vf_add_z(const ViscGeo& vg, int pt, const double* Z, const double*
 }
 
 // ---------------------------------------------------------------------------
-// k_visc_in2: g = [-r_w] + vq(Yq) - vvhat(x); modes as k_visc_in
+// k_visc_in2: g = -r_w[1,2] - vvhat(x)[0,2] + vq(M^-1 (r_q[1,2] + qvhat(x)[0,2]))
+//   (mode 0 matvec, 1 condensed rhs, 2 recovery)
 // ---------------------------------------------------------------------------
 template <int P>
 __global__ void __launch_bounds__(128, 4)
@@ -194,12 +195,12 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
 #pragma unroll
             for (int t = 0; t < 5; ++t) xq[t] += b2 * S.X[(k * NFN + j) * 5 + t];
           }
-          const double* h = hhat + (((size_t)e * 4 + k) * NQF + qp) * 25;
+          const double* h = hhat + ((size_t)e * 4 + k) * 25 * NQF + qp;   // (E,4,25,NQF)
 #pragma unroll
           for (int s2 = 0; s2 < 5; ++s2) {
             double a = 0.0;
 #pragma unroll
-            for (int t = 0; t < 5; ++t) a += h[s2 * 5 + t] * xq[t];
+            for (int t = 0; t < 5; ++t) a += h[(s2 * 5 + t) * NQF] * xq[t];
             hx[s2] = a;
           }
         }
@@ -314,14 +315,14 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
       visc_G(vg, g.form, wq, u, yq, gam, Gv);
       const double fwq = g.fw[qp] * S.geo[22 + k];
       const double n0 = S.geo[10 + k * 3], n1 = S.geo[11 + k * 3], n2 = S.geo[12 + k * 3];
-      const size_t base = (((size_t)e * 4 + k) * NQF + qp) * 25;
+      const size_t base = ((size_t)e * 4 + k) * 25 * NQF + qp;   // (E,4,25,NQF)
 #pragma unroll
       for (int s2 = 0; s2 < 5; ++s2) {
         double a = 0.0, b2 = 0.0;
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
-          a += hw[base + s2 * 5 + t] * zq[t];
-          if (mode == 0) b2 += hh[base + s2 * 5 + t] * xq[t];
+          a += hw[base + (s2 * 5 + t) * NQF] * zq[t];
+          if (mode == 0) b2 += hh[base + (s2 * 5 + t) * NQF] * xq[t];
         }
         const double gn = (Gv[s2][0] * n0 + Gv[s2][1] * n1) + Gv[s2][2] * n2;
         S.Gf[it * 5 + s2] = fwq * b2 + (fwq * a - fwq * gn);

@@ -273,152 +273,6 @@ k_residual_visc(Geo g, ViscGeo vg, const double* __restrict__ w, const double* _
 }
 
 // ---------------------------------------------------------------------------
-// S -= A_vq M^-1 A_qv  (assembly.py:835-854, 923-942), on S (row-major) in
-// global memory, before the batched inverse.  dG/dq by unit vectors:
-//   gq[q][s][a][tb] = G(w_q, e_tb)[s][a]
-//   A_s[tb][i][l]   = -sum_q sum_kk B[q][kk][i] (vw sum_a Jinv[kk][a] gq[q][s][a][tb]) phi[q][l]
-//                     + faces: sum_qf fw phi_face[qf][i] (G(w,e_tb).n)[s] phi_face[qf][l]
-//   S[(i,s),(j,t)] -= sum_b sum_l A_s[(t,b)][i][l] P_b[l][j],  P_b = sum_k Jinv[k][b] Pref_k
-// ---------------------------------------------------------------------------
-template <int P>
-struct SCorr {
-  using D = Dims<P>;
-  static constexpr int NT = 256;
-  static constexpr int CV = D::NQ * 3 * 5 * 15;    // C'[q][kk][s][tb]
-  static constexpr int CF = 4 * D::NQF * 5 * 15;   // face [k][qf][s][tb] (weighted, .n)
-  static constexpr int A_ = 15 * D::NN * D::NN;    // A_s[tb][i][l]
-  static constexpr int PB = 3 * D::NN * D::NN;
-  static constexpr size_t bytes = (size_t)(CV + CF + A_ + PB + D::NN * 5 + 16) * 8 + (size_t)(4 * D::NFN) * 4;
-};
-
-template <int P>
-__global__ void __launch_bounds__(256, 1)
-k_visc_scorr(Geo g, ViscGeo vg, const double* __restrict__ w, double* __restrict__ S) {
-  using D = Dims<P>;
-  using SC = SCorr<P>;
-  constexpr int NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF, NM = D::NM, NT = SC::NT;
-  extern __shared__ __align__(16) double smem[];
-  double* sC = smem;                 // CV
-  double* sF = sC + SC::CV;          // CF
-  double* sA = sF + SC::CF;          // A_
-  double* sP = sA + SC::A_;          // PB: P_b[l][j]
-  double* sW = sP + SC::PB;          // NN*5
-  double* sGeo = sW + NN * 5;        // 16: det, invj(9), (areas via g)
-  int* sRows = (int*)(sGeo + 16);
-  const int tid = threadIdx.x;
-  const double gam = g.gamma;
-  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
-  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
-    __syncthreads();
-    for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
-    if (tid == 0) sGeo[0] = g.det[e];
-    if (tid >= 1 && tid < 10) sGeo[tid] = g.invj[(size_t)e * 9 + tid - 1];
-    __syncthreads();
-    // P_b = sum_k Jinv[k][b] Pref_k
-    for (int o = tid; o < 3 * NN * NN; o += NT) {
-      const int b = o / (NN * NN), lj = o % (NN * NN);
-      sP[o] = (sGeo[1 + b] * vg.pref[lj] + sGeo[4 + b] * vg.pref[NN * NN + lj]) + sGeo[7 + b] * vg.pref[2 * NN * NN + lj];
-    }
-    // volume points: C'[q][kk][s][tb]
-    for (int qp = tid; qp < NQ; qp += NT) {
-      const double* ph = g.B + ((size_t)qp * 4 + 3) * NN;
-      double wq[5] = {0, 0, 0, 0, 0};
-      for (int i = 0; i < NN; ++i) {
-        const double a = __ldg(ph + i);
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) wq[s2] += a * sW[i * 5 + s2];
-      }
-      double u[5];
-      to_conservative(wq, g.form, gam, u);
-      const double vw = g.qw[qp] * sGeo[0];
-      for (int tb = 0; tb < 15; ++tb) {
-        double e1[5][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-        e1[tb / 3][tb % 3] = 1.0;
-        double Gv[5][3];
-        visc_G(vg, g.form, wq, u, e1, gam, Gv);
-#pragma unroll
-        for (int kk = 0; kk < 3; ++kk) {
-          const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2)
-            sC[((qp * 3 + kk) * 5 + s2) * 15 + tb] = -(vw * ((j0 * Gv[s2][0] + j1 * Gv[s2][1]) + j2 * Gv[s2][2]));
-        }
-      }
-    }
-    // face points: fw (G(w, e_tb) . n)[s]
-    for (int it = tid; it < 4 * NQF; it += NT) {
-      const int k = it / NQF, qp = it % NQF;
-      const double* pf = g.pf + (size_t)it * NFN;
-      double wq[5] = {0, 0, 0, 0, 0};
-      for (int j = 0; j < NFN; ++j) {
-        const double a = __ldg(pf + j);
-        const int row = sRows[k * NFN + j];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) wq[s2] += a * sW[row * 5 + s2];
-      }
-      double u[5];
-      to_conservative(wq, g.form, gam, u);
-      const double n0 = g.nrm[(size_t)e * 12 + k * 3], n1 = g.nrm[(size_t)e * 12 + k * 3 + 1],
-                   n2 = g.nrm[(size_t)e * 12 + k * 3 + 2];
-      const double fwq = g.fw[qp] * g.area[(size_t)e * 4 + k];
-      for (int tb = 0; tb < 15; ++tb) {
-        double e1[5][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-        e1[tb / 3][tb % 3] = 1.0;
-        double Gv[5][3];
-        visc_G(vg, g.form, wq, u, e1, gam, Gv);
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2)
-          sF[(it * 5 + s2) * 15 + tb] = fwq * ((Gv[s2][0] * n0 + Gv[s2][1] * n1) + Gv[s2][2] * n2);
-      }
-    }
-    __syncthreads();
-    for (int s2 = 0; s2 < 5; ++s2) {
-      // A_s[tb][i][l] = sum_q (sum_kk B[q][kk][i] C'[q][kk][s][tb]) phi[q][l]
-      for (int o = tid; o < 15 * NN * NN; o += NT) {
-        const int tb = o / (NN * NN), il = o % (NN * NN), i = il / NN, l = il % NN;
-        double acc = 0.0;
-        for (int qp = 0; qp < NQ; ++qp) {
-          const double* Bq = g.B + (size_t)qp * 4 * NN;
-          const double* c = sC + (size_t)qp * 3 * 75 + s2 * 15 + tb;
-          const double d = (__ldg(Bq + i) * c[0] + __ldg(Bq + NN + i) * c[75]) + __ldg(Bq + 2 * NN + i) * c[150];
-          acc += d * __ldg(Bq + 3 * NN + l);
-        }
-        sA[o] = acc;
-      }
-      __syncthreads();
-      // face blocks of A_vq: rows/cols of tile k
-      for (int k = 0; k < 4; ++k) {
-        for (int o = tid; o < 15 * NFN * NFN; o += NT) {
-          const int tb = o / (NFN * NFN), il = o % (NFN * NFN), i = il / NFN, l = il % NFN;
-          double acc = 0.0;
-          for (int qp = 0; qp < NQF; ++qp) {
-            const double* pf = g.pf + (size_t)(k * NQF + qp) * NFN;
-            acc += (__ldg(pf + i) * sF[((k * NQF + qp) * 5 + s2) * 15 + tb]) * __ldg(pf + l);
-          }
-          sA[(tb * NN + sRows[k * NFN + i]) * NN + sRows[k * NFN + l]] += acc;
-        }
-        __syncthreads();
-      }
-      // S[(i,s),(j,t)] -= sum_b sum_l A_s[(t,b)][i][l] P_b[l][j]
-      double* Se = S + (size_t)e * NM * NM;
-      for (int o = tid; o < NN * NN * 5; o += NT) {
-        const int i = o / (NN * 5), j = (o / 5) % NN, t = o % 5;
-        double acc = 0.0;
-        for (int b = 0; b < 3; ++b) {
-          const double* a = sA + ((t * 3 + b) * NN + i) * NN;
-          const double* pb = sP + b * NN * NN + j;
-          double ab = 0.0;
-          for (int l = 0; l < NN; ++l) ab += a[l] * pb[l * NN];
-          acc += ab;
-        }
-        Se[(i * 5 + s2) * NM + j * 5 + t] -= acc;
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // viscous condensed operator pieces (assembly.py:1037-1173), CTA per macro.
 //   k_visc_in : g = -r_w[1,2] - vvhat(x)[0,2] + vq(M^-1 (r_q[1,2] + qvhat(x)[0,2]))
 //   k_visc_out: y += hh x[0] + hw z - vhatq(M^-1 (qv z + qvhat(x)[0] + r_q[1]))
@@ -426,15 +280,6 @@ k_visc_scorr(Geo g, ViscGeo vg, const double* __restrict__ w, double* __restrict
 // with qvhat(x)[i][t][b] = -sum_k E_k,b x_k (rows), qv(z) = K_b z, and
 // vq / vhatq evaluated matrix-free as G(w_lin, .) at quadrature points.
 // ---------------------------------------------------------------------------
-template <int P>
-struct VOp {
-  using D = Dims<P>;
-  static constexpr int NT = 128;
-  static constexpr size_t bytes = (size_t)(D::NN * 5 + 4 * D::NFN * 5 + D::NN * 15 * 2 + D::NM + D::NQ * 15 + 4 * D::NQF * 5 +
-                                           4 * D::NQF * 25 + 4 * D::NFN * 5 + 26) * 8 +
-                                  (size_t)(4 * D::NFN * 2 + 4 + 3 * D::NN) * 4;
-};
-
 // Y (NN x 15) += qvhat(x) : -sum_k (area n_b) Eref_k x_k scattered to rows
 template <int P>
 __device__ void add_qvhat(const ViscGeo& vg, const double* sGeo, const int* sRows, const double* sX, double* Y,
@@ -479,252 +324,6 @@ __device__ void mass_solve(const ViscGeo& vg, const double* sGeo, const double* 
     double acc = 0.0;
     for (int j = 0; j < NN; ++j) acc += vg.minv[i * NN + j] * Y[j * 15 + tb];
     Yq[o] = acc / sGeo[0];
-  }
-}
-
-template <int P>
-__global__ void __launch_bounds__(128)
-k_visc_in(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const double* __restrict__ hhat,
-          const double* __restrict__ x, const double* __restrict__ r_w, const double* __restrict__ r_q,
-          double* __restrict__ gout) {
-  using D = Dims<P>;
-  constexpr int NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF, NM = D::NM, NT = 128;
-  extern __shared__ __align__(16) double smem[];
-  double* sW = smem;                   // NN*5
-  double* sX = sW + NN * 5;            // 4*NFN*5
-  double* sY = sX + 4 * NFN * 5;       // NN*15
-  double* sYq = sY + NN * 15;          // NN*15
-  double* sV = sYq + NN * 15;          // NM (vvhat and vq accumulator)
-  double* sGq = sV + NM;               // NQ*15  (volume rows, reference space: kk*5+s)
-  double* sGf = sGq + NQ * 15;         // 4*NQF*5
-  double* sA = sGf + 4 * NQF * 5;      // 4*NQF*25 scratch (hhat x per face point: 4*NQF*5 used)
-  double* sT = sA + 4 * NQF * 25;      // 4*NFN*5
-  double* sGeo = sT + 4 * NFN * 5;     // 26
-  int* sRows = (int*)(sGeo + 26);
-  int* sFid = sRows + 4 * NFN;
-  int* sTid = sFid + 4;
-  int* sNF = sTid + 4 * NFN;
-  const int tid = threadIdx.x;
-  const double gam = g.gamma;
-  const bool use_x = mode != 1, use_r = mode != 0;
-  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
-  for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
-  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
-    __syncthreads();
-    for (int i = tid; i < NN * 5; i += NT) sW[i] = wlin[(size_t)e * NN * 5 + i];
-    if (tid < 4) sFid[tid] = g.fid[e * 4 + tid];
-    for (int i = tid; i < 4 * NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * NFN + i];
-    if (tid == 0) sGeo[0] = g.det[e];
-    if (tid >= 1 && tid < 10) sGeo[tid] = g.invj[(size_t)e * 9 + tid - 1];
-    if (tid >= 10 && tid < 22) sGeo[tid] = g.nrm[(size_t)e * 12 + tid - 10];
-    if (tid >= 22 && tid < 26) sGeo[tid] = g.area[(size_t)e * 4 + tid - 22];
-    for (int i = tid; i < NN * 15; i += NT) sY[i] = use_r ? r_q[(size_t)e * NN * 15 + i] : 0.0;
-    for (int i = tid; i < NM; i += NT) sV[i] = 0.0;
-    __syncthreads();
-    if (use_x) {
-      for (int i = tid; i < 4 * NFN * 5; i += NT) {
-        const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
-        sX[i] = x[((size_t)sFid[k] * NFN + sTid[k * NFN + j]) * 5 + s2];
-      }
-      __syncthreads();
-      add_qvhat<P>(vg, sGeo, sRows, sX, sY, NT);
-      // vvhat: hhat x at face points -> tested with phi_face (stored into sA)
-      for (int it = tid; it < 4 * NQF; it += NT) {
-        const int k = it / NQF, qp = it % NQF;
-        double xq[5] = {0, 0, 0, 0, 0};
-        for (int j = 0; j < NFN; ++j) {
-          const double b2 = __ldg(g.fphi + (size_t)qp * NFN + j);
-#pragma unroll
-          for (int t = 0; t < 5; ++t) xq[t] += b2 * sX[(k * NFN + j) * 5 + t];
-        }
-        const double fwq = g.fw[qp] * sGeo[22 + k];
-        const double* h = hhat + (((size_t)e * 4 + k) * NQF + qp) * 25;
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) {
-          double a = 0.0;
-#pragma unroll
-          for (int t = 0; t < 5; ++t) a += h[s2 * 5 + t] * xq[t];
-          sA[it * 5 + s2] = fwq * a;
-        }
-      }
-      __syncthreads();
-    }
-    mass_solve<P>(vg, sGeo, sY, sYq, NT);
-    __syncthreads();
-    // vq(Yq): volume (reference-space rows) and face (normal) at quadrature points
-    for (int qp = tid; qp < NQ; qp += NT) {
-      const double* ph = g.B + ((size_t)qp * 4 + 3) * NN;
-      double wq[5] = {0, 0, 0, 0, 0}, yq[5][3];
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) yq[s2][0] = yq[s2][1] = yq[s2][2] = 0.0;
-      for (int i = 0; i < NN; ++i) {
-        const double a = __ldg(ph + i);
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) {
-          wq[s2] += a * sW[i * 5 + s2];
-#pragma unroll
-          for (int b = 0; b < 3; ++b) yq[s2][b] += a * sYq[i * 15 + s2 * 3 + b];
-        }
-      }
-      double u[5], Gv[5][3];
-      to_conservative(wq, g.form, gam, u);
-      visc_G(vg, g.form, wq, u, yq, gam, Gv);
-      const double vw = g.qw[qp] * sGeo[0];
-#pragma unroll
-      for (int kk = 0; kk < 3; ++kk) {
-        const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2)
-          sGq[qp * 15 + kk * 5 + s2] = -(vw * ((j0 * Gv[s2][0] + j1 * Gv[s2][1]) + j2 * Gv[s2][2]));
-      }
-    }
-    for (int it = tid; it < 4 * NQF; it += NT) {
-      const int k = it / NQF, qp = it % NQF;
-      double wq[5] = {0, 0, 0, 0, 0}, yq[5][3];
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) yq[s2][0] = yq[s2][1] = yq[s2][2] = 0.0;
-      for (int j = 0; j < NFN; ++j) {
-        const double a = __ldg(g.pf + (size_t)it * NFN + j);
-        const int row = sRows[k * NFN + j];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) {
-          wq[s2] += a * sW[row * 5 + s2];
-#pragma unroll
-          for (int b = 0; b < 3; ++b) yq[s2][b] += a * sYq[row * 15 + s2 * 3 + b];
-        }
-      }
-      double u[5], Gv[5][3];
-      to_conservative(wq, g.form, gam, u);
-      visc_G(vg, g.form, wq, u, yq, gam, Gv);
-      const double fwq = g.fw[qp] * sGeo[22 + k];
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2)
-        sGf[it * 5 + s2] = fwq * ((Gv[s2][0] * sGeo[10 + k * 3] + Gv[s2][1] * sGeo[11 + k * 3]) +
-                                  Gv[s2][2] * sGeo[12 + k * 3]);
-    }
-    __syncthreads();
-    // face-tile tests: T1 = phi_face . (hhat x) [vvhat],  T2 = phi_face . G.n [vq face]
-    for (int o = tid; o < 4 * NFN * 5; o += NT) {
-      const int k = o / (NFN * 5), j = (o / 5) % NFN, s2 = o % 5;
-      double a = 0.0, b2 = 0.0;
-      for (int qp = 0; qp < NQF; ++qp) {
-        const double pf = __ldg(g.pf + (size_t)(k * NQF + qp) * NFN + j);
-        if (use_x) a += pf * sA[(k * NQF + qp) * 5 + s2];
-        b2 += pf * sGf[(k * NQF + qp) * 5 + s2];
-      }
-      sT[o] = b2 - a;   // vq face part minus vvhat part
-    }
-    __syncthreads();
-    for (int o = tid; o < NM; o += NT) {
-      const int i = o / 5, s2 = o % 5;
-      double vol = 0.0;
-      for (int qp = 0; qp < NQ; ++qp) {
-        const double* Bq = g.B + (size_t)qp * 4 * NN + i;
-        vol += (__ldg(Bq) * sGq[qp * 15 + s2] + __ldg(Bq + NN) * sGq[qp * 15 + 5 + s2]) +
-               __ldg(Bq + 2 * NN) * sGq[qp * 15 + 10 + s2];
-      }
-      double f = 0.0;
-      for (int c = 0; c < 3; ++c) {
-        const int kj = sNF[i * 3 + c];
-        if (kj < 0) break;
-        f += sT[kj * 5 + s2];
-      }
-      const double v = vol + f;
-      gout[(size_t)e * NM + o] = use_r ? (-r_w[(size_t)e * NM + o] + v) : v;
-    }
-  }
-}
-
-template <int P>
-__global__ void __launch_bounds__(128)
-k_visc_out(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const double* __restrict__ hh,
-           const double* __restrict__ hw, const double* __restrict__ x, const double* __restrict__ z,
-           const double* __restrict__ r_q, double* __restrict__ y) {
-  using D = Dims<P>;
-  constexpr int NN = D::NN, NFN = D::NFN, NQF = D::NQF, NM = D::NM, NT = 128;
-  extern __shared__ __align__(16) double smem[];
-  double* sW = smem;
-  double* sX = sW + NN * 5;
-  double* sY = sX + 4 * NFN * 5;
-  double* sYq = sY + NN * 15;
-  double* sZ = sYq + NN * 15;          // NM
-  double* sGq = sZ + NM;               // (unused volume scratch) NQ*15
-  double* sGf = sGq + Dims<P>::NQ * 15; // 4*NQF*5 : -fw G.n + hw z + hh x (weighted)
-  double* sA = sGf + 4 * NQF * 5;      // 4*NQF*25
-  double* sT = sA + 4 * NQF * 25;
-  double* sGeo = sT + 4 * NFN * 5;
-  int* sRows = (int*)(sGeo + 26);
-  int* sFid = sRows + 4 * NFN;
-  int* sTid = sFid + 4;
-  const int tid = threadIdx.x;
-  const double gam = g.gamma;
-  for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
-  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
-    __syncthreads();
-    for (int i = tid; i < NN * 5; i += NT) sW[i] = wlin[(size_t)e * NN * 5 + i];
-    for (int i = tid; i < NM; i += NT) sZ[i] = z[(size_t)e * NM + i];
-    if (tid < 4) sFid[tid] = g.fid[e * 4 + tid];
-    for (int i = tid; i < 4 * NFN; i += NT) sTid[i] = g.tidx[(size_t)e * 4 * NFN + i];
-    if (tid == 0) sGeo[0] = g.det[e];
-    if (tid >= 1 && tid < 10) sGeo[tid] = g.invj[(size_t)e * 9 + tid - 1];
-    if (tid >= 10 && tid < 22) sGeo[tid] = g.nrm[(size_t)e * 12 + tid - 10];
-    if (tid >= 22 && tid < 26) sGeo[tid] = g.area[(size_t)e * 4 + tid - 22];
-    for (int i = tid; i < NN * 15; i += NT) sY[i] = (mode == 1) ? r_q[(size_t)e * NN * 15 + i] : 0.0;
-    __syncthreads();
-    if (mode == 0) {
-      for (int i = tid; i < 4 * NFN * 5; i += NT) {
-        const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
-        sX[i] = x[((size_t)sFid[k] * NFN + sTid[k * NFN + j]) * 5 + s2];
-      }
-      __syncthreads();
-      add_qvhat<P>(vg, sGeo, sRows, sX, sY, NT);
-    }
-    add_qv<P>(vg, sGeo, sZ, sY, NT);
-    __syncthreads();
-    mass_solve<P>(vg, sGeo, sY, sYq, NT);
-    __syncthreads();
-    // per face point: fw [hw zq + hh xq - G(w, yq).n]
-    for (int it = tid; it < 4 * NQF; it += NT) {
-      const int k = it / NQF, qp = it % NQF;
-      double wq[5] = {0, 0, 0, 0, 0}, yq[5][3], zq[5] = {0, 0, 0, 0, 0}, xq[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) yq[s2][0] = yq[s2][1] = yq[s2][2] = 0.0;
-      for (int j = 0; j < NFN; ++j) {
-        const double a = __ldg(g.pf + (size_t)it * NFN + j), b2 = __ldg(g.fphi + (size_t)qp * NFN + j);
-        const int row = sRows[k * NFN + j];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) {
-          wq[s2] += a * sW[row * 5 + s2];
-          zq[s2] += a * sZ[row * 5 + s2];
-          if (mode == 0) xq[s2] += b2 * sX[(k * NFN + j) * 5 + s2];
-#pragma unroll
-          for (int b = 0; b < 3; ++b) yq[s2][b] += a * sYq[row * 15 + s2 * 3 + b];
-        }
-      }
-      double u[5], Gv[5][3];
-      to_conservative(wq, g.form, gam, u);
-      visc_G(vg, g.form, wq, u, yq, gam, Gv);
-      const double fwq = g.fw[qp] * sGeo[22 + k];
-      const size_t base = (((size_t)e * 4 + k) * NQF + qp) * 25;
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) {
-        double a = 0.0, b2 = 0.0;
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-          a += hw[base + s2 * 5 + t] * zq[t];
-          if (mode == 0) b2 += hh[base + s2 * 5 + t] * xq[t];
-        }
-        const double gn = (Gv[s2][0] * sGeo[10 + k * 3] + Gv[s2][1] * sGeo[11 + k * 3]) + Gv[s2][2] * sGeo[12 + k * 3];
-        sGf[it * 5 + s2] = fwq * b2 + (fwq * a - fwq * gn);
-      }
-    }
-    __syncthreads();
-    for (int o = tid; o < 4 * NFN * 5; o += NT) {
-      const int k = o / (NFN * 5), j = (o / 5) % NFN, s2 = o % 5;
-      double acc = 0.0;
-      for (int qp = 0; qp < NQF; ++qp) acc += __ldg(g.fphi + (size_t)qp * NFN + j) * sGf[(k * NQF + qp) * 5 + s2];
-      atomicAdd(&y[((size_t)sFid[k] * NFN + sTid[k * NFN + j]) * 5 + s2], acc);
-    }
   }
 }
 
