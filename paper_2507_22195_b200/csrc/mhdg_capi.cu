@@ -15,6 +15,7 @@
 #include "mhdg_kernels.cuh"
 #include "mhdg_viscous.cuh"
 #include "mhdg_visc_fast.cuh"
+#include "mhdg_gj_blocked.cuh"
 
 using namespace mhdg;
 
@@ -384,10 +385,9 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
     c->launches++;
   }
   constexpr int NM = Dims<P>::NM;
-  constexpr int TR = NM >= 64 ? 16 : 8, TC = NM >= 64 ? 16 : 8;
-  const size_t gsm = GJBatch<NM, TR, TC>::bytes;
-  if (set_smem(k_gj_batched<NM, TR, TC>, gsm)) return MHDG_CUDA_ERROR;
-  k_gj_batched<NM, TR, TC><<<grid_for(c, c->E, occ(k_gj_batched<NM, TR, TC>, TR * TC, gsm)), TR * TC, gsm, s>>>(
+  const size_t gsm = GJB<NM>::bytes;
+  if (set_smem(k_gj_blocked<NM>, gsm)) return MHDG_CUDA_ERROR;
+  k_gj_blocked<NM><<<grid_for(c, c->E, occ(k_gj_blocked<NM>, GJB<NM>::NT, gsm)), GJB<NM>::NT, gsm, s>>>(
       c->E, L->sinv, c->d_status);
   (void)ptc;
   c->launches++;
@@ -423,11 +423,24 @@ template <int P, int NT>
 static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* hh_rem,
                                  const int* tidx_rem, const double* area_rem, cudaStream_t s) {
   size_t smem = PreSmem<P, NT>::bytes;
-  if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = occ(k_precond_factor<P, NT>, NT, smem);
-  k_precond_factor<P, NT><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
-      c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
-  c->launches++;
+  constexpr int NB = Dims<P>::NB;
+  if constexpr (NB % 2 == 0) {   // assemble, then the blocked tensor-core Gauss-Jordan
+    if (set_smem(k_precond_factor<P, NT, false>, smem)) return MHDG_CUDA_ERROR;
+    int per_sm = occ(k_precond_factor<P, NT, false>, NT, smem);
+    k_precond_factor<P, NT, false><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
+        c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
+    using GB = GJB<NB>;
+    if (set_smem(k_gj_blocked<NB>, GB::bytes)) return MHDG_CUDA_ERROR;
+    k_gj_blocked<NB><<<grid_for(c, c->n_owned, occ(k_gj_blocked<NB>, GB::NT, GB::bytes)), GB::NT, GB::bytes, s>>>(
+        c->n_owned, L->pinv, c->d_status + 1);
+    c->launches += 2;
+  } else {
+    if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;
+    int per_sm = occ(k_precond_factor<P, NT>, NT, smem);
+    k_precond_factor<P, NT><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
+        c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
+    c->launches++;
+  }
   CK(cudaGetLastError());
   return MHDG_OK;
 }

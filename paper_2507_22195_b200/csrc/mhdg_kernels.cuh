@@ -1137,7 +1137,7 @@ struct PreSmem {
                                   ((size_t)D::NFN + 2 * NB + 2) * 4;
 };
 
-template <int P, int NT>
+template <int P, int NT, bool INV = true>   // INV false: store the assembled block row-major
 __global__ void __launch_bounds__(NT)
 k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double* __restrict__ hh_rem,
                  const int* __restrict__ tidx_rem, const double* __restrict__ area_rem,
@@ -1204,6 +1204,10 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
       if (tid == 0 && !(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
     }
     __syncthreads();
+    if (!INV) {   // inverted afterwards by k_gj_blocked<NB>
+      for (int i = tid; i < NB * NB; i += NT) pinv[(size_t)f * NB * NB + i] = A[i];
+      continue;
+    }
     using G = GJDims<NB, TR, TC>;
     double wr[G::RA][G::CB];
     {
