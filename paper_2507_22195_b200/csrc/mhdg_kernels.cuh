@@ -838,7 +838,7 @@ struct Lin2 {
   static constexpr int C_ = D::NQ * 4 * CS;
   static constexpr int DD_ = QC * 25 * NNP;
   static constexpr int doubles = S_ + C_ + DD_ + D::NN * 5 + 4 * D::NFN * 5 + 4 * D::NQF * D::FS +
-                                 D::NQF * D::FS + D::NQ + D::NQF + D::NQF * 25 + 4 * D::NM + 32;
+                                 D::NQF * D::FS + D::NQ + D::NQF + 4 * D::NQF * 25 + 4 * D::NM + 32;
   static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + 2 * D::NM + 4;
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4 + 16 + D::NN * 15 * 8;
 };
@@ -863,8 +863,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
   double* sFP = sPF + 4 * NQF * D::FS;       // NQF*FS
   double* sQW = sFP + NQF * D::FS;           // NQ
   double* sFW = sQW + NQ;                    // NQF
-  double* sHW = sFW + NQF;                   // NQF*25
-  double* sCol = sHW + NQF * 25;             // 2*NM
+  double* sHW = sFW + NQF;                   // 4*NQF*25 (all tiles)
+  double* sCol = sHW + 4 * NQF * 25;         // 2*NM
   double* sRow = sCol + 2 * NM;              // 2*NM
   double* sGeo = sRow + 2 * NM;              // 32
   int* sRows = (int*)(sGeo + 32);
@@ -1020,11 +1020,14 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           }
       }
     }
-    // ---- face tiles: hw, hhat, hh tensors and the S face blocks
-    for (int k = 0; k < 4; ++k) {
-      __syncthreads();
-      const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
-      for (int it = tid; it < NQF * 10; it += NT) {
+    // ---- face tiles: hw, hhat, hh tensors of all four tiles in one pass,
+    //      then the S face blocks tile by tile (fixed accumulation order)
+    __syncthreads();
+    for (int it4 = tid; it4 < 4 * NQF * 10; it4 += NT) {
+      {
+        const int k = it4 / (NQF * 10), it = it4 % (NQF * 10);
+        const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
+        double* sHWk = sHW + k * NQF * 25;
         const int q = it / 10, t = (it % 10) % 5, which = (it % 10) / 5;
         const double* pf = sPF + (k * NQF + q) * D::FS;
         const double* fp = sFP + q * D::FS;
@@ -1072,7 +1075,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
 #pragma unroll
           for (int s2 = 0; s2 < 5; ++s2) {
             hw_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
-            sHW[q * 25 + s2 * 5 + t] = fd[s2].d;
+            sHWk[q * 25 + s2 * 5 + t] = fd[s2].d;
           }
         } else {
           double hv[5];
@@ -1105,18 +1108,26 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           for (int s2 = 0; s2 < 5; ++s2) hh_out[base + (s2 * 5 + t) * NQF] = hv[s2];
         }
       }
+    }
+    for (int k = 0; k < 4; ++k) {
       __syncthreads();
+      const double* sHWk = sHW + k * NQF * 25;
       const double ar = sGeo[22 + k];
-      for (int o = tid; o < NFN * NFN * 25; o += NT) {
-        const int ij = o / 25, st = o % 25;
-        const int i = ij / NFN, j = ij % NFN, s2 = st / 5, t = st % 5;
-        double acc2 = 0.0;
+      // face block of S: thread = (node pair, row component), 5 accumulators
+      for (int o = tid; o < NFN * NFN * 5; o += NT) {
+        const int ij = o / 5, s2 = o % 5;
+        const int i = ij / NFN, j = ij % NFN;
+        double acc2[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
         for (int q = 0; q < NQF; ++q) {
           const double* pf = sPF + (k * NQF + q) * D::FS;
-          acc2 += (((sFW[q] * ar) * pf[i]) * sHW[q * 25 + st]) * pf[j];
+          const double ci = (sFW[q] * ar) * pf[i], pj = pf[j];
+#pragma unroll
+          for (int t = 0; t < 5; ++t) acc2[t] += (ci * sHWk[q * 25 + s2 * 5 + t]) * pj;
         }
-        const int r = sRows[k * NFN + i] * 5 + s2, c = sRows[k * NFN + j] * 5 + t;
-        S[r * NM + c] += acc2;
+        const int r = sRows[k * NFN + i] * 5 + s2, c = sRows[k * NFN + j] * 5;
+#pragma unroll
+        for (int t = 0; t < 5; ++t) S[r * NM + c + t] += acc2[t];
       }
     }
     __syncthreads();
@@ -1179,13 +1190,18 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
         for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * area_rem[r];
       }
       __syncthreads();
-      for (int o = tid; o < D::NFN * D::NFN * 25; o += NT) {
-        const int ij = o / 25, stt = o % 25;
-        const int i = ij / D::NFN, j = ij % D::NFN, s = stt / 5, t = stt % 5;
-        double acc = 0.0;
-        for (int q = 0; q < D::NQF; ++q)
-          acc += ((sFw[q] * sFP[q * D::NFN + i]) * sHH[q * 25 + stt]) * sFP[q * D::NFN + j];
-        A[(sT[i] * 5 + s) * NB + sT[j] * 5 + t] += acc;
+      for (int o = tid; o < D::NFN * D::NFN * 5; o += NT) {   // (node pair, row component)
+        const int ij = o / 5, s = o % 5;
+        const int i = ij / D::NFN, j = ij % D::NFN;
+        double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int q = 0; q < D::NQF; ++q) {
+          const double ci = sFw[q] * sFP[q * D::NFN + i], pj = sFP[q * D::NFN + j];
+#pragma unroll
+          for (int t = 0; t < 5; ++t) acc[t] += (ci * sHH[q * 25 + s * 5 + t]) * pj;
+        }
+#pragma unroll
+        for (int t = 0; t < 5; ++t) A[(sT[i] * 5 + s) * NB + sT[j] * 5 + t] += acc[t];
       }
     }
     __syncthreads();
