@@ -122,6 +122,12 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   g.E = (int)E; g.F = (int)F;
   g.form = t->formulation; g.kind = t->flux_kind; g.gamma = t->gamma;
   g.B = upload(c, B.data(), B.size(), err);
+  {
+    std::vector<double> phit((size_t)NN * NQ);
+    for (int q = 0; q < NQ; ++q)
+      for (int i = 0; i < NN; ++i) phit[(size_t)i * NQ + q] = t->phi[(size_t)q * NN + i];
+    g.phit = upload(c, phit.data(), phit.size(), err);
+  }
   g.qw = upload(c, t->quad_wts, NQ, err);
   g.pf = upload(c, t->phi_face, (size_t)4 * NQF * NFN, err);
   g.fphi = upload(c, t->fphi, (size_t)NQF * NFN, err);

@@ -42,6 +42,7 @@ struct Geo {
   double gamma;
   // reference tables
   const double* B;     // (NQ, 4, NN): dphi_x, dphi_y, dphi_z, phi
+  const double* phit;  // (NN, NQ): phi transposed (coalesced per-point interpolation)
   const double* qw;    // (NQ)
   const double* pf;    // (4, NQF, NFN)
   const double* fphi;  // (NQF, NFN)
@@ -137,10 +138,14 @@ struct ResCfg {
                        FR_ = 4 * D::NFN * 5, VOL_ = DW * D::NN * 5, GEO_ = 26;
   static constexpr int per_macro = W_ + TR_ + G_ + 2 * H_ + FR_ + VOL_ + GEO_;
   static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF;
-  static constexpr int per_macro_int = 4 + 4 * D::NFN + 4;
+  static constexpr int per_macro_int = 4 + 4 * D::NFN + 4;   // x 2 slots (double-buffered)
+  static constexpr int META = 4 + 4 * D::NFN + 4;
+  static constexpr int WPT = (EB * D::NN * 5 + NT - 1) / NT;       // prefetch registers per thread
+  static constexpr int TPT = (EB * 4 * D::NFN * 5 + NT - 1) / NT;
+  static constexpr int GPT = (EB * 26 + NT - 1) / NT;
   static constexpr int table_int = 4 * D::NFN + 3 * D::NN;
   static constexpr size_t bytes =
-      (size_t)(tables + EB * per_macro) * 8 + (size_t)(table_int + EB * per_macro_int) * 4;
+      (size_t)(tables + EB * per_macro) * 8 + (size_t)(table_int + 2 * EB * per_macro_int) * 4;
 };
 
 template <int P>
@@ -179,37 +184,89 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   auto FR = [&](int m) { return HG(m) + R::H_; };
   auto VOL = [&](int m) { return FR(m) + R::FR_; };
   auto GEO = [&](int m) { return VOL(m) + R::VOL_; };
-  auto FID = [&](int m) { return ib + m * R::per_macro_int; };
+  // meta (face ids, trace permutations, boundary flags) is double-buffered:
+  // slot `cur` serves the batch being computed, slot `cur ^ 1` receives the
+  // next batch's, whose w / trace / geometry are prefetched into registers
+  // during the contraction phase (no dependent global round trip left on
+  // the critical path except the first batch's).
+  int cur = 0;
+  auto FID = [&](int m) { return ib + (cur * EB + m) * R::per_macro_int; };
   auto TID = [&](int m) { return FID(m) + 4; };
   auto BND = [&](int m) { return TID(m) + 4 * NFN; };
+  auto meta_ld = [&](int e0n, int i, int& v) {     // i over EB*META
+    const int m = i / R::META, r = i % R::META, e = e0n + m;
+    if (e >= g.E) return;
+    if (r < 4) v = g.fid[e * 4 + r];
+    else if (r < 4 + 4 * NFN) v = g.tidx[(size_t)e * 4 * NFN + r - 4];
+    else v = g.bnd ? g.bnd[e * 4 + r - 4 - 4 * NFN] : 0;
+  };
+  auto geo_ld = [&](int e0n, int i) -> double {     // i over EB*26
+    const int m = i / 26, c = i % 26, e = e0n + m;
+    if (e >= g.E) return 0.0;
+    if (c == 0) return g.det[e];
+    if (c < 10) return g.invj[(size_t)e * 9 + c - 1];
+    if (c < 22) return g.nrm[(size_t)e * 12 + c - 10];
+    return g.area[(size_t)e * 4 + c - 22];
+  };
+  double pW[R::WPT], pT[R::TPT], pG[R::GPT];
+  auto prefetch_wg = [&](int e0n) {                 // w and geometry
+    const int nmn = min(EB, g.E - e0n);
+#pragma unroll
+    for (int c = 0; c < R::WPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < nmn * NN * 5) pW[c] = w[(size_t)e0n * NN * 5 + i];
+    }
+#pragma unroll
+    for (int c = 0; c < R::GPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < EB * 26) pG[c] = geo_ld(e0n, i);
+    }
+  };
+  auto prefetch_tr = [&](int e0n, int slot) {       // trace values through slot's meta
+    const int nmn = min(EB, g.E - e0n);
+#pragma unroll
+    for (int c = 0; c < R::TPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < nmn * 4 * NFN * 5) {
+        const int m = i / (4 * NFN * 5), r = i % (4 * NFN * 5);
+        const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
+        const int* mt = ib + (slot * EB + m) * R::per_macro_int;
+        pT[c] = trace[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s];
+      }
+    }
+  };
+  {   // first batch: meta, then its data
+    const int e00 = blockIdx.x * EB;
+    if (e00 < g.E) {
+      for (int i = tid; i < EB * R::META; i += NT) {
+        int v = 0;
+        meta_ld(e00, i, v);
+        ib[(i / R::META) * R::per_macro_int + i % R::META] = v;
+      }
+      __syncthreads();
+      prefetch_wg(e00);
+      prefetch_tr(e00, 0);
+    }
+  }
 
   for (int e0 = blockIdx.x * EB; e0 < g.E; e0 += gridDim.x * EB) {
     const int nm = min(EB, g.E - e0);
+    const int e1 = e0 + gridDim.x * EB;
     __syncthreads();
-    for (int i = tid; i < nm * NN * 5; i += NT) W(i / (NN * 5))[i % (NN * 5)] = w[(size_t)e0 * NN * 5 + i];
-    for (int i = tid; i < nm * 4; i += NT) {
-      const int m = i / 4, k = i % 4, e = e0 + m;
-      FID(m)[k] = g.fid[e * 4 + k];
-      BND(m)[k] = g.bnd ? g.bnd[e * 4 + k] : 0;
+#pragma unroll
+    for (int c = 0; c < R::WPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < nm * NN * 5) W(i / (NN * 5))[i % (NN * 5)] = pW[c];
     }
-    for (int i = tid; i < nm * 4 * NFN; i += NT) {
-      const int m = i / (4 * NFN);
-      TID(m)[i % (4 * NFN)] = g.tidx[(size_t)e0 * 4 * NFN + i];
+#pragma unroll
+    for (int c = 0; c < R::TPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < nm * 4 * NFN * 5) TR(i / (4 * NFN * 5))[i % (4 * NFN * 5)] = pT[c];
     }
-    for (int i = tid; i < nm * 26; i += NT) {
-      const int m = i / 26, c = i % 26, e = e0 + m;
-      double v;
-      if (c == 0) v = g.det[e];
-      else if (c < 10) v = g.invj[(size_t)e * 9 + c - 1];
-      else if (c < 22) v = g.nrm[(size_t)e * 12 + c - 10];
-      else v = g.area[(size_t)e * 4 + c - 22];
-      GEO(m)[c] = v;
-    }
-    __syncthreads();
-    for (int i = tid; i < nm * 4 * NFN * 5; i += NT) {
-      const int m = i / (4 * NFN * 5), r = i % (4 * NFN * 5);
-      const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
-      TR(m)[r] = trace[((size_t)FID(m)[k] * NFN + TID(m)[k * NFN + j]) * 5 + s];
+#pragma unroll
+    for (int c = 0; c < R::GPT; ++c) {
+      const int i = tid + c * NT;
+      if (i < EB * 26) GEO(i / 26)[i % 26] = pG[c];
     }
     __syncthreads();
 
@@ -255,12 +312,11 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     // ---- 1b. volume quadrature points: reference-space flux + temporal term
     for (int it = tid; it < nm * NQ; it += NT) {
       const int m = it / NQ, q = it % NQ, e = e0 + m;
-      const double* ph = Bt + ((size_t)q * 4 + 3) * NN;
       const double* sw = W(m);
       double wq[5] = {0, 0, 0, 0, 0};
 #pragma unroll 4
       for (int i = 0; i < NN; ++i) {
-        const double a = __ldg(ph + i);
+        const double a = __ldg(g.phit + (size_t)i * NQ + q);
 #pragma unroll
         for (int s = 0; s < 5; ++s) wq[s] += a * sw[i * 5 + s];
       }
@@ -288,6 +344,15 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         }
         gr[15 + s] = tmp;
       }
+    }
+    // next batch: meta straight into the other slot, w / geometry into registers
+    if (e1 < g.E) {
+      for (int i = tid; i < EB * R::META; i += NT) {
+        int v = 0;
+        meta_ld(e1, i, v);
+        ib[((cur ^ 1) * EB + i / R::META) * R::per_macro_int + i % R::META] = v;
+      }
+      prefetch_wg(e1);
     }
     __syncthreads();
 
@@ -351,6 +416,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
     }
     __syncthreads();
+    if (e1 < g.E) prefetch_tr(e1, cur ^ 1);
     // ---- 3. r_w = volume part + face parts (tile order)
     for (int o = tid; o < nm * NN * 5; o += NT) {
       const int m = o / (NN * 5), is = o % (NN * 5), i = is / 5, s = is % 5;
@@ -365,6 +431,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
       r_w[(size_t)e0 * NN * 5 + o] = r;
     }
+    cur ^= 1;
   }
 }
 
