@@ -129,6 +129,10 @@ struct ResCfg {
   static constexpr int EB = (P >= 4) ? 1 : 2;      // macros per CTA iteration
   static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per CTA
   static constexpr int NT = NW * 32;
+#ifndef MHDG_RES_MINB
+#define MHDG_RES_MINB 4
+#endif
+  static constexpr int MINB = (P >= 4) ? 2 : MHDG_RES_MINB;   // resident CTAs per SM (register cap)
   static constexpr int WPM = NW / EB;              // warps per macro
   static constexpr int DW = WPM / 2;               // DMMA warps per macro (K split)
   static constexpr int FW = WPM - DW;              // face warps per macro
@@ -149,7 +153,7 @@ struct ResCfg {
 };
 
 template <int P>
-__global__ void __launch_bounds__(ResCfg<P>::NT, 512 / ResCfg<P>::NT)
+__global__ void __launch_bounds__(ResCfg<P>::NT, ResCfg<P>::MINB)
 k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace,
            int has_stage, double alpha, const double* __restrict__ offset, int check,
            double* __restrict__ r_w, double* __restrict__ r_tr, unsigned long long* status) {
