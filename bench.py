@@ -16,8 +16,13 @@ API with pinned host inputs copied in and results copied out every step.
 
 --impl reference: the CPU oracle port (oracle/, the numpy restatement of the
 reference) timed on the host cores on a bounded sample of the same workload.
-Under torchrun (N>1) every rank runs an independent replica (weak scaling);
-rank 0 prints the JSON line.
+Under torchrun (N>1) the macro-elements are partitioned: the
+global mesh is n*N x n x n cells (N x-slabs of the config-2 mesh, weak
+scaling), every rank runs the partitioned operator (local kernels + trace
+halo exchange of partial face sums / ghost values over NCCL + all-reduced
+dots), and value = all ranks' DoF-applications / the max-over-ranks device
+time.  --replicas keeps the older independent-replica mode.  Rank 0 prints
+the JSON line.
 """
 
 from __future__ import annotations
@@ -46,12 +51,19 @@ def parse():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=16, help="cells per axis (config 2: 16)")
+    ap.add_argument("--ncells", type=int, default=16, help="cells per axis (config 2: 16)")
     ap.add_argument("--p", type=int, default=3)
     ap.add_argument("--flux", default="es")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=4)
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of the partitioned operator")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="use the partitioned operator also at N=1 (exchange-free)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="partitioned runs: gloo stages the halo through host memory "
+                         "(several ranks may then share one GPU)")
     return ap.parse_args()
 
 
@@ -206,7 +218,7 @@ def run_b200(args, rank, local_rank, world):
     if world > 1:
         torch.distributed.init_process_group("nccl", device_id=dev)
 
-    gas, mesh, vx, alpha = make_problem(args.n, args.p, args.flux)
+    gas, mesh, vx, alpha = make_problem(args.ncells, args.p, args.flux)
     disc = Discretization(mesh, p=args.p, gas=gas, formulation="entropy",
                           flux=DissipationSpec(args.flux), device=dev)
     t = disc.tables
@@ -397,7 +409,7 @@ def run_b200(args, rank, local_rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (projected isentropic-vortex IC, seeded x)",
-            "config": {"workload": f"config2 isentropic vortex n={args.n} ({E} macros) k={args.p} "
+            "config": {"workload": f"config2 isentropic vortex n={args.ncells} ({E} macros) k={args.p} "
                                    f"{args.flux} entropy m=1; step = residual + condensed "
                                    "matvec + face-block precond",
                        "macros": E, "faces": F, "dofs_per_step": per_step,
@@ -419,11 +431,196 @@ def run_b200(args, rank, local_rank, world):
         torch.distributed.destroy_process_group()
 
 
+def run_b200_partitioned(args, rank, local_rank, world):
+    """N ranks, one x-slab of macro-elements each, trace halo over NCCL."""
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2507_22195_b200.assembly import FieldSet, StageContext
+    from paper_2507_22195_b200.cases import IsentropicVortex
+    from paper_2507_22195_b200.distributed import PartitionedDiscretization
+    from paper_2507_22195_b200.fluxes import DissipationSpec
+    from paper_2507_22195_b200.gas import GasModel
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+    from paper_2507_22195_b200.tables import HDGTables
+    from paper_2507_22195_b200.time_march import dirk33_tableau
+
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % ndev)
+    torch.cuda.set_device(dev)
+    if world > 1 or args.backend == "gloo":
+        if args.backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=dev)
+        else:
+            torch.distributed.init_process_group("gloo")
+    gas = GasModel(1.4)
+    n = args.ncells
+    mesh = build_box_macro_mesh(np.array([[0.0, 10.0 * world], [0.0, 10.0], [0.0, 10.0]]),
+                                (n * world, n, n), 1)
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          center=(5.0, 5.0), gas=gas)
+    alpha = float(dirk33_tableau().d[0, 0] / 0.01)
+    full = HDGTables(mesh, args.p)
+    pdisc = PartitionedDiscretization(mesh, args.p, rank, world, device=dev, full_tables=full,
+                                      gas=gas, formulation="entropy",
+                                      flux=DissipationSpec(args.flux))
+    disc = pdisc.local
+    t = disc.tables
+    part = pdisc.part
+    E_l = part.macro_hi - part.macro_lo
+    F_own, nc, nt = part.n_owned, t.layout.n_unique, t.fphi.shape[1]
+    fields = disc.project(vx.initial)
+    u_n = disc.volume_quad_states(fields)
+    offset = (-alpha * u_n).contiguous()
+    stage = StageContext(alpha=alpha, offset=offset)
+    lin = pdisc.jacobian(fields, stage, ptc_weight=1.0)
+    F_l = fields.trace.shape[0]
+    x = torch.as_tensor(np.random.default_rng(1 + rank).standard_normal((F_l, nt, 5)), device=dev)
+    torch.cuda.synchronize()
+    units = dof_units(E_l, F_own, nc, nt)
+    per_step = sum(units.values())
+    tot = torch.tensor([float(per_step)], dtype=torch.float64, device=dev)
+    pdisc.exchange.allreduce_sum(tot)
+    per_step_all = float(tot.item())
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        res = pdisc.residuals(fields, stage, sync=False)
+        if ev:
+            ev[1].record(stream)
+        y = lin.matvec(x)
+        if ev:
+            ev[2].record(stream)
+        z = lin.apply_preconditioner(x)
+        if ev:
+            ev[3].record(stream)
+        return res, y, z
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if torch.distributed.is_initialized():
+            torch.distributed.barrier()
+
+    def max_over_ranks(v):
+        tt = torch.tensor([v], dtype=torch.float64, device=dev)
+        if torch.distributed.is_initialized():
+            if args.backend == "gloo":
+                h = tt.cpu()
+                torch.distributed.all_reduce(h, op=torch.distributed.ReduceOp.MAX)
+                return float(h.item())
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return float(tt.item())
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    launches0 = disc.launch_count
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = disc.launch_count - launches0
+    ms = max_over_ranks(start.elapsed_time(end))
+    k_ms = {k: max_over_ranks(float(np.mean([e[a].elapsed_time(e[a + 1]) for e in evs])))
+            for a, k in enumerate(("residual", "matvec", "precond"))}
+    value = per_step_all * args.steps / (ms * 1e-3)
+
+    # e2e through the partitioned API with pinned host buffers
+    w_h = fields.w.cpu().pin_memory()
+    tr_h = fields.trace.cpu().pin_memory()
+    off_h = offset.cpu().pin_memory()
+    x_h = x.cpu().pin_memory()
+    out_h = [torch.empty(s, dtype=torch.float64).pin_memory()
+             for s in (fields.w.shape, fields.trace.shape, x.shape, x.shape)]
+    h2d = 8 * (w_h.numel() + tr_h.numel() + off_h.numel() + x_h.numel())
+    d2h = 8 * sum(o.numel() for o in out_h)
+
+    def e2e_step():
+        wd = w_h.to(dev, non_blocking=True)
+        td = tr_h.to(dev, non_blocking=True)
+        od = off_h.to(dev, non_blocking=True)
+        xd = x_h.to(dev, non_blocking=True)
+        res = pdisc.residuals(FieldSet(wd, td), StageContext(alpha=alpha, offset=od), sync=False)
+        y = lin.matvec(xd)
+        z = lin.apply_preconditioner(xd)
+        for o, src in zip(out_h, (res.r_w, res.r_trace, y, z)):
+            o.copy_(src, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e2.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(s2.elapsed_time(e2))
+    e2e_value = per_step_all * args.e2e_steps / (e2e_ms * 1e-3)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    nqf = t.fphi.shape[0]
+    NM = 5 * nc
+    # rank-local matvec bytes (the exchange time is inside the measured interval)
+    bytes_mv = 8 * E_l * NM * NM + 3 * 8 * E_l * 4 * nqf * 25 + 2 * 8 * F_l * nt * 5 + \
+        4 * E_l * 4 * (1 + nt) + 8 * E_l * 4
+    ach = bytes_mv / (k_ms["matvec"] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None, "kernel": "matvec (incl. halo exchange)",
+                "peak_source": "measured MEASURED_PEAKS.json hbm_gbs"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (projected isentropic-vortex IC, seeded x)",
+            "config": {"workload": f"config2 isentropic vortex, {n * world}x{n}x{n} cells "
+                                   f"({mesh.n_macros} macros, {n}^3 cells x 6 per rank) k={args.p} "
+                                   f"{args.flux}; step = residual + condensed matvec + face-block "
+                                   f"precond through the partitioned operator",
+                       "macros": mesh.n_macros, "macros_per_rank": E_l,
+                       "owned_faces_rank0": F_own, "dofs_per_step": per_step_all,
+                       "parallelism": f"{world} ranks, x-slab macro partition, trace halo + "
+                                      f"allreduce over {args.backend}",
+                       "l2": "inputs larger than L2: S^-1 streamed every step"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "kernels_ms": k_ms,
+            "clocks": clk.summary(),
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if torch.distributed.is_initialized():
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, local_rank, world = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if (world > 1 and not args.replicas) or args.partitioned:
+        run_b200_partitioned(args, rank, local_rank, world)
         return
     run_b200(args, rank, local_rank, world)
 

@@ -66,8 +66,8 @@ class PartitionedDiscretization:
         return math.sqrt(self.allreduce([local])[0])
 
     # -- operators -----------------------------------------------------------
-    def residuals(self, fields, stage=None, check=True):
-        res = self.local.residuals(self._fields(fields), stage, check)
+    def residuals(self, fields, stage=None, check=True, sync=True):
+        res = self.local.residuals(self._fields(fields), stage, check, sync=sync)
         self.exchange.reduce_partials(res.r_trace)
         return ResidualSet(res.r_w, res.r_trace, None, _disc=self)
 
@@ -148,10 +148,12 @@ def gather_remote_sides(pdisc, lin):
     owning the other macro."""
     torch = __import__("torch")
     part = pdisc.part
+    nqf = pdisc.local.tables.fphi.shape[0]
+    # every rank takes part in the exchange: a rank that owns no halo face
+    # (e.g. both slab boundaries owned by the neighbour) still sends its sides
+    hh_r = pdisc.exchange.gather_sides(lin.hh, nqf).contiguous()
     if part.n_remote_sides == 0:
         return None, None, None
-    nqf = pdisc.local.tables.fphi.shape[0]
-    hh_r = pdisc.exchange.gather_sides(lin.hh, nqf).contiguous()
     dev = pdisc.device
     tidx = torch.as_tensor(part.remote_tidx, device=dev)
     area = torch.as_tensor(part.remote_area, device=dev)

@@ -105,6 +105,15 @@ class LocalPartition:
         lt.dphi_phys = np.einsum("qik,eska->esqia", lt.dphi, lt.sub_inv_jac)
         lt.face_w = lt.facet_wts[None, None, :] * lt.face_area[:, :, None]
         lt.mesh = SimpleNamespace(n_macros=E_l, dim=t.mesh.dim, m=t.mesh.m)
+        # coordinates of the local nodes / trace nodes / quadrature points
+        # (projection and error norms on one rank)
+        mesh = t.mesh
+        lt.node_coords = (np.einsum("eab,nb->ena", mesh.macro_jacobians[sl], t.layout.unique_nodes)
+                          + mesh.macro_origins[sl][:, None, :])
+        lt.trace_coords = t.trace_coords[self.global_faces]
+        sub_v = mesh.sub_vertices[sl]
+        lt.quad_coords = (np.einsum("esab,qb->esqa", lt.sub_jac, t.basis.quad_pts)
+                          + sub_v[:, :, 0, :][:, :, None, :])
         # preconditioner sides of owned faces: local (e*n_st + k) or a remote
         # side encoded as -2 - (index into the gathered remote-side list)
         fs = t.face_sides[self.global_faces[: self.n_owned]].copy()
@@ -131,6 +140,7 @@ class LocalPartition:
         tile_of[t.st_face] = np.arange(t.n_st)
         rem_e = skel.neighbor[gf] if len(rows) else rows
         rem_k = tile_of[skel.neighbor_face[gf]] if len(rows) else rows
+        self.remote_side_ids = rem_e * t.n_st + rem_k      # global (macro, tile) of each remote side
         self.remote_tidx = np.ascontiguousarray(t.trace_idx[rem_e, rem_k], dtype=np.int32)
         self.remote_area = np.ascontiguousarray(t.face_area[rem_e, rem_k])
         remote_of_row = {int(r): i for i, r in enumerate(remote_rows)}
@@ -157,23 +167,37 @@ class LocalPartition:
 
 
 class TorchDistExchange:
-    """Halo transport over torch.distributed (NCCL on GPU, gloo on CPU)."""
+    """Halo transport over torch.distributed (NCCL on GPU, gloo on CPU).
+
+    With the gloo backend, device tensors are staged through host memory
+    (gloo has no device transport); this is what lets several ranks share
+    one GPU in tests without their kernels waiting on each other."""
 
     def __init__(self, part, group=None):
+        import torch.distributed as dist
+
         self.part = part
         self.group = group
+        self.host_staged = dist.is_initialized() and dist.get_backend(group) == "gloo"
 
     def _exchange(self, sends, recvs):
         import torch.distributed as dist
 
+        if self.host_staged:
+            dev_recvs = recvs
+            sends = {h: b.cpu() for h, b in sends.items()}
+            recvs = {h: b.new_empty(b.shape, device="cpu") for h, b in recvs.items()}
         ops = []
         for h, buf in sends.items():
             ops.append(dist.P2POp(dist.isend, buf.contiguous(), h, self.group))
         for h, buf in recvs.items():
             ops.append(dist.P2POp(dist.irecv, buf, h, self.group))
-        if ops:
+        if ops and dist.is_initialized():
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if self.host_staged:
+            for h, b in recvs.items():
+                dev_recvs[h].copy_(b)
 
     def reduce_partials(self, trace_like):
         """owner += neighbour partials on shared faces; returns trace_like."""
@@ -206,6 +230,13 @@ class TorchDistExchange:
     def allreduce_sum(self, t):
         import torch.distributed as dist
 
+        if not dist.is_initialized():      # single rank
+            return t
+        if self.host_staged and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+            return t
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 

@@ -1,0 +1,127 @@
+"""Partitioned operator with real processes: two ranks (torch.distributed,
+gloo backend, halo staged through host memory) share one GPU, each running
+PartitionedDiscretization / PartitionedLinearizedSystem on its macro range.
+Owned rows of the residual, condensed matvec and face-block preconditioner
+must equal the single-device results bit for bit, and the distributed
+FGMRES (DistVectors, all-reduced dots) must reproduce the single-device
+iteration count and solution.  The x-slab split leaves one rank owning no
+halo face, which exercises the asymmetric exchanges."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _problem():
+    from paper_2507_22195_b200 import DissipationSpec, GasModel
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+    from paper_2507_22195_b200.tables import HDGTables
+
+    gas = GasModel(1.4)
+    mesh = build_box_macro_mesh(np.array([[0.0, 2.0], [0.0, 1.0], [0.0, 1.0]]), (4, 2, 2), 1)
+    t = HDGTables(mesh, 3)
+    rng = np.random.default_rng(91)
+    E, nc, F, nt = mesh.n_macros, t.layout.n_unique, t.n_faces, t.n_trace
+
+    def st(n):
+        return gas.entropy_vars(gas.conservative(rng.uniform(0.9, 1.1, n),
+                                                 rng.uniform(-0.5, 0.5, (n, 3)),
+                                                 rng.uniform(0.9, 1.1, n)))
+
+    w, tr = st(E * nc).reshape(E, nc, 5), st(F * nt).reshape(F, nt, 5)
+    x = rng.standard_normal(tr.shape)
+    return gas, mesh, t, DissipationSpec("es"), w, tr, x
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22195_b200.assembly import FieldSet, StageContext
+        from paper_2507_22195_b200.distributed import PartitionedDiscretization
+        from paper_2507_22195_b200.solver import solve_condensed
+
+        torch.cuda.set_device(0)
+        gas, mesh, t, spec, w, tr, x = _problem()
+        pd = PartitionedDiscretization(mesh, 3, rank, world, device="cuda:0", full_tables=t,
+                                       gas=gas, flux=spec)
+        part = pd.part
+        lo, hi = part.macro_lo, part.macro_hi
+        wl, trl = part.local_fields(w, tr)
+        alpha = 120.0
+        fl = FieldSet(torch.from_numpy(wl.copy()).cuda(), torch.from_numpy(trl.copy()).cuda())
+        off = -alpha * pd.volume_quad_states(fl)
+        stage = StageContext(alpha, off)
+        res = pd.residuals(fl, stage)
+        lin = pd.jacobian(fl, stage, ptc_weight=1.0)
+        xl = torch.from_numpy(x[part.global_faces].copy()).cuda()
+        y = lin.matvec(xl)
+        z = lin.apply_preconditioner(xl)
+        d_trace, stats = solve_condensed(lin, res, rel_tol=1e-8, restart=20, max_outer=80)
+        own = part.n_owned
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), lo=lo, hi=hi,
+                 faces=part.global_faces[:own], r_w=res.r_w.cpu().numpy(),
+                 r_t=res.r_trace[:own].cpu().numpy(), y=y[:own].cpu().numpy(),
+                 z=z[:own].cpu().numpy(), d=d_trace[:own].cpu().numpy(),
+                 its=stats.outer_iterations, inner=stats.inner_iterations,
+                 n_remote=part.n_remote_sides)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(900)
+def test_two_processes_share_one_gpu(cuda_ok, tmp_path):
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2507_22195_b200 import Discretization
+    from paper_2507_22195_b200.assembly import FieldSet, StageContext
+    from paper_2507_22195_b200.solver import solve_condensed
+
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    gas, mesh, t, spec, w, tr, x = _problem()
+    full = Discretization(mesh, p=3, gas=gas, flux=spec, device="cuda:0", tables=t)
+    alpha = 120.0
+    f = FieldSet(torch.from_numpy(w).cuda(), torch.from_numpy(tr).cuda())
+    off = -alpha * full.volume_quad_states(f)
+    stage = StageContext(alpha, off)
+    ref = full.residuals(f, stage)
+    lin = full.jacobian(f, stage, ptc_weight=1.0)
+    xd = torch.from_numpy(x).cuda()
+    y_ref = lin.matvec(xd).cpu().numpy()
+    z_ref = lin.apply_preconditioner(xd).cpu().numpy()
+    d_ref, st_ref = solve_condensed(lin, ref, rel_tol=1e-8, restart=20, max_outer=80)
+    d_ref = d_ref.cpu().numpy()
+    rw_ref, rt_ref = ref.r_w.cpu().numpy(), ref.r_trace.cpu().numpy()
+    n_remote = []
+    for rank in range(world):
+        o = np.load(tmp_path / f"rank{rank}.npz")
+        lo, hi, faces = int(o["lo"]), int(o["hi"]), o["faces"]
+        n_remote.append(int(o["n_remote"]))
+        assert np.array_equal(o["r_w"], rw_ref[lo:hi])
+        assert np.array_equal(o["r_t"], rt_ref[faces])
+        assert np.array_equal(o["y"], y_ref[faces])
+        assert np.array_equal(o["z"], z_ref[faces])
+        assert int(o["its"]) == st_ref.outer_iterations
+        assert int(o["inner"]) == st_ref.inner_iterations
+        err = np.abs(o["d"] - d_ref[faces]).max() / np.abs(d_ref).max()
+        assert err <= 1e-10, err
+    assert min(n_remote) == 0

@@ -156,11 +156,20 @@ def _worker(rank, world, port, flux, results):
                                    x.ravel(), rel_tol=1e-8, restart=15, max_iters=60)
         xd = res.x.view(shape).numpy()[: part.n_owned]
         err_x = float(np.abs(xd - xr.reshape(tr.shape)[own]).max() / np.abs(xr).max())
-        results[rank] = (ok_res, ok_fill, err_mv, res.iterations, it_ref, err_x)
+        # remote face sides for the face-block preconditioner: every rank
+        # takes part, including one that owns no halo face
+        nqf = t.fphi.shape[0]
+        hh_glob = np.arange(E * 4 * nqf * 25, dtype=np.float64).reshape(E * 4, nqf * 25)
+        hh_loc = torch.from_numpy(hh_glob[lo * 4:hi * 4].copy())
+        got = ex.gather_sides(hh_loc, nqf).numpy()
+        ok_sides = np.array_equal(got, hh_glob[part.remote_side_ids])
+        results[rank] = (ok_res and ok_sides, ok_fill, err_mv, res.iterations, it_ref, err_x,
+                         part.n_remote_sides)
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.timeout(600)
 @pytest.mark.parametrize("flux", ["es", "kepes"])
 def test_gloo_world2_partitioned_operator_and_fgmres(flux):
     world = 2
@@ -168,8 +177,9 @@ def test_gloo_world2_partitioned_operator_and_fgmres(flux):
     results = mgr.dict()
     mp.start_processes(_worker, args=(world, _free_port(), flux, results), nprocs=world,
                        join=True, start_method="spawn")
+    assert min(results[r][6] for r in range(world)) == 0, "one rank should own no halo face"
     for rank in range(world):
-        ok_res, ok_fill, err_mv, it, it_ref, err_x = results[rank]
+        ok_res, ok_fill, err_mv, it, it_ref, err_x, _ = results[rank]
         assert ok_res, "partitioned residual must be bit-identical"
         assert ok_fill
         assert err_mv <= 1e-14
