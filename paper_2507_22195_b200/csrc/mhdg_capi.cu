@@ -286,11 +286,21 @@ static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int h
                            const double* off, int check, double* rw, double* rt, cudaStream_t s) {
   using RC = ResCfg<P>;
   size_t smem = RC::bytes;
-  if (set_smem(k_residual<P>, smem)) return MHDG_CUDA_ERROR;
-  int per_sm = occ(k_residual<P>, RC::NT, smem);
-  int blocks = std::min((c->E + RC::EB - 1) / RC::EB, c->n_sms * per_sm);
-  k_residual<P><<<std::max(1, blocks), RC::NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check, rw, rt,
-                                                          c->d_status);
+  // the ES flux gets its own instantiation (40 B of spills instead of 244 B
+  // with the run-time switch over all four kinds; a KEPES-only variant
+  // allocates worse than the switch, so KEPES / EC / LF share it)
+  auto go = [&](auto kern) -> int {
+    if (set_smem(kern, smem)) return MHDG_CUDA_ERROR;
+    int per_sm = occ(kern, RC::NT, smem);
+    int blocks = std::min((c->E + RC::EB - 1) / RC::EB, c->n_sms * per_sm);
+    kern<<<std::max(1, blocks), RC::NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check, rw, rt,
+                                                   c->d_status);
+    return MHDG_OK;
+  };
+  int rc;
+  if (c->geo.kind == FLUX_ES) rc = go(k_residual<P, FLUX_ES>);
+  else rc = go(k_residual<P, -1>);
+  if (rc) return rc;
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;

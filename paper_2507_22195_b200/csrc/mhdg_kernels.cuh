@@ -152,7 +152,7 @@ struct ResCfg {
       (size_t)(tables + EB * per_macro) * 8 + (size_t)(table_int + 2 * EB * per_macro_int) * 4;
 };
 
-template <int P>
+template <int P, int FK = -1>   // FK: flux kind fixed at compile time (-1: g.kind at run time)
 __global__ void __launch_bounds__(ResCfg<P>::NT, ResCfg<P>::MINB)
 k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace,
            int has_stage, double alpha, const double* __restrict__ offset, int check,
@@ -300,7 +300,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       const double* geo = GEO(m);
       const double n[3] = {geo[10 + k * 3], geo[11 + k * 3], geo[12 + k * 3]};
       double fh[5];
-      numerical_flux(g.kind, u, uh, n, gam, fh);
+      numerical_flux(FK >= 0 ? FK : g.kind, u, uh, n, gam, fh);
       const double fwq = sFW[q] * geo[22 + k];
       double* h = H(m) + kq * 5;
 #pragma unroll
@@ -308,7 +308,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       if (BND(m)[k] && g.has_uinf) {
         const double mn[3] = {-n[0], -n[1], -n[2]};
         double gh[5];
-        numerical_flux(g.kind, g.uinf, uh, mn, gam, gh);
+        numerical_flux(FK >= 0 ? FK : g.kind, g.uinf, uh, mn, gam, gh);
 #pragma unroll
         for (int s = 0; s < 5; ++s) HG(m)[kq * 5 + s] = fwq * gh[s];
       }
