@@ -394,10 +394,15 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
     c->launches += 2;
     CK(cudaMemcpyAsync(L->wlin, w, sizeof(double) * (size_t)c->E * c->nn * 5, cudaMemcpyDeviceToDevice, s));
   } else {
-    if (set_smem(k_linearize2<P, false>, smem)) return MHDG_CUDA_ERROR;
-    int grid = grid_for(c, c->E, occ(k_linearize2<P, false>, 256, smem));
-    k_linearize2<P, false><<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw,
-                                                   L->hhat, L->hh, c->d_status);
+    auto go = [&](auto kern) -> int {
+      if (set_smem(kern, smem)) return MHDG_CUDA_ERROR;
+      int grid = grid_for(c, c->E, occ(kern, 256, smem));
+      kern<<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat, L->hh,
+                                   c->d_status);
+      return MHDG_OK;
+    };
+    const int rc = (c->geo.kind == FLUX_ES) ? go(k_linearize2<P, false, FLUX_ES>) : go(k_linearize2<P, false>);
+    if (rc) return rc;
     c->launches++;
   }
   constexpr int NM = Dims<P>::NM;

@@ -914,7 +914,7 @@ struct Lin2 {
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4 + 16 + D::NN * 15 * 8;
 };
 
-template <int P, bool VISC>
+template <int P, bool VISC, int FK = -1>   // FK: flux kind fixed at compile time (-1: run time)
 __global__ void __launch_bounds__(256, 1)
 k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __restrict__ qn,
              const double* __restrict__ trace, double weight,
@@ -1120,7 +1120,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         }
         to_conservative(wd, g.form, gam, ud);
         to_conservative(whd, g.form, gam, uhd);
-        numerical_flux(g.kind, ud, uhd, n, gam, fd);
+        numerical_flux(FK >= 0 ? FK : g.kind, ud, uhd, n, gam, fd);
         if (VISC) {
           double qq[5][3];
 #pragma unroll
@@ -1160,7 +1160,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
 #pragma unroll
             for (int s2 = 0; s2 < 5; ++s2) ui[s2] = mk(g.uinf[s2], 0.0);
             const double mn[3] = {-n[0], -n[1], -n[2]};
-            numerical_flux(g.kind, ui, uhd, mn, gam, gd);
+            numerical_flux(FK >= 0 ? FK : g.kind, ui, uhd, mn, gam, gd);
             if (VISC) {
               double winf[5];
               if (g.form == FORM_ENTROPY) entropy_vars(g.uinf, gam, winf);
