@@ -837,52 +837,6 @@ __device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, doub
   return __syncthreads_or(bad) == 0;
 }
 
-// Batched in-place inverse: mats[e] holds S_e row-major on entry and
-// S_e^-1 column-major on exit (register Gauss-Jordan, implicit pivoting).
-template <int N, int TR, int TC>
-struct GJBatch {
-  using G = GJDims<N, TR, TC>;
-  static constexpr size_t bytes = (size_t)(N * N + 2 * G::NPR + 2 * G::NPC) * 8 + (size_t)(2 * N + 2) * 4;
-};
-
-template <int N, int TR, int TC>
-__global__ void __launch_bounds__(TR * TC, 2)
-k_gj_batched(int nmat, double* __restrict__ mats, unsigned long long* status) {
-  using G = GJDims<N, TR, TC>;
-  extern __shared__ __align__(16) double smem[];
-  double* Y = smem;
-  double* colbuf = Y + N * N;
-  double* rowbuf = colbuf + 2 * G::NPR;
-  int* q = (int*)(rowbuf + 2 * G::NPC);
-  int* qi = q + N;
-  int* flag = qi + N;
-  const int tid = threadIdx.x;
-  const int tr = tid / TC, tc = tid % TC;
-  for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
-    double* M = mats + (size_t)m * N * N;
-    double w[G::RA][G::CB];
-#pragma unroll
-    for (int a = 0; a < G::RA; ++a)
-#pragma unroll
-      for (int b = 0; b < G::CB; ++b) {
-        const int r = tr + TR * a, c = tc + TC * b;
-        w[a][b] = (r < N && c < N) ? M[r * N + c] : 0.0;
-      }
-    bool ok = gj_inverse_reg<N, TR, TC>(w, colbuf, rowbuf, q, flag);
-#pragma unroll
-    for (int a = 0; a < G::RA; ++a)
-#pragma unroll
-      for (int b = 0; b < G::CB; ++b) {
-        const int r = tr + TR * a, c = tc + TC * b;
-        if (r < N && c < N) Y[r * N + c] = w[a][b];
-      }
-    __syncthreads();
-    ok = gj_store_colmajor<N, TR * TC>(Y, q, qi, M) && ok;
-    if (!ok && tid == 0) report(status, 0, 0, m);
-    __syncthreads();
-  }
-}
-
 // ===========================================================================
 // K2 v2 (P <= 3): linearization with the S assembly on the FP64 tensor cores.
 //   pointwise : C[q][kk][st] (kk=0..2: -vol_w J^-1 dF/dw, kk=3: weight vol_w du/dw)
@@ -891,7 +845,7 @@ k_gj_batched(int nmat, double* __restrict__ mats, unsigned long long* status) {
 //   stage 2   : S_st[i][j] += sum_q D[q][i][st] phi[q][j]            (DMMA, per q chunk)
 //               accumulated in registers across chunks
 //   faces     : hw/hhat/hh tensors + face blocks of S (as in v1)
-//   inverse   : register-blocked Gauss-Jordan, implicit pivoting
+//   inverse   : k_gj_blocked (mhdg_gj_blocked.cuh), implicit pivoting
 // ===========================================================================
 template <int P>
 struct Lin2 {
@@ -1202,7 +1156,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
       }
     }
     __syncthreads();
-    // ---- S (row-major) to the S^-1 buffer; k_gj_batched inverts in place
+    // ---- S (row-major) to the S^-1 buffer; k_gj_blocked inverts in place
     double* out = sinv + (size_t)e * NM * NM;
     for (int o = tid; o < NM * NM; o += NT) out[o] = S[o];
   }
