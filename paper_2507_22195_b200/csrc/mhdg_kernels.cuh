@@ -912,6 +912,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
   for (int i = tid; i < L::C_; i += NT) sC[i] = 0.0;
 
   for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    if (tid == 0) bulk_wait_read();   // previous macro's S left shared memory
     __syncthreads();
     for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
     if (VISC)
@@ -1155,11 +1156,13 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         for (int t = 0; t < 5; ++t) S[r * NM + c + t] += acc2[t];
       }
     }
+    // ---- S (row-major) to the S^-1 buffer with one TMA bulk store (80 KB at
+    //      k = 3); k_gj_blocked inverts it in place
+    fence_proxy_async();
     __syncthreads();
-    // ---- S (row-major) to the S^-1 buffer; k_gj_blocked inverts in place
-    double* out = sinv + (size_t)e * NM * NM;
-    for (int o = tid; o < NM * NM; o += NT) out[o] = S[o];
+    if (tid == 0) bulk_s2g(sinv + (size_t)e * NM * NM, S, (uint32_t)(NM * NM * sizeof(double)));
   }
+  if (tid == 0) bulk_wait_all();
 }
 
 // ===========================================================================
