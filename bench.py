@@ -482,6 +482,9 @@ def run_b200_partitioned(args, rank, local_rank, world):
             torch.distributed.init_process_group("nccl", device_id=dev)
         else:
             torch.distributed.init_process_group("gloo")
+        # first collective over the whole group (NCCL's batched P2P requires
+        # the communicator to exist before ranks exchange with neighbours only)
+        torch.distributed.barrier()
     gas = GasModel(1.4)
     n = args.ncells
     mesh = build_box_macro_mesh(np.array([[0.0, 10.0 * world], [0.0, 10.0], [0.0, 10.0]]),
