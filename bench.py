@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--flux", default="es")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-implicit", action="store_true", help="skip the implicit-step timing")
     ap.add_argument("--cpu-sample-n", type=int, default=4)
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas instead of the partitioned operator")
@@ -396,33 +397,35 @@ def run_b200(args, rank, local_rank, world):
 
     # ---- time per implicit step (one DIRK(3,3) step, dt = 0.01) and one
     # Jacobian build, measured after the operator timing (not part of value)
-    from paper_2507_22195_b200.time_march import DIRKIntegrator
+    implicit = None
+    if not args.no_implicit:
+        from paper_2507_22195_b200.time_march import DIRKIntegrator
 
-    # the operator timing's factors are released first; one untimed build
-    # warms the caching allocator so the timed build measures the kernels
-    # (and the allocator's steady state), as inside a long run
-    del lin
-    lin2 = disc.jacobian(fields, stage, ptc_weight=1.0)
-    del lin2
-    torch.cuda.synchronize()
-    jb0 = time.perf_counter()
-    lin2 = disc.jacobian(fields, stage, ptc_weight=1.0)
-    torch.cuda.synchronize()
-    jac_ms = 1e3 * (time.perf_counter() - jb0)
-    del lin2
-    integ = DIRKIntegrator(disc)
-    torch.cuda.synchronize()
-    st0 = time.perf_counter()
-    integ.run(fields, t_final=0.01, dt=0.01)
-    torch.cuda.synchronize()
-    step_s = time.perf_counter() - st0
-    rec = integ.records
-    implicit = {"seconds_per_step": step_s, "jacobian_build_ms": jac_ms,
-                "newton_iters": sum(r["newton_iters"] for r in rec),
-                "fgmres_outer": sum(r["fgmres_iters"] for r in rec),
-                "fgmres_inner": sum(r["inner_iters_total"] for r in rec),
-                "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
-                "dt": 0.01, "tableau": "DIRK(3,3)"}
+        # the operator timing's factors are released first; one untimed build
+        # warms the caching allocator so the timed build measures the kernels
+        # (and the allocator's steady state), as inside a long run
+        del lin
+        lin2 = disc.jacobian(fields, stage, ptc_weight=1.0)
+        del lin2
+        torch.cuda.synchronize()
+        jb0 = time.perf_counter()
+        lin2 = disc.jacobian(fields, stage, ptc_weight=1.0)
+        torch.cuda.synchronize()
+        jac_ms = 1e3 * (time.perf_counter() - jb0)
+        del lin2
+        integ = DIRKIntegrator(disc)
+        torch.cuda.synchronize()
+        st0 = time.perf_counter()
+        integ.run(fields, t_final=0.01, dt=0.01)
+        torch.cuda.synchronize()
+        step_s = time.perf_counter() - st0
+        rec = integ.records
+        implicit = {"seconds_per_step": step_s, "jacobian_build_ms": jac_ms,
+                    "newton_iters": sum(r["newton_iters"] for r in rec),
+                    "fgmres_outer": sum(r["fgmres_iters"] for r in rec),
+                    "fgmres_inner": sum(r["inner_iters_total"] for r in rec),
+                    "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
+                    "dt": 0.01, "tableau": "DIRK(3,3)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -285,14 +285,15 @@ template <int P>
 static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int has_stage, double alpha,
                            const double* off, int check, double* rw, double* rt, cudaStream_t s) {
   using RC = ResCfg<P>;
-  size_t smem = RC::bytes;
+  size_t smem = RC::bytes(c->geo.has_uinf);
   // the ES flux gets its own instantiation (40 B of spills instead of 244 B
   // with the run-time switch over all four kinds; a KEPES-only variant
   // allocates worse than the switch, so KEPES / EC / LF share it)
   auto go = [&](auto kern) -> int {
     if (set_smem(kern, smem)) return MHDG_CUDA_ERROR;
     int per_sm = occ(kern, RC::NT, smem);
-    int blocks = std::min((c->E + RC::EB - 1) / RC::EB, c->n_sms * per_sm);
+    const int batches = (c->E + RC::EB - 1) / RC::EB;
+    int blocks = std::min((batches + RC::NG - 1) / RC::NG, c->n_sms * per_sm);
     kern<<<std::max(1, blocks), RC::NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check, rw, rt,
                                                    c->d_status);
     return MHDG_OK;

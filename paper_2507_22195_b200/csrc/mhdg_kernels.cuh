@@ -123,33 +123,64 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// pure (non-volatile) DMMA: lets the scheduler hoist the operand loads
+__device__ __forceinline__ void dmma_8x8x4_nv(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// named barrier over one thread group (id 0 is __syncthreads)
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Residual launch geometry.  A CTA holds NG independent groups of NW warps;
+// each group processes EB macros per iteration and synchronises with its own
+// named barrier, so the groups drift in phase against each other like
+// separate CTAs would, while the basis tables (B in DMMA-fragment layout,
+// phi^T for the per-point interpolation) are staged ONCE per CTA in shared
+// memory instead of being re-read through a small L1 (with 4 CTAs x 51 KB of
+// shared memory per SM the 51 KB of tables missed L1 a third of the time:
+// 590 MB of L2 reads per launch at config 2 for 132 MB of DRAM traffic).
 template <int P>
 struct ResCfg {
   using D = Dims<P>;
-  static constexpr int EB = (P >= 4) ? 1 : 2;      // macros per CTA iteration
-  static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per CTA
-  static constexpr int NT = NW * 32;
-#ifndef MHDG_RES_MINB
-#define MHDG_RES_MINB 4
-#endif
-  static constexpr int MINB = (P >= 4) ? 2 : MHDG_RES_MINB;   // resident CTAs per SM (register cap)
+  static constexpr int EB = (P >= 4) ? 1 : 2;      // macros per group iteration
+  static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per group
+  static constexpr int GT = NW * 32;               // threads per group
+  static constexpr int NG = (P >= 4) ? 1 : 4;      // groups per CTA
+  static constexpr bool SB = P <= 3;               // basis tables in shared memory
+  static constexpr int NT = NG * GT;
+  static constexpr int MINB = (P >= 4) ? 2 : 1;    // resident CTAs per SM (register cap)
   static constexpr int WPM = NW / EB;              // warps per macro
   static constexpr int DW = WPM / 2;               // DMMA warps per macro (K split)
   static constexpr int FW = WPM - DW;              // face warps per macro
   static constexpr int NTILE = (D::NN + 7) / 8;    // DMMA N tiles over nodes
+  // B row stride: >= NN and = 4 (mod 16) so that the B-fragment reads
+  // (lane = 4 n + kk -> word kk*RS + n) are free of bank conflicts
+  static constexpr int RS = D::NN + ((4 - D::NN) % 16 + 16) % 16;
   static constexpr int GS = 21;                    // G row stride (odd)
   static constexpr int W_ = D::NN * 5, TR_ = 4 * D::NFN * 5, G_ = D::NQ * GS, H_ = 4 * D::NQF * 5,
                        FR_ = 4 * D::NFN * 5, VOL_ = DW * D::NN * 5, GEO_ = 26;
-  static constexpr int per_macro = W_ + TR_ + G_ + 2 * H_ + FR_ + VOL_ + GEO_;
-  static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF;
+  // w / trace (phase 1) and the face / volume partial rows (phases 2-3)
+  // share one region; the far-field flux rows HG exist only with a
+  // free-stream boundary (has_uinf)
+  static constexpr int AREG = (W_ + TR_ > FR_ + VOL_) ? W_ + TR_ : FR_ + VOL_;
+  static constexpr int per_macro_base = AREG + G_ + H_ + GEO_;
+  static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF +
+                                (SB ? D::NQ * 4 * RS + D::NN * D::NQ : 0);
   static constexpr int per_macro_int = 4 + 4 * D::NFN + 4;   // x 2 slots (double-buffered)
   static constexpr int META = 4 + 4 * D::NFN + 4;
-  static constexpr int WPT = (EB * D::NN * 5 + NT - 1) / NT;       // prefetch registers per thread
-  static constexpr int TPT = (EB * 4 * D::NFN * 5 + NT - 1) / NT;
-  static constexpr int GPT = (EB * 26 + NT - 1) / NT;
+  static constexpr int WPT = (EB * D::NN * 5 + GT - 1) / GT;       // prefetch registers per thread
+  static constexpr int TPT = (EB * 4 * D::NFN * 5 + GT - 1) / GT;
+  static constexpr int GPT = (EB * 26 + GT - 1) / GT;
   static constexpr int table_int = 4 * D::NFN + 3 * D::NN;
-  static constexpr size_t bytes =
-      (size_t)(tables + EB * per_macro) * 8 + (size_t)(table_int + 2 * EB * per_macro_int) * 4;
+  __host__ __device__ static constexpr int per_macro(int has_uinf) { return per_macro_base + (has_uinf ? H_ : 0); }
+  __host__ __device__ static constexpr size_t bytes(int has_uinf) {
+    return (size_t)(tables + NG * EB * per_macro(has_uinf)) * 8 +
+           (size_t)(table_int + NG * 2 * EB * per_macro_int) * 4;
+  }
 };
 
 template <int P, int FK = -1>   // FK: flux kind fixed at compile time (-1: g.kind at run time)
@@ -159,35 +190,49 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
            double* __restrict__ r_w, double* __restrict__ r_tr, unsigned long long* status) {
   using D = Dims<P>;
   using R = ResCfg<P>;
-  constexpr int NT = R::NT, EB = R::EB, NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF;
-  constexpr int GS = R::GS;
+  constexpr int NT = R::NT, GT = R::GT, EB = R::EB, NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF;
+  constexpr int GS = R::GS, RS = R::RS;
   extern __shared__ __align__(16) double smem[];
+  const int PM = R::per_macro(g.has_uinf);
   double* sPF = smem;                              // 4*NQF*FS
   double* sFP = sPF + 4 * NQF * D::FS;             // NQF*FS
   double* sQW = sFP + NQF * D::FS;                 // NQ
   double* sFW = sQW + NQ;                          // NQF
-  double* mb = sFW + NQF;                          // EB * per_macro
-  int* sRows = (int*)(mb + EB * R::per_macro);     // 4*NFN
+  double* sB = sFW + NQF;                          // NQ*4*RS (SB)
+  double* sPT = sB + (R::SB ? NQ * 4 * RS : 0);    // NN*NQ   (SB)
+  double* mball = smem + R::tables;                // NG * EB * PM
+  int* sRows = (int*)(mball + R::NG * EB * PM);    // 4*NFN
   int* sNF = sRows + 4 * NFN;                      // 3*NN
-  int* ib = sNF + 3 * NN;                          // EB * per_macro_int
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* iball = sNF + 3 * NN;                       // NG * 2 * EB * per_macro_int
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int grp = tid / GT, gtid = tid % GT, gwarp = gtid >> 5;
   for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
   for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
   for (int i = tid; i < NQ; i += NT) sQW[i] = g.qw[i];
   for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
   for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
   for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
+  if constexpr (R::SB) {
+    for (int i = tid; i < NQ * 4 * NN; i += NT) sB[(i / NN) * RS + i % NN] = g.B[i];
+    for (int i = tid; i < NN * NQ; i += NT) sPT[i] = g.phit[i];
+  }
+  __syncthreads();
   const double gam = g.gamma;
-  const double* __restrict__ Bt = g.B;
+  const double* __restrict__ Bt = R::SB ? sB : g.B;
+  const int bstride = R::SB ? RS : NN;
+  double* mb = mball + grp * EB * PM;
+  int* ib = iball + grp * 2 * EB * R::per_macro_int;
+  const int bar_id = 1 + grp;
+  auto gsync = [&]() { group_sync(bar_id, GT); };
 
-  auto W = [&](int m) { return mb + m * R::per_macro; };
+  auto W = [&](int m) { return mb + m * PM; };
   auto TR = [&](int m) { return W(m) + R::W_; };
-  auto G = [&](int m) { return TR(m) + R::TR_; };
+  auto FR = [&](int m) { return W(m); };                 // aliases W / TR (phases 2-3)
+  auto VOL = [&](int m) { return W(m) + R::FR_; };
+  auto G = [&](int m) { return W(m) + R::AREG; };
   auto H = [&](int m) { return G(m) + R::G_; };
-  auto HG = [&](int m) { return H(m) + R::H_; };
-  auto FR = [&](int m) { return HG(m) + R::H_; };
-  auto VOL = [&](int m) { return FR(m) + R::FR_; };
-  auto GEO = [&](int m) { return VOL(m) + R::VOL_; };
+  auto GEO = [&](int m) { return H(m) + R::H_; };
+  auto HG = [&](int m) { return GEO(m) + R::GEO_; };     // only with has_uinf
   // meta (face ids, trace permutations, boundary flags) is double-buffered:
   // slot `cur` serves the batch being computed, slot `cur ^ 1` receives the
   // next batch's, whose w / trace / geometry are prefetched into registers
@@ -217,12 +262,12 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     const int nmn = min(EB, g.E - e0n);
 #pragma unroll
     for (int c = 0; c < R::WPT; ++c) {
-      const int i = tid + c * NT;
+      const int i = gtid + c * GT;
       if (i < nmn * NN * 5) pW[c] = w[(size_t)e0n * NN * 5 + i];
     }
 #pragma unroll
     for (int c = 0; c < R::GPT; ++c) {
-      const int i = tid + c * NT;
+      const int i = gtid + c * GT;
       if (i < EB * 26) pG[c] = geo_ld(e0n, i);
     }
   };
@@ -230,7 +275,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     const int nmn = min(EB, g.E - e0n);
 #pragma unroll
     for (int c = 0; c < R::TPT; ++c) {
-      const int i = tid + c * NT;
+      const int i = gtid + c * GT;
       if (i < nmn * 4 * NFN * 5) {
         const int m = i / (4 * NFN * 5), r = i % (4 * NFN * 5);
         const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
@@ -239,43 +284,44 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
     }
   };
+  const int gidx = blockIdx.x * R::NG + grp, gstride = gridDim.x * R::NG;
   {   // first batch: meta, then its data
-    const int e00 = blockIdx.x * EB;
+    const int e00 = gidx * EB;
     if (e00 < g.E) {
-      for (int i = tid; i < EB * R::META; i += NT) {
+      for (int i = gtid; i < EB * R::META; i += GT) {
         int v = 0;
         meta_ld(e00, i, v);
         ib[(i / R::META) * R::per_macro_int + i % R::META] = v;
       }
-      __syncthreads();
+      gsync();
       prefetch_wg(e00);
       prefetch_tr(e00, 0);
     }
   }
 
-  for (int e0 = blockIdx.x * EB; e0 < g.E; e0 += gridDim.x * EB) {
+  for (int e0 = gidx * EB; e0 < g.E; e0 += gstride * EB) {
     const int nm = min(EB, g.E - e0);
-    const int e1 = e0 + gridDim.x * EB;
-    __syncthreads();
+    const int e1 = e0 + gstride * EB;
+    gsync();
 #pragma unroll
     for (int c = 0; c < R::WPT; ++c) {
-      const int i = tid + c * NT;
+      const int i = gtid + c * GT;
       if (i < nm * NN * 5) W(i / (NN * 5))[i % (NN * 5)] = pW[c];
     }
 #pragma unroll
     for (int c = 0; c < R::TPT; ++c) {
-      const int i = tid + c * NT;
+      const int i = gtid + c * GT;
       if (i < nm * 4 * NFN * 5) TR(i / (4 * NFN * 5))[i % (4 * NFN * 5)] = pT[c];
     }
 #pragma unroll
     for (int c = 0; c < R::GPT; ++c) {
-      const int i = tid + c * NT;
+      const int i = gtid + c * GT;
       if (i < EB * 26) GEO(i / 26)[i % 26] = pG[c];
     }
-    __syncthreads();
+    gsync();
 
     // ---- 1a. face quadrature points: two-point flux, weighted
-    for (int it = tid; it < nm * 4 * NQF; it += NT) {
+    for (int it = gtid; it < nm * 4 * NQF; it += GT) {
       const int m = it / (4 * NQF), kq = it % (4 * NQF), k = kq / NQF, q = kq % NQF, e = e0 + m;
       const double* pf = sPF + kq * D::FS;
       const double* fp = sFP + q * D::FS;
@@ -305,7 +351,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       double* h = H(m) + kq * 5;
 #pragma unroll
       for (int s = 0; s < 5; ++s) h[s] = fwq * fh[s];
-      if (BND(m)[k] && g.has_uinf) {
+      if (g.has_uinf && BND(m)[k]) {
         const double mn[3] = {-n[0], -n[1], -n[2]};
         double gh[5];
         numerical_flux(FK >= 0 ? FK : g.kind, g.uinf, uh, mn, gam, gh);
@@ -314,13 +360,13 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
     }
     // ---- 1b. volume quadrature points: reference-space flux + temporal term
-    for (int it = tid; it < nm * NQ; it += NT) {
+    for (int it = gtid; it < nm * NQ; it += GT) {
       const int m = it / NQ, q = it % NQ, e = e0 + m;
       const double* sw = W(m);
       double wq[5] = {0, 0, 0, 0, 0};
 #pragma unroll 4
       for (int i = 0; i < NN; ++i) {
-        const double a = __ldg(g.phit + (size_t)i * NQ + q);
+        const double a = R::SB ? sPT[i * NQ + q] : __ldg(g.phit + (size_t)i * NQ + q);
 #pragma unroll
         for (int s = 0; s < 5; ++s) wq[s] += a * sw[i * 5 + s];
       }
@@ -351,18 +397,18 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     }
     // next batch: meta straight into the other slot, w / geometry into registers
     if (e1 < g.E) {
-      for (int i = tid; i < EB * R::META; i += NT) {
+      for (int i = gtid; i < EB * R::META; i += GT) {
         int v = 0;
         meta_ld(e1, i, v);
         ib[((cur ^ 1) * EB + i / R::META) * R::per_macro_int + i % R::META] = v;
       }
       prefetch_wg(e1);
     }
-    __syncthreads();
+    gsync();
 
     // ---- 2. contraction, warp-specialized per macro
     {
-      const int m = warp / R::WPM, role = warp % R::WPM;
+      const int m = gwarp / R::WPM, role = gwarp % R::WPM;
       if (m < nm) {
         if (role < R::DW) {
           // DMMA: C[s][i] += sum_k G^T[s][k] B[k][i], k = (q, kk)
@@ -372,15 +418,18 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
 #pragma unroll
           for (int t = 0; t < R::NTILE; ++t) c[t][0] = c[t][1] = 0.0;
           const double* gm = G(m);
+#pragma unroll 2
           for (int q = q0; q < q1; ++q) {
             const double a = s_a < 5 ? gm[q * GS + kk * 5 + s_a] : 0.0;
-            const double* brow = Bt + ((size_t)q * 4 + kk) * NN;
+            const double* brow = Bt + ((size_t)q * 4 + kk) * bstride;
+            double b[R::NTILE];
 #pragma unroll
             for (int t = 0; t < R::NTILE; ++t) {
               const int i = t * 8 + (lane >> 2);
-              const double b = i < NN ? __ldg(brow + i) : 0.0;
-              dmma_8x8x4(c[t], a, b);
+              b[t] = i < NN ? (R::SB ? brow[i] : __ldg(brow + i)) : 0.0;
             }
+#pragma unroll
+            for (int t = 0; t < R::NTILE; ++t) dmma_8x8x4_nv(c[t], a, b[t]);
           }
           double* vol = VOL(m) + role * NN * 5;
           const int s_c = lane >> 2;
@@ -419,10 +468,10 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         }
       }
     }
-    __syncthreads();
+    gsync();
     if (e1 < g.E) prefetch_tr(e1, cur ^ 1);
     // ---- 3. r_w = volume part + face parts (tile order)
-    for (int o = tid; o < nm * NN * 5; o += NT) {
+    for (int o = gtid; o < nm * NN * 5; o += GT) {
       const int m = o / (NN * 5), is = o % (NN * 5), i = is / 5, s = is % 5;
       double r = VOL(m)[is];
 #pragma unroll

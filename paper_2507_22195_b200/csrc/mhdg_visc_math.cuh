@@ -29,7 +29,7 @@ MHDG_DEV void vt_grads(int form, const T w[5], const T u[5], const Q g[5][3], do
                        T gt[3]) {
   if (form == FORM_ENTROPY) {
     const T ve = w[4];
-    const T ive2 = 1.0 / (ve * ve);
+    const T ive2 = dv(1.0, ve * ve);
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -40,7 +40,7 @@ MHDG_DEV void vt_grads(int form, const T w[5], const T u[5], const Q g[5][3], do
   }
   T rho, vel[3], p;
   primitive(u, gam, rho, vel, p);
-  const T irho = 1.0 / rho;
+  const T irho = dv(1.0, rho);
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
