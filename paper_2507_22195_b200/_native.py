@@ -22,7 +22,7 @@ from .errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmhdg_b200.so")
+LIB_PATH = os.environ.get("MHDG_LIB") or os.path.join(HERE, "libmhdg_b200.so")
 
 MHDG_OK = 0
 _WHERE = ("volume sub", "face tile", "trace tile")

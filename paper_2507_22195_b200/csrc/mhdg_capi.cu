@@ -1023,6 +1023,44 @@ extern "C" double mhdg_dmma_probe(int device, void* stream) {
   return flops / (ms * 1e-3) / 1e9;
 }
 
+#ifdef MHDG_RES_TIMING
+// experiment builds: residual phase clocks, DFMA dependent-chain latency
+extern "C" void mhdg_debug_res_clk(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_res_clk, sizeof(unsigned long long) * 9);
+  if (reset) {
+    unsigned long long z[9] = {0};
+    cudaMemcpyToSymbol(g_res_clk, z, sizeof(z));
+  }
+}
+__global__ void k_dfma_lat(int n, double* out, long long* cyc) {
+  double a = out[0], b = 1.0000001, c = 1e-9;
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) a = fma(a, b, c);
+  const long long t1 = clock64();
+  out[1] = a;
+  cyc[0] = t1 - t0;
+}
+__global__ void k_trans_lat(int n, double* out, long long* cyc, int which) {
+  double a = out[0] + 1.5;
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) a = which == 0 ? ::log(a) + 2.0 : which == 1 ? ::exp(a) * 0.5 : ddiv(a, 1.25);
+  const long long t1 = clock64();
+  out[1] = a;
+  cyc[0] = t1 - t0;
+}
+extern "C" double mhdg_debug_latency(int which) {
+  double* d; long long* cy; long long h = 0;
+  cudaMalloc(&d, 16); cudaMalloc(&cy, 8); cudaMemset(d, 0, 16);
+  const int n = 4096;
+  if (which < 0) k_dfma_lat<<<1, 32>>>(n, d, cy);
+  else k_trans_lat<<<1, 32>>>(n, d, cy, which);
+  cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d); cudaFree(cy);
+  return (double)h / n;
+}
+#endif
+
 extern "C" double mhdg_fp64_probe(int device, void* stream) {
   cudaStream_t s = S(stream);
   cudaSetDevice(device);

@@ -123,6 +123,21 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+#ifdef MHDG_RES_TIMING
+// phase clocks of the residual (experiment builds only): per group leader
+__device__ unsigned long long g_res_clk[9];
+#define RES_T(k)                                                   \
+  do {                                                             \
+    const long long t_ = clock64();                                \
+    if (gtid == 0) atomicAdd(&g_res_clk[k], (unsigned long long)(t_ - t_prev)); \
+    t_prev = t_;                                                   \
+  } while (0)
+#else
+#define RES_T(k) \
+  do {           \
+  } while (0)
+#endif
+
 // pure (non-volatile) DMMA: lets the scheduler hoist the operand loads
 __device__ __forceinline__ void dmma_8x8x4_nv(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -154,21 +169,22 @@ struct ResCfg {
   static constexpr int NT = NG * GT;
   static constexpr int MINB = (P >= 4) ? 2 : 1;    // resident CTAs per SM (register cap)
   static constexpr int WPM = NW / EB;              // warps per macro
-  static constexpr int DW = WPM / 2;               // DMMA warps per macro (K split)
-  static constexpr int FW = WPM - DW;              // face warps per macro
-  static constexpr int NTILE = (D::NN + 7) / 8;    // DMMA N tiles over nodes
+  static constexpr int NTILE = (D::NN + 7) / 8;    // DMMA N tiles over nodes (volume test)
+  static constexpr int FMT = (2 * D::NFN + 7) / 8; // face test: M tiles over phi_face + fphi rows
+  static constexpr int FKS = (D::NQF + 3) / 4;     // face test: K steps over face points
+  static constexpr int AF_ = 4 * FMT * FKS * 32;   // face-test A fragments, lane-swizzled
   // B row stride: >= NN and = 4 (mod 16) so that the B-fragment reads
   // (lane = 4 n + kk -> word kk*RS + n) are free of bank conflicts
   static constexpr int RS = D::NN + ((4 - D::NN) % 16 + 16) % 16;
   static constexpr int GS = 21;                    // G row stride (odd)
   static constexpr int W_ = D::NN * 5, TR_ = 4 * D::NFN * 5, G_ = D::NQ * GS, H_ = 4 * D::NQF * 5,
-                       FR_ = 4 * D::NFN * 5, VOL_ = DW * D::NN * 5, GEO_ = 26;
+                       FR_ = 4 * D::NFN * 5, VOL_ = WPM * D::NN * 5, GEO_ = 26;
   // w / trace (phase 1) and the face / volume partial rows (phases 2-3)
   // share one region; the far-field flux rows HG exist only with a
   // free-stream boundary (has_uinf)
   static constexpr int AREG = (W_ + TR_ > FR_ + VOL_) ? W_ + TR_ : FR_ + VOL_;
   static constexpr int per_macro_base = AREG + G_ + H_ + GEO_;
-  static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF +
+  static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF + AF_ +
                                 (SB ? D::NQ * 4 * RS + D::NN * D::NQ : 0);
   static constexpr int per_macro_int = 4 + 4 * D::NFN + 4;   // x 2 slots (double-buffered)
   static constexpr int META = 4 + 4 * D::NFN + 4;
@@ -198,7 +214,8 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   double* sFP = sPF + 4 * NQF * D::FS;             // NQF*FS
   double* sQW = sFP + NQF * D::FS;                 // NQ
   double* sFW = sQW + NQ;                          // NQF
-  double* sB = sFW + NQF;                          // NQ*4*RS (SB)
+  double* sAF = sFW + NQF;                         // AF_
+  double* sB = sAF + R::AF_;                       // NQ*4*RS (SB)
   double* sPT = sB + (R::SB ? NQ * 4 * RS : 0);    // NN*NQ   (SB)
   double* mball = smem + R::tables;                // NG * EB * PM
   int* sRows = (int*)(mball + R::NG * EB * PM);    // 4*NFN
@@ -212,6 +229,19 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
   for (int i = tid; i < 4 * NFN; i += NT) sRows[i] = g.rows[i];
   for (int i = tid; i < 3 * NN; i += NT) sNF[i] = g.nodef[i];
+  // face-test A fragments: [k][mt][ks][lane], lane = 4 r + c holds
+  // A[row = 8 mt + r][q = 4 ks + c] (row < NFN: phi_face[k][q][row],
+  // row < 2 NFN: fphi[q][row - NFN], zero padding elsewhere)
+  for (int i = tid; i < R::AF_; i += NT) {
+    const int ln = i % 32, ks = (i / 32) % R::FKS, mt = (i / (32 * R::FKS)) % R::FMT, k = i / (32 * R::FKS * R::FMT);
+    const int row = mt * 8 + (ln >> 2), q = ks * 4 + (ln & 3);
+    double v = 0.0;
+    if (q < NQF) {
+      if (row < NFN) v = g.pf[(k * NQF + q) * NFN + row];
+      else if (row < 2 * NFN) v = g.fphi[q * NFN + row - NFN];
+    }
+    sAF[i] = v;
+  }
   if constexpr (R::SB) {
     for (int i = tid; i < NQ * 4 * NN; i += NT) sB[(i / NN) * RS + i % NN] = g.B[i];
     for (int i = tid; i < NN * NQ; i += NT) sPT[i] = g.phit[i];
@@ -299,10 +329,14 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     }
   }
 
+#ifdef MHDG_RES_TIMING
+  long long t_prev = clock64();
+#endif
   for (int e0 = gidx * EB; e0 < g.E; e0 += gstride * EB) {
     const int nm = min(EB, g.E - e0);
     const int e1 = e0 + gstride * EB;
     gsync();
+    RES_T(0);
 #pragma unroll
     for (int c = 0; c < R::WPT; ++c) {
       const int i = gtid + c * GT;
@@ -319,6 +353,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       if (i < EB * 26) GEO(i / 26)[i % 26] = pG[c];
     }
     gsync();
+    RES_T(1);
 
     // ---- 1a. face quadrature points: two-point flux, weighted
     for (int it = gtid; it < nm * 4 * NQF; it += GT) {
@@ -359,6 +394,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         for (int s = 0; s < 5; ++s) HG(m)[kq * 5 + s] = fwq * gh[s];
       }
     }
+    RES_T(2);
     // ---- 1b. volume quadrature points: reference-space flux + temporal term
     for (int it = gtid; it < nm * NQ; it += GT) {
       const int m = it / NQ, q = it % NQ, e = e0 + m;
@@ -404,32 +440,32 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
       prefetch_wg(e1);
     }
+    RES_T(3);
     gsync();
+    RES_T(4);
 
-    // ---- 2. contraction, warp-specialized per macro
+    // ---- 2. contraction on the FP64 tensor cores, all WPM warps of a macro
+    // alike: warp r takes the volume-test K range q in [r NQ/WPM, (r+1)
+    // NQ/WPM) and the face tests of faces k = r, r + WPM, ...
     {
       const int m = gwarp / R::WPM, role = gwarp % R::WPM;
       if (m < nm) {
-        if (role < R::DW) {
-          // DMMA: C[s][i] += sum_k G^T[s][k] B[k][i], k = (q, kk)
-          const int q0 = role * NQ / R::DW, q1 = (role + 1) * NQ / R::DW;
+        {   // volume test: C[s][i] += sum_k G^T[s][k] B[k][i], k = (q, kk)
+          const int q0 = role * NQ / R::WPM, q1 = (role + 1) * NQ / R::WPM;
           const int s_a = lane >> 2, kk = lane & 3;
           double c[R::NTILE][2];
 #pragma unroll
           for (int t = 0; t < R::NTILE; ++t) c[t][0] = c[t][1] = 0.0;
           const double* gm = G(m);
-#pragma unroll 2
           for (int q = q0; q < q1; ++q) {
             const double a = s_a < 5 ? gm[q * GS + kk * 5 + s_a] : 0.0;
             const double* brow = Bt + ((size_t)q * 4 + kk) * bstride;
-            double b[R::NTILE];
 #pragma unroll
             for (int t = 0; t < R::NTILE; ++t) {
               const int i = t * 8 + (lane >> 2);
-              b[t] = i < NN ? (R::SB ? brow[i] : __ldg(brow + i)) : 0.0;
+              const double b = i < NN ? (R::SB ? brow[i] : __ldg(brow + i)) : 0.0;
+              dmma_8x8x4_nv(c[t], a, b);
             }
-#pragma unroll
-            for (int t = 0; t < R::NTILE; ++t) dmma_8x8x4_nv(c[t], a, b[t]);
           }
           double* vol = VOL(m) + role * NN * 5;
           const int s_c = lane >> 2;
@@ -442,40 +478,70 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
                 if (i < NN) vol[i * 5 + s_c] = c[t][h2];
               }
           }
-        } else {
-          const int fr = role - R::DW, fl = fr * 32 + lane, fstride = R::FW * 32;
-          const double* hm = H(m);
-          const int* fid = FID(m);
-          const int* tdx = TID(m);
-          const bool bnd_any = g.has_uinf && (BND(m)[0] | BND(m)[1] | BND(m)[2] | BND(m)[3]);
-          for (int o = fl; o < 4 * NFN * 5; o += fstride) {
-            const int k = o / (NFN * 5), j = (o / 5) % NFN, s = o % 5;
-            double a = 0.0, b = 0.0;
-#pragma unroll 4
-            for (int q = 0; q < NQF; ++q) {
-              const double hv = hm[(k * NQF + q) * 5 + s];
-              a += sPF[(k * NQF + q) * D::FS + j] * hv;
-              b += sFP[q * D::FS + j] * hv;
-            }
-            FR(m)[o] = a;
-            if (bnd_any && BND(m)[k]) {
-              double gsum = 0.0;
-              for (int q = 0; q < NQF; ++q) gsum += sFP[q * D::FS + j] * HG(m)[(k * NQF + q) * 5 + s];
-              b += gsum;
-            }
-            atomicAdd(&r_tr[((size_t)fid[k] * NFN + tdx[k * NFN + j]) * 5 + s], b);
+        }
+        // face tests, per face k: C[row][s] = sum_q A[row][q] H[k][q][s] with
+        // rows 0..NFN-1 = phi_face (the r_w face rows) and NFN..2NFN-1 = fphi
+        // (this side's r_trace contribution); A fragments come pre-swizzled
+        // from sAF, the far-field rows HG (free-stream faces only) take a
+        // second pass over the fphi rows
+        const double* hm = H(m);
+        const int* fid = FID(m);
+        const int* tdx = TID(m);
+        const int kq_ = lane & 3, n_ = lane >> 2;
+        for (int k = role; k < 4; k += R::WPM) {
+          const bool bnd = g.has_uinf && BND(m)[k];
+          double c[R::FMT][2], cg[R::FMT][2];
+#pragma unroll
+          for (int t = 0; t < R::FMT; ++t) c[t][0] = c[t][1] = cg[t][0] = cg[t][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < R::FKS; ++ks) {
+            const int q = ks * 4 + kq_;
+            const double hb = (n_ < 5 && q < NQF) ? hm[(k * NQF + q) * 5 + n_] : 0.0;
+#pragma unroll
+            for (int t = 0; t < R::FMT; ++t)
+              dmma_8x8x4_nv(c[t], sAF[((k * R::FMT + t) * R::FKS + ks) * 32 + lane], hb);
           }
+          if (bnd) {
+#pragma unroll
+            for (int ks = 0; ks < R::FKS; ++ks) {
+              const int q = ks * 4 + kq_;
+              const double hb = (n_ < 5 && q < NQF) ? HG(m)[(k * NQF + q) * 5 + n_] : 0.0;
+#pragma unroll
+              for (int t = 0; t < R::FMT; ++t)
+                dmma_8x8x4_nv(cg[t], sAF[((k * R::FMT + t) * R::FKS + ks) * 32 + lane], hb);
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < R::FMT; ++t)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int row = t * 8 + n_, sc = kq_ * 2 + h2;
+              if (sc < 5) {
+                if (row < NFN) {
+                  FR(m)[(k * NFN + row) * 5 + sc] = c[t][h2];
+                } else if (row < 2 * NFN) {
+                  const int j = row - NFN;
+                  const double v = bnd ? c[t][h2] + cg[t][h2] : c[t][h2];
+                  atomicAdd(&r_tr[((size_t)fid[k] * NFN + tdx[k * NFN + j]) * 5 + sc], v);
+                }
+              }
+            }
         }
       }
     }
+#ifdef MHDG_RES_TIMING
+    if (gtid == 32) atomicAdd(&g_res_clk[8], (unsigned long long)(clock64() - t_prev));
+#endif
+    RES_T(5);
     gsync();
+    RES_T(6);
     if (e1 < g.E) prefetch_tr(e1, cur ^ 1);
     // ---- 3. r_w = volume part + face parts (tile order)
     for (int o = gtid; o < nm * NN * 5; o += GT) {
       const int m = o / (NN * 5), is = o % (NN * 5), i = is / 5, s = is % 5;
       double r = VOL(m)[is];
 #pragma unroll
-      for (int d2 = 1; d2 < R::DW; ++d2) r += VOL(m)[d2 * NN * 5 + is];
+      for (int d2 = 1; d2 < R::WPM; ++d2) r += VOL(m)[d2 * NN * 5 + is];
 #pragma unroll
       for (int c2 = 0; c2 < 3; ++c2) {
         const int kj = sNF[i * 3 + c2];
@@ -484,6 +550,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
       r_w[(size_t)e0 * NN * 5 + o] = r;
     }
+    RES_T(7);
     cur ^= 1;
   }
 }

@@ -1,0 +1,43 @@
+"""Experiment: residual phase clocks and FP64 latencies (needs the
+MHDG_RES_TIMING build: MHDG_LIB=paper_2507_22195_b200/libmhdg_timing.so)."""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2507_22195_b200 import _native  # noqa: E402
+from bench import make_problem  # noqa: E402
+from paper_2507_22195_b200.assembly import Discretization, StageContext  # noqa: E402
+from paper_2507_22195_b200.fluxes import DissipationSpec  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+gas, mesh, vx, alpha = make_problem(n, 3, "es")
+disc = Discretization(mesh, p=3, gas=gas, formulation="entropy", flux=DissipationSpec("es"),
+                      device="cuda:0")
+fields = disc.project(vx.initial)
+stage = StageContext(alpha=alpha, offset=(-alpha * disc.volume_quad_states(fields)).contiguous())
+lib = _native.load()
+lib.mhdg_debug_latency.restype = C.c_double
+lat = {k: lib.mhdg_debug_latency(v) for k, v in (("dfma", -1), ("log", 0), ("exp", 1), ("div", 2))}
+buf = (C.c_ulonglong * 9)()
+for _ in range(3):
+    disc.residuals(fields, stage, sync=False)
+torch.cuda.synchronize()
+lib.mhdg_debug_res_clk(buf, C.c_int(1))
+reps = 20
+for _ in range(reps):
+    disc.residuals(fields, stage, sync=False)
+torch.cuda.synchronize()
+lib.mhdg_debug_res_clk(buf, C.c_int(1))
+E = disc.mesh.n_macros
+groups = 148 * 4
+iters = reps * (E / 2) / groups          # group iterations per group
+names = ["top_barrier", "stage_data", "face_points", "vol_points+prefetch", "phase1_barrier",
+         "contraction", "phase2_barrier", "combine+prefetch_tr", "contraction_face_warp"]
+cyc = {nm: buf[i] / groups / iters for i, nm in enumerate(names)}
+print(json.dumps({"latency_cycles": lat, "cycles_per_group_iteration": cyc,
+                  "total": sum(cyc.values())}, indent=1))
