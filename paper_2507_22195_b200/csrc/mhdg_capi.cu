@@ -142,6 +142,23 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   g.tidx = upload_i64(c, t->trace_idx, E * 4 * NFN, err);
   g.bnd = t->boundary_st ? upload(c, t->boundary_st, E * 4, err) : nullptr;
   g.fsides = upload_i64(c, t->face_sides, (size_t)c->n_owned * 2, err);
+  {   // packed per-macro geometry and meta for the residual's coalesced prefetch
+    std::vector<double> geo26(E * 26);
+    std::vector<int> meta(E * (8 + 4 * NFN));
+    for (size_t e = 0; e < E; ++e) {
+      double* gp = &geo26[e * 26];
+      gp[0] = t->sub_det[e];
+      for (int i = 0; i < 9; ++i) gp[1 + i] = t->sub_inv_jac[e * 9 + i];
+      for (int i = 0; i < 12; ++i) gp[10 + i] = t->face_normals[e * 12 + i];
+      for (int i = 0; i < 4; ++i) gp[22 + i] = t->face_area[e * 4 + i];
+      int* mp = &meta[e * (8 + 4 * NFN)];
+      for (int i = 0; i < 4; ++i) mp[i] = (int)t->face_id_st[e * 4 + i];
+      for (int i = 0; i < 4 * NFN; ++i) mp[4 + i] = (int)t->trace_idx[e * 4 * NFN + i];
+      for (int i = 0; i < 4; ++i) mp[4 + 4 * NFN + i] = t->boundary_st ? (int)t->boundary_st[e * 4 + i] : 0;
+    }
+    g.geo26 = upload(c, geo26.data(), geo26.size(), err);
+    g.meta = upload(c, meta.data(), meta.size(), err);
+  }
   g.has_uinf = t->freestream != nullptr;
   if (t->freestream)
     for (int s = 0; s < 5; ++s) g.uinf[s] = t->freestream[s];

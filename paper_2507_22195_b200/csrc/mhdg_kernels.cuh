@@ -58,6 +58,8 @@ struct Geo {
   const int* tidx;     // (E, 4, NFN)
   const unsigned char* bnd;  // (E, 4)
   const int* fsides;   // (F, 2)
+  const double* geo26; // (E, 26): det, J^-1 (9), normals (12), areas (4)
+  const int* meta;     // (E, 8 + 4 NFN): face ids (4), trace permutations (4 NFN), boundary flags (4)
   int has_uinf;
   double uinf[5];
 };
@@ -272,20 +274,11 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   auto FID = [&](int m) { return ib + (cur * EB + m) * R::per_macro_int; };
   auto TID = [&](int m) { return FID(m) + 4; };
   auto BND = [&](int m) { return TID(m) + 4 * NFN; };
-  auto meta_ld = [&](int e0n, int i, int& v) {     // i over EB*META
-    const int m = i / R::META, r = i % R::META, e = e0n + m;
-    if (e >= g.E) return;
-    if (r < 4) v = g.fid[e * 4 + r];
-    else if (r < 4 + 4 * NFN) v = g.tidx[(size_t)e * 4 * NFN + r - 4];
-    else v = g.bnd ? g.bnd[e * 4 + r - 4 - 4 * NFN] : 0;
+  auto meta_ld = [&](int e0n, int i, int& v) {     // i over EB*META (packed per-macro meta)
+    if (e0n + i / R::META < g.E) v = g.meta[(size_t)e0n * R::META + i];
   };
-  auto geo_ld = [&](int e0n, int i) -> double {     // i over EB*26
-    const int m = i / 26, c = i % 26, e = e0n + m;
-    if (e >= g.E) return 0.0;
-    if (c == 0) return g.det[e];
-    if (c < 10) return g.invj[(size_t)e * 9 + c - 1];
-    if (c < 22) return g.nrm[(size_t)e * 12 + c - 10];
-    return g.area[(size_t)e * 4 + c - 22];
+  auto geo_ld = [&](int e0n, int i) -> double {     // i over EB*26 (packed per-macro geometry)
+    return e0n + i / 26 < g.E ? g.geo26[(size_t)e0n * 26 + i] : 0.0;
   };
   double pW[R::WPT], pT[R::TPT], pG[R::GPT];
   auto prefetch_wg = [&](int e0n) {                 // w and geometry
