@@ -199,6 +199,11 @@ int64_t mhdg_launch_count(const mhdg_ctx* ctx);
 double mhdg_fp64_probe(int device, void* stream);
 /* FP64 tensor-core (mma.sync m8n8k4 f64, SASS DMMA) probe, GFLOP/s */
 double mhdg_dmma_probe(int device, void* stream);
+/* y[i] = f(x[i]) with the operator's device elementary functions
+   (fn 0: exp, 1: log, 2: division 1 / x): accuracy check of the pointwise
+   algebra against libm; replaces no reference symbol (numpy's exp / log /
+   true_divide inside gas.py / fluxes.py) */
+int mhdg_math_eval(int fn, int64_t n, const double* x, double* y, void* stream);
 const char* mhdg_version(void);
 
 #ifdef __cplusplus

@@ -95,6 +95,7 @@ _SIGS = {
     "mhdg_launch_count": (C.c_int64, [C.c_void_p]),
     "mhdg_fp64_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_dmma_probe": (C.c_double, [C.c_int, C.c_void_p]),
+    "mhdg_math_eval": (C.c_int, [C.c_int, C.c_int64, dptr, dptr, C.c_void_p]),
     "mhdg_version": (C.c_char_p, []),
 }
 
@@ -170,6 +171,18 @@ def raise_for(code, st=None, context=""):
 def dmma_probe(device=0):
     lib = require_cuda()
     return float(lib.mhdg_dmma_probe(device, stream_handle()))
+
+
+def math_eval(fn, x):
+    """Device elementary function (0 exp, 1 log, 2 reciprocal) on a CUDA
+    float64 tensor (accuracy tests)."""
+    import torch
+
+    lib = require_cuda()
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    raise_for(lib.mhdg_math_eval(fn, x.numel(), ptr(x), ptr(y), stream_handle()), context="(math_eval)")
+    return y
 
 
 def fp64_probe(device=0):

@@ -1015,6 +1015,18 @@ __global__ void k_dmma_probe(int iters, double* out) {
 }
 
 // FP64 tensor-core (DMMA m8n8k4) throughput probe, GFLOP/s
+__global__ void k_math_eval(int fn, int64_t n, const double* x, double* y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fn == 0 ? dexp(x[i]) : fn == 1 ? dlog(x[i]) : dv(1.0, x[i]);
+}
+
+extern "C" int mhdg_math_eval(int fn, int64_t n, const double* x, double* y, void* stream) {
+  if (n <= 0) return MHDG_OK;
+  k_math_eval<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, S(stream)>>>(fn, n, x, y);
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
 extern "C" double mhdg_dmma_probe(int device, void* stream) {
   cudaStream_t s = S(stream);
   cudaSetDevice(device);
