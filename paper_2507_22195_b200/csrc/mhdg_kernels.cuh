@@ -1441,8 +1441,14 @@ struct Face2 {
   static constexpr int ZPT = (EB * D::NM + NT - 1) / NT;
   static constexpr int META = 4 + 4 * D::NFN;
   static constexpr int MPT = (EB * (META + 4) + NT - 1) / NT;
+  // phase-2 test contraction on DMMA: M tiles over the NFN face nodes, K
+  // steps over the NQF face points; A fragments (phi_face per tile for
+  // MODE 0, fphi for MODE 1) lane-swizzled in shared memory
+  static constexpr int TMT = (D::NFN + 7) / 8;
+  static constexpr int TKS = (D::NQF + 3) / 4;
+  static constexpr int AF = 4 * TMT * TKS * 32;
   static constexpr int doubles = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQF + EB * (NX + D::NM + 2 * NI * 5 + NX) +
-                                 3 * EB * 4;
+                                 3 * EB * 4 + AF;
   static constexpr int ints = 4 * D::NFN + 3 * D::NN + 3 * EB * META;
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
 };
@@ -1468,10 +1474,20 @@ k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restri
   double* sB = sA + EB * NI * 5;          // EB*NI*5
   double* sT = sB + EB * NI * 5;          // EB*NX
   double* sAr = sT + EB * NX;             // 3*EB*4
-  int* sRows = (int*)(sAr + 3 * EB * 4);
+  double* sAF = sAr + 3 * EB * 4;         // AF
+  int* sRows = (int*)(sAF + F2::AF);
   int* sNF = sRows + 4 * NFN;
   int* sMeta = sNF + 3 * NN;              // 3*EB*META
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // [k][mt][ks][lane]: lane = 4 r + c holds F[q = 4 ks + c][j = 8 mt + r]
+  for (int i = tid; i < F2::AF; i += NT) {
+    const int ln = i % 32, ks = (i / 32) % F2::TKS, mt = (i / (32 * F2::TKS)) % F2::TMT,
+              k = i / (32 * F2::TKS * F2::TMT);
+    const int j = mt * 8 + (ln >> 2), q = ks * 4 + (ln & 3);
+    double v = 0.0;
+    if (q < NQF && j < NFN) v = (MODE == 0) ? g.pf[(k * NQF + q) * NFN + j] : g.fphi[q * NFN + j];
+    sAF[i] = v;
+  }
   for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
   for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
   for (int i = tid; i < NQF; i += NT) sFW[i] = g.fw[i];
@@ -1602,38 +1618,41 @@ k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restri
             a += rA[c][s2 * 5 + t] * (MODE == 0 ? xq[t] : zq[t]);
             if (use_b) b += rB[c][s2 * 5 + t] * xq[t];
           }
-          sA[it * 5 + s2] = fwq * a;
-          if (use_b) sB[it * 5 + s2] = fwq * b;
+          // MODE 1 tests A_hv z and A_hh x with the same fphi rows: one sum
+          sA[it * 5 + s2] = use_b ? fwq * a + fwq * b : fwq * a;
         }
       }
     }
     // next batch: tensor rows / trace values / z into the same registers
     if (e1 < g.E) prefetch(e1, s1);
     __syncthreads();
-    // ---- phase 2: per (slot m, tile k, node j): 5 outputs
-    for (int o = tid; o < nm * 4 * NFN; o += NT) {
-      const int m = o / (4 * NFN), kj = o % (4 * NFN), k = kj / NFN, j = kj % NFN;
-      double a[5] = {0, 0, 0, 0, 0}, b[5] = {0, 0, 0, 0, 0};
-      const double* A = sA + (m * NI + k * NQF) * 5;
-      const double* B = sB + (m * NI + k * NQF) * 5;
-#pragma unroll 4
-      for (int q = 0; q < NQF; ++q) {
-        const double f = (MODE == 0) ? sPF[(k * NQF + q) * D::FS + j] : sFP[q * D::FS + j];
+    // ---- phase 2: per (slot m, tile k) on DMMA: C[j][s] = sum_q F[q][j] V[q][s]
+    for (int job = warp; job < nm * 4; job += NT / 32) {
+      const int m = job / 4, k = job % 4;
+      const double* V = sA + (m * NI + k * NQF) * 5;
+      const double* af = sAF + (MODE == 0 ? k * F2::TMT * F2::TKS * 32 : 0);
+      const int kq_ = lane & 3, n_ = lane >> 2;
+      double c[F2::TMT][2];
 #pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) {
-          a[s2] += f * A[q * 5 + s2];
-          if (use_b) b[s2] += f * B[q * 5 + s2];
+      for (int t = 0; t < F2::TMT; ++t) c[t][0] = c[t][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < F2::TKS; ++ks) {
+        const int q = ks * 4 + kq_;
+        const double vb = (n_ < 5 && q < NQF) ? V[q * 5 + n_] : 0.0;
+#pragma unroll
+        for (int t = 0; t < F2::TMT; ++t) dmma_8x8x4(c[t], af[(t * F2::TKS + ks) * 32 + lane], vb);
+      }
+      const int* mt = sMeta + (slot * EB + m) * META;
+#pragma unroll
+      for (int t = 0; t < F2::TMT; ++t)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int j = t * 8 + n_, s2 = kq_ * 2 + h2;
+          if (j < NFN && s2 < 5) {
+            if (MODE == 0) sT[m * NX + (k * NFN + j) * 5 + s2] = c[t][h2];
+            else atomicAdd(&out[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s2], c[t][h2]);
+          }
         }
-      }
-      if (MODE == 0) {
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) sT[m * NX + kj * 5 + s2] = a[s2];
-      } else {
-        const int* mt = sMeta + (slot * EB + m) * META;
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2)
-          atomicAdd(&out[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s2], b[s2] + a[s2]);
-      }
     }
     if (MODE == 0) {
       __syncthreads();
