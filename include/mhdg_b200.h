@@ -140,6 +140,24 @@ int mhdg_precond_factor(mhdg_ctx* ctx, const mhdg_lin_buffers* lin,
                         const int32_t* tidx_remote, const double* area_remote,
                         mhdg_status* st, void* stream);
 
+/* Macro-range forms for partitioned runs (no reference counterpart: the
+ * reference is single-process; these compute the same operators as
+ * Discretization.residuals (assembly.py:459-549) and LinearizedSystem.matvec
+ * (assembly.py:1131-1143) restricted to the contributions of macros
+ * [e_begin, e_end), accumulated into the trace outputs).  zero = 1 clears
+ * r_trace / y (and the residual status) first.  Calling them for the
+ * interior macros and then for the halo macros gives results bit-identical
+ * to the whole-range call (two contributions per trace node, 0 + a + b),
+ * which lets the trace halo exchange overlap the interior work.  matvec
+ * stages: bit 0 = face-in + local solve, bit 1 = face-out.  Inviscid only
+ * (MHDG_INVALID_CONFIG for a viscous context). */
+int mhdg_residual_range(mhdg_ctx* ctx, const double* w, const double* trace, int has_stage,
+                        double alpha, const double* offset, int check, double* r_w,
+                        double* r_trace, int64_t e_begin, int64_t e_end, int zero,
+                        void* stream);
+int mhdg_matvec_range(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* x, double* y,
+                      int64_t e_begin, int64_t e_end, int stages, int zero, void* stream);
+
 /* LinearizedSystem.matvec (assembly.py:1131-1143): y = A^ x */
 int mhdg_matvec(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* x,
                 double* y, void* stream);

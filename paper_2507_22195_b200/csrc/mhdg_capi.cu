@@ -270,6 +270,25 @@ static int set_smem(K kernel, size_t bytes) {
   return MHDG_OK;
 }
 
+// Geo restricted to macros [e0, e1): per-macro arrays offset, E = count
+// (partitioned runs launch the interior and halo macros separately so the
+// halo exchange overlaps the interior work)
+static Geo geo_range(const Geo& g0, int e0, int e1, int nfn) {
+  Geo g = g0;
+  g.E = e1 - e0;
+  g.e_base = g0.e_base + e0;
+  g.det += e0;
+  g.invj += (size_t)e0 * 9;
+  g.nrm += (size_t)e0 * 12;
+  g.area += (size_t)e0 * 4;
+  g.fid += (size_t)e0 * 4;
+  g.tidx += (size_t)e0 * 4 * nfn;
+  if (g.bnd) g.bnd += (size_t)e0 * 4;
+  g.geo26 += (size_t)e0 * 26;
+  g.meta += (size_t)e0 * (8 + 4 * nfn);
+  return g;
+}
+
 static int grid_for(mhdg_ctx* c, int items, int per_sm) {
   return std::max(1, std::min(items, c->n_sms * per_sm));
 }
@@ -300,8 +319,16 @@ static void decode_status(unsigned long long key, mhdg_status* st, bool admissib
 
 template <int P>
 static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int has_stage, double alpha,
-                           const double* off, int check, double* rw, double* rt, cudaStream_t s) {
+                           const double* off, int check, double* rw, double* rt, cudaStream_t s,
+                           int e0 = 0, int e1 = -1) {
   using RC = ResCfg<P>;
+  if (e1 < 0) e1 = c->E;
+  if (e1 <= e0) return MHDG_OK;
+  const Geo gv = geo_range(c->geo, e0, e1, c->nfn);
+  const size_t NMe = (size_t)c->nn * 5, NQe = (size_t)c->nq * 5;
+  w += e0 * NMe;
+  rw += e0 * NMe;
+  if (off) off += e0 * NQe;
   size_t smem = RC::bytes(c->geo.has_uinf);
   // the ES flux gets its own instantiation (40 B of spills instead of 244 B
   // with the run-time switch over all four kinds; a KEPES-only variant
@@ -309,9 +336,9 @@ static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int h
   auto go = [&](auto kern) -> int {
     if (set_smem(kern, smem)) return MHDG_CUDA_ERROR;
     int per_sm = occ(kern, RC::NT, smem);
-    const int batches = (c->E + RC::EB - 1) / RC::EB;
+    const int batches = (gv.E + RC::EB - 1) / RC::EB;
     int blocks = std::min((batches + RC::NG - 1) / RC::NG, c->n_sms * per_sm);
-    kern<<<std::max(1, blocks), RC::NT, smem, s>>>(c->geo, w, tr, has_stage, alpha, off, check, rw, rt,
+    kern<<<std::max(1, blocks), RC::NT, smem, s>>>(gv, w, tr, has_stage, alpha, off, check, rw, rt,
                                                    c->d_status);
     return MHDG_OK;
   };
@@ -360,6 +387,26 @@ extern "C" int mhdg_solve_gradient(mhdg_ctx* c, const double* w, const double* t
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;
+}
+
+extern "C" int mhdg_residual_range(mhdg_ctx* c, const double* w, const double* trace, int has_stage,
+                                   double alpha, const double* offset, int check, double* r_w,
+                                   double* r_trace, int64_t e_begin, int64_t e_end, int zero,
+                                   void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  if (c->visc || e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
+  if (zero) {
+    CK(cudaMemsetAsync(c->d_status, 0xff, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(r_trace, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
+  }
+  const int e0 = (int)e_begin, e1 = (int)e_end;
+  switch (c->p) {
+    case 1: return launch_residual<1>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s, e0, e1);
+    case 2: return launch_residual<2>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s, e0, e1);
+    case 3: return launch_residual<3>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s, e0, e1);
+    default: return launch_residual<4>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s, e0, e1);
+  }
 }
 
 extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, const double* q, int has_stage,
@@ -565,28 +612,38 @@ extern "C" int mhdg_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, int n
 // ---------------------------------------------------------------------------
 // condensed operator
 // ---------------------------------------------------------------------------
+// stages: bit 0 = face-in (g = -A_vh x) + local solve (z = S^-1 g), bit 1 =
+// face-out (y += A_hh x + A_hv z); macros [e0, e1)
 template <int P>
 static int condensed_face2(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
-                           double* y, double* dw, cudaStream_t s) {
+                           double* y, double* dw, cudaStream_t s, int e0 = 0, int e1 = -1, int stages = 3) {
   using D = Dims<P>;
   using F2 = Face2<P>;
+  if (e1 < 0) e1 = c->E;
+  if (e1 <= e0) return MHDG_OK;
   const size_t fsm = F2::bytes;
   if (set_smem(k_face2<P, 0>, fsm) || set_smem(k_face2<P, 1>, fsm)) return MHDG_CUDA_ERROR;
-  const int nb = (c->E + F2::EB - 1) / F2::EB;
-  double* gbuf = c->d_gbuf;
-  double* zbuf = (mode == 2) ? dw : c->d_zbuf;
-  if (mode != 1) {
-    k_face2<P, 0><<<grid_for(c, nb, occ(k_face2<P, 0>, 128, fsm)), 128, fsm, s>>>(c->geo, mode, L->hhat, nullptr, x,
-                                                                                  nullptr, rw, gbuf);
+  const Geo gv = geo_range(c->geo, e0, e1, c->nfn);
+  const int E = e1 - e0;
+  const int nb = (E + F2::EB - 1) / F2::EB;
+  const size_t ten = (size_t)e0 * 4 * c->nqf * 25, vm = (size_t)e0 * D::NM;
+  double* gbuf = c->d_gbuf + vm;
+  double* zbuf = ((mode == 2) ? dw : c->d_zbuf) + vm;
+  const double* rwv = rw ? rw + vm : nullptr;
+  if (stages & 1) {
+    if (mode != 1) {
+      k_face2<P, 0><<<grid_for(c, nb, occ(k_face2<P, 0>, 128, fsm)), 128, fsm, s>>>(gv, mode, L->hhat + ten, nullptr,
+                                                                                    x, nullptr, rwv, gbuf);
+      c->launches++;
+    }
+    constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
+    k_local_solve<D::NM, GT><<<grid_for(c, E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(
+        E, L->sinv + vm * D::NM, mode == 1 ? rwv : gbuf, mode == 1, zbuf);
     c->launches++;
   }
-  constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
-  k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(
-      c->E, L->sinv, mode == 1 ? rw : gbuf, mode == 1, zbuf);
-  c->launches++;
-  if (mode != 2) {
-    k_face2<P, 1><<<grid_for(c, nb, occ(k_face2<P, 1>, 128, fsm)), 128, fsm, s>>>(c->geo, mode, L->hw, L->hh, x,
-                                                                                  zbuf, nullptr, y);
+  if ((stages & 2) && mode != 2) {
+    k_face2<P, 1><<<grid_for(c, nb, occ(k_face2<P, 1>, 128, fsm)), 128, fsm, s>>>(gv, mode, L->hw + ten, L->hh + ten,
+                                                                                  x, zbuf, nullptr, y);
     c->launches++;
   }
   CK(cudaGetLastError());
@@ -633,6 +690,21 @@ static int condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const dou
     case 2: return condensed_face2<2>(c, mode, L, x, rw, y, dw, s);
     case 3: return condensed_face2<3>(c, mode, L, x, rw, y, dw, s);
     default: return condensed_face2<4>(c, mode, L, x, rw, y, dw, s);
+  }
+}
+
+extern "C" int mhdg_matvec_range(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* x, double* y,
+                                 int64_t e_begin, int64_t e_end, int stages, int zero, void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  if (c->visc || e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
+  if (zero) CK(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
+  const int e0 = (int)e_begin, e1 = (int)e_end;
+  switch (c->p) {
+    case 1: return condensed_face2<1>(c, 0, L, x, nullptr, y, nullptr, s, e0, e1, stages);
+    case 2: return condensed_face2<2>(c, 0, L, x, nullptr, y, nullptr, s, e0, e1, stages);
+    case 3: return condensed_face2<3>(c, 0, L, x, nullptr, y, nullptr, s, e0, e1, stages);
+    default: return condensed_face2<4>(c, 0, L, x, nullptr, y, nullptr, s, e0, e1, stages);
   }
 }
 

@@ -60,6 +60,7 @@ struct Geo {
   const int* fsides;   // (F, 2)
   const double* geo26; // (E, 26): det, J^-1 (9), normals (12), areas (4)
   const int* meta;     // (E, 8 + 4 NFN): face ids (4), trace permutations (4 NFN), boundary flags (4)
+  int e_base;          // global index of macro 0 of this (sub-range) view, for error reports
   int has_uinf;
   double uinf[5];
 };
@@ -367,10 +368,10 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         }
       }
       double u[5], uh[5];
-      if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e);
-      if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e);
-      if (check && !admissible(u, gam)) report(status, 1 + k, 2, e);
-      if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e);
+      if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e + g.e_base);
+      if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e + g.e_base);
+      if (check && !admissible(u, gam)) report(status, 1 + k, 2, e + g.e_base);
+      if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e + g.e_base);
       const double* geo = GEO(m);
       const double n[3] = {geo[10 + k * 3], geo[11 + k * 3], geo[12 + k * 3]};
       double fh[5];
@@ -400,8 +401,8 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         for (int s = 0; s < 5; ++s) wq[s] += a * sw[i * 5 + s];
       }
       double u[5];
-      if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e);
-      if (check && !admissible(u, gam)) report(status, 0, 2, e);
+      if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e + g.e_base);
+      if (check && !admissible(u, gam)) report(status, 0, 2, e + g.e_base);
       double F[5][3];
       flux(u, gam, F);
       const double* geo = GEO(m);

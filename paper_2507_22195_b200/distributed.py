@@ -66,10 +66,47 @@ class PartitionedDiscretization:
         return math.sqrt(self.allreduce([local])[0])
 
     # -- operators -----------------------------------------------------------
+    @property
+    def overlap(self):
+        """Halo exchange overlapped with the interior macros' kernels: an
+        asynchronous transport (start / finish), an inviscid operator and a
+        non-empty contiguous interior range."""
+        i0, i1 = self.part.interior
+        return (hasattr(self.exchange, "fill_ghosts_start") and self.local.viscosity is None
+                and i1 > i0)
+
     def residuals(self, fields, stage=None, check=True, sync=True):
-        res = self.local.residuals(self._fields(fields), stage, check, sync=sync)
-        self.exchange.reduce_partials(res.r_trace)
-        return ResidualSet(res.r_w, res.r_trace, None, _disc=self)
+        if not self.overlap:
+            res = self.local.residuals(self._fields(fields), stage, check, sync=sync)
+            self.exchange.reduce_partials(res.r_trace)
+            return ResidualSet(res.r_w, res.r_trace, None, _disc=self)
+        # ghost traces in flight while the interior macros run; halo macros
+        # after them; then the ghost-face partial sums go to their owners
+        torch = __import__("torch")
+        d = self.local
+        w, tr = d._fields(fields)
+        fields.w, fields.trace = w, tr
+        h = self.exchange.fill_ghosts_start(tr)
+        r_w, r_tr = torch.empty_like(w), torch.empty_like(tr)
+        off = None
+        if stage is not None and stage.offset is not None:
+            off = d._dev(stage.offset)
+        args = (int(stage is not None), float(stage.alpha) if stage is not None else 0.0,
+                N.ptr(off), int(bool(check)), N.ptr(r_w), N.ptr(r_tr))
+        i0, i1 = self.part.interior
+        rc = d._lib.mhdg_residual_range(d._ctx, N.ptr(w), N.ptr(tr), *args, i0, i1, 1,
+                                        N.stream_handle())
+        N.raise_for(rc)
+        self.exchange.fill_ghosts_finish(h)
+        for a, b in self.part.halo_ranges():
+            rc = d._lib.mhdg_residual_range(d._ctx, N.ptr(w), N.ptr(tr), *args, a, b, 0,
+                                            N.stream_handle())
+            N.raise_for(rc)
+        if sync:
+            st = N.Status()
+            N.raise_for(d._lib.mhdg_status_fetch(d._ctx, C.byref(st), N.stream_handle()), st)
+        self.exchange.reduce_partials(r_tr)
+        return ResidualSet(r_w, r_tr, None, _disc=self)
 
     def jacobian(self, fields, stage=None, ptc_weight=0.0):
         return PartitionedLinearizedSystem(self, self._fields(fields), stage, ptc_weight)
@@ -120,10 +157,32 @@ class PartitionedLinearizedSystem:
         N.raise_for(rc, st)
 
     def matvec(self, xh):
+        pd = self.pdisc
         x = self.disc._dev(xh).reshape(self.trace_shape).clone()
-        self.pdisc.exchange.fill_ghosts(x)
-        y = self.lin.matvec(x)
-        self.pdisc.exchange.reduce_partials(y)
+        if not pd.overlap:
+            pd.exchange.fill_ghosts(x)
+            y = self.lin.matvec(x)
+            pd.exchange.reduce_partials(y)
+            return y
+        # x ghosts in flight during the interior face-in + local solves; the
+        # halo macros' full chain next; the ghost-face partials of y travel
+        # during the interior face-out (interior macros touch no halo face)
+        torch = __import__("torch")
+        d, buf = self.disc, C.byref(self.lin._buf)
+        y = torch.empty_like(x)
+        i0, i1 = pd.part.interior
+        ex = pd.exchange
+        h = ex.fill_ghosts_start(x)
+        N.raise_for(d._lib.mhdg_matvec_range(d._ctx, buf, N.ptr(x), N.ptr(y), i0, i1, 1, 1,
+                                             N.stream_handle()))
+        ex.fill_ghosts_finish(h)
+        for a, b in pd.part.halo_ranges():
+            N.raise_for(d._lib.mhdg_matvec_range(d._ctx, buf, N.ptr(x), N.ptr(y), a, b, 3, 0,
+                                                 N.stream_handle()))
+        h2 = ex.reduce_partials_start(y)
+        N.raise_for(d._lib.mhdg_matvec_range(d._ctx, buf, N.ptr(x), N.ptr(y), i0, i1, 2, 0,
+                                             N.stream_handle()))
+        ex.reduce_partials_finish(h2)
         return y
 
     def condensed_rhs(self, res):

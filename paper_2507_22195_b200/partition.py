@@ -79,6 +79,38 @@ class LocalPartition:
                 plan.ghost[h] = g2l[theirs]
         self.plan = plan
         self.tables = self._local_tables(t, lo, hi, g2l, nb_r, own_r)
+        self.interior = self._interior_range()
+
+    def _interior_range(self):
+        """Contiguous local macro range [i0, i1) touching no halo face (a
+        face shared with another rank).  Those macros read only owned trace
+        values and write only faces no neighbour contributes to, so their
+        kernels can run while the halo exchange is in flight; the halo
+        macros [0, i0) and [i1, E_l) run after it.  With x-slab partitions
+        the halo macros are the first and last cell planes of the slab."""
+        halo_face = np.zeros(self.n_local_faces, dtype=bool)
+        halo_face[self.n_owned:] = True
+        for ids in self.plan.owned_shared.values():
+            halo_face[ids] = True
+        halo_macro = halo_face[self.tables.face_id_st].any(axis=1)
+        # longest run of non-halo macros (the few non-halo tets of the slab's
+        # boundary cell planes simply run with the halo macros)
+        best, start = (0, 0), None
+        for e, h in enumerate(np.append(halo_macro, True)):
+            if not h and start is None:
+                start = e
+            elif h and start is not None:
+                if e - start > best[1] - best[0]:
+                    best = (start, e)
+                start = None
+        return best
+
+    def halo_ranges(self):
+        E_l = self.macro_hi - self.macro_lo
+        i0, i1 = self.interior
+        if i1 <= i0:
+            return [(0, E_l)]
+        return [r for r in ((0, i0), (i1, E_l)) if r[1] > r[0]]
 
     def _local_tables(self, t, lo, hi, g2l, nb_r, own_r):
         """HDGTables-shaped namespace restricted to this rank."""
@@ -181,6 +213,35 @@ class TorchDistExchange:
         self.host_staged = dist.is_initialized() and dist.get_backend(group) == "gloo"
 
     def _exchange(self, sends, recvs):
+        self._finish(self._start(sends, recvs))
+
+    def _start(self, sends, recvs):
+        """Issue the batched point-to-point exchange.  NCCL: the transfers
+        run on NCCL's stream after the work already queued on the current
+        stream; nothing blocks until _finish."""
+        import torch.distributed as dist
+
+        if self.host_staged:
+            return (None, sends, recvs, True)
+        ops = []
+        for h, buf in sends.items():
+            ops.append(dist.P2POp(dist.isend, buf.contiguous(), h, self.group))
+        for h, buf in recvs.items():
+            ops.append(dist.P2POp(dist.irecv, buf, h, self.group))
+        reqs = dist.batch_isend_irecv(ops) if ops and dist.is_initialized() else []
+        return (reqs, sends, recvs, False)
+
+    def _finish(self, handle):
+        """Make the current stream wait for the exchange (host-staged gloo
+        transfers run here, synchronously)."""
+        reqs, sends, recvs, staged = handle
+        if staged:
+            self._exchange_staged(sends, recvs)
+            return
+        for req in reqs:
+            req.wait()
+
+    def _exchange_staged(self, sends, recvs):
         import torch.distributed as dist
 
         if self.host_staged:
@@ -201,6 +262,11 @@ class TorchDistExchange:
 
     def reduce_partials(self, trace_like):
         """owner += neighbour partials on shared faces; returns trace_like."""
+        return self.reduce_partials_finish(self.reduce_partials_start(trace_like))
+
+    def reduce_partials_start(self, trace_like):
+        """Send the ghost-face partial sums (snapshot taken now, on the
+        current stream); the owner's add happens in reduce_partials_finish."""
         import torch
 
         plan = self.part.plan
@@ -208,13 +274,24 @@ class TorchDistExchange:
                  for h, ids in plan.ghost.items()}
         recvs = {h: torch.empty((len(ids),) + tuple(trace_like.shape[1:]), dtype=trace_like.dtype,
                                 device=trace_like.device) for h, ids in plan.owned_shared.items()}
-        self._exchange(sends, recvs)
-        for h, ids in plan.owned_shared.items():
+        return (trace_like, recvs, self._start(sends, recvs))
+
+    def reduce_partials_finish(self, handle):
+        import torch
+
+        trace_like, recvs, h_ex = handle
+        self._finish(h_ex)
+        for h, ids in self.part.plan.owned_shared.items():
             idx = torch.as_tensor(ids, device=trace_like.device)
             trace_like[idx] = trace_like[idx] + recvs[h]
         return trace_like
 
     def fill_ghosts(self, trace_like):
+        return self.fill_ghosts_finish(self.fill_ghosts_start(trace_like))
+
+    def fill_ghosts_start(self, trace_like):
+        """Send owned values of shared faces (snapshot taken now); the ghost
+        rows are written in fill_ghosts_finish."""
         import torch
 
         plan = self.part.plan
@@ -222,8 +299,14 @@ class TorchDistExchange:
                  for h, ids in plan.owned_shared.items()}
         recvs = {h: torch.empty((len(ids),) + tuple(trace_like.shape[1:]), dtype=trace_like.dtype,
                                 device=trace_like.device) for h, ids in plan.ghost.items()}
-        self._exchange(sends, recvs)
-        for h, ids in plan.ghost.items():
+        return (trace_like, recvs, self._start(sends, recvs))
+
+    def fill_ghosts_finish(self, handle):
+        import torch
+
+        trace_like, recvs, h_ex = handle
+        self._finish(h_ex)
+        for h, ids in self.part.plan.ghost.items():
             trace_like[torch.as_tensor(ids, device=trace_like.device)] = recvs[h]
         return trace_like
 

@@ -43,6 +43,28 @@ def test_partition_structure(world):
         assert sum(len(v) for v in pg.recv_remote_idx.values()) == pg.n_remote_sides
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_interior_and_halo_macro_ranges(world):
+    """Interior macros (run while the halo exchange is in flight) touch no
+    face shared with another rank; interior + halo ranges tile the slab."""
+    t = small_tables(n=(8, 2, 2))
+    for g in range(world):
+        pg = LocalPartition(t, g, world)
+        E_l = pg.macro_hi - pg.macro_lo
+        i0, i1 = pg.interior
+        assert 0 < i0 < i1 < E_l, (i0, i1)
+        shared = set(range(pg.n_owned, pg.n_local_faces))
+        for ids in pg.plan.owned_shared.values():
+            shared |= set(int(i) for i in ids)
+        fid = pg.tables.face_id_st
+        assert not any(int(f) in shared for f in fid[i0:i1].ravel())
+        covered = sorted([(i0, i1)] + pg.halo_ranges())
+        assert covered[0][0] == 0 and covered[-1][1] == E_l
+        assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+        # the interior is most of the slab (all but ~the boundary cell planes)
+        assert i1 - i0 >= E_l - 2 * 6 * 2 * 2
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
