@@ -636,9 +636,9 @@ static int condensed_face2(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, con
                                                                                     x, nullptr, rwv, gbuf);
       c->launches++;
     }
-    constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
-    k_local_solve<D::NM, GT><<<grid_for(c, E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(
-        E, L->sinv + vm * D::NM, mode == 1 ? rwv : gbuf, mode == 1, zbuf);
+    using LS = LocalSolveCfg<D::NM>;
+    k_local_solve<D::NM, LS::NT><<<grid_for(c, (E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)),
+                                   LS::NT, 0, s>>>(E, L->sinv + vm * D::NM, mode == 1 ? rwv : gbuf, mode == 1, zbuf);
     c->launches++;
   }
   if ((stages & 2) && mode != 2) {
@@ -662,9 +662,9 @@ static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, cons
   const int nbi = (c->E + V::MBI - 1) / V::MBI, nbo = (c->E + V::MBO - 1) / V::MBO;
   k_visc_in2<P><<<grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s>>>(c->geo, c->vg, mode, L->wlin,
                                                                                  L->hhat, x, rw, rq, gbuf);
-  constexpr int GT = D::NM <= 64 ? 64 : (D::NM <= 128 ? 128 : 192);
-  k_local_solve<D::NM, GT><<<grid_for(c, c->E, occ(k_local_solve<D::NM, GT>, GT, 0)), GT, 0, s>>>(c->E, L->sinv,
-                                                                                                 gbuf, 0, zbuf);
+  using LS = LocalSolveCfg<D::NM>;
+  k_local_solve<D::NM, LS::NT><<<grid_for(c, (c->E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)),
+                                 LS::NT, 0, s>>>(c->E, L->sinv, gbuf, 0, zbuf);
   c->launches += 2;
   if (mode != 2) {
     k_visc_out2<P><<<grid_for(c, nbo, occ(k_visc_out2<P>, 128, osm)), 128, osm, s>>>(

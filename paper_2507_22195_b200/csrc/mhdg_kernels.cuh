@@ -164,14 +164,16 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
 template <int P>
 struct ResCfg {
   using D = Dims<P>;
-  static constexpr int EB = (P >= 4) ? 1 : 2;      // macros per group iteration
+  // macros per group iteration: enough quadrature points for the group's
+  // threads at low degree (P = 1: 8 volume + 16 face points per macro)
+  static constexpr int EB = (P >= 4) ? 1 : (P == 1 ? 8 : (P == 2 ? 3 : 2));
   static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per group
   static constexpr int GT = NW * 32;               // threads per group
   static constexpr int NG = (P >= 4) ? 1 : 4;      // groups per CTA
   static constexpr bool SB = P <= 3;               // basis tables in shared memory
   static constexpr int NT = NG * GT;
   static constexpr int MINB = (P >= 4) ? 2 : 1;    // resident CTAs per SM (register cap)
-  static constexpr int WPM = NW / EB;              // warps per macro
+  static constexpr int WPM = NW / EB > 0 ? NW / EB : 1;   // warps per macro in the contraction
   static constexpr int NTILE = (D::NN + 7) / 8;    // DMMA N tiles over nodes (volume test)
   static constexpr int FMT = (2 * D::NFN + 7) / 8; // face test: M tiles over phi_face + fphi rows
   static constexpr int FKS = (D::NQF + 3) / 4;     // face test: K steps over face points
@@ -441,9 +443,9 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     // ---- 2. contraction on the FP64 tensor cores, all WPM warps of a macro
     // alike: warp r takes the volume-test K range q in [r NQ/WPM, (r+1)
     // NQ/WPM) and the face tests of faces k = r, r + WPM, ...
-    {
-      const int m = gwarp / R::WPM, role = gwarp % R::WPM;
-      if (m < nm) {
+    for (int job = gwarp; job < nm * R::WPM; job += R::NW) {
+      const int m = job / R::WPM, role = job % R::WPM;
+      {
         {   // volume test: C[s][i] += sum_k G^T[s][k] B[k][i], k = (q, kk)
           const int q0 = role * NQ / R::WPM, q1 = (role + 1) * NQ / R::WPM;
           const int s_a = lane >> 2, kk = lane & 3;
@@ -1400,27 +1402,43 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
 //   k_face_out : y += A_hh x [matvec] + A_hv z, scattered to the trace with
 //                fp64 atomics (two sides per node on a zeroed output)
 // ===========================================================================
-// z_e = S_e^-1 g_e (column-major S^-1); neg: g = -gin (condensed rhs)
+// z_e = S_e^-1 g_e (column-major S^-1); neg: g = -gin (condensed rhs).
+// Thread (macro slot, row) per output; small systems (NM < NT / 2) take
+// several macros per block so every thread streams a row.
+template <int NM>
+struct LocalSolveCfg {
+  static constexpr int NT = NM <= 128 ? 128 : 192;
+  static constexpr int MB = NM <= NT / 2 ? NT / NM : 1;   // macros per block iteration
+};
+
 template <int NM, int NT>
 __global__ void __launch_bounds__(NT)
 k_local_solve(int E, const double* __restrict__ sinv, const double* __restrict__ gin, int neg,
               double* __restrict__ z) {
-  __shared__ double sg[NM];
-  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+  constexpr int MB = LocalSolveCfg<NM>::MB;
+  __shared__ double sg[MB * NM];
+  const int ml = threadIdx.x / NM, rr = threadIdx.x % NM;
+  for (int e0 = blockIdx.x * MB; e0 < E; e0 += gridDim.x * MB) {
+    const int nm = min(MB, E - e0);
     __syncthreads();
-    for (int i = threadIdx.x; i < NM; i += NT) sg[i] = neg ? -gin[(size_t)e * NM + i] : gin[(size_t)e * NM + i];
+    for (int i = threadIdx.x; i < nm * NM; i += NT) sg[i] = neg ? -gin[(size_t)e0 * NM + i] : gin[(size_t)e0 * NM + i];
     __syncthreads();
+    if constexpr (MB > 1) {
+      if (ml >= nm) continue;
+    }
+    const int e = e0 + (MB > 1 ? ml : 0);
     const double* A = sinv + (size_t)e * NM * NM;
-    for (int r = threadIdx.x; r < NM; r += NT) {
+    const double* g = sg + (MB > 1 ? ml * NM : 0);
+    for (int r = (MB > 1 ? rr : threadIdx.x); r < NM; r += (MB > 1 ? NM : NT)) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int c = 0;
       for (; c + 3 < NM; c += 4) {
-        a0 += __ldcs(A + (size_t)(c + 0) * NM + r) * sg[c + 0];
-        a1 += __ldcs(A + (size_t)(c + 1) * NM + r) * sg[c + 1];
-        a2 += __ldcs(A + (size_t)(c + 2) * NM + r) * sg[c + 2];
-        a3 += __ldcs(A + (size_t)(c + 3) * NM + r) * sg[c + 3];
+        a0 += __ldcs(A + (size_t)(c + 0) * NM + r) * g[c + 0];
+        a1 += __ldcs(A + (size_t)(c + 1) * NM + r) * g[c + 1];
+        a2 += __ldcs(A + (size_t)(c + 2) * NM + r) * g[c + 2];
+        a3 += __ldcs(A + (size_t)(c + 3) * NM + r) * g[c + 3];
       }
-      for (; c < NM; ++c) a0 += __ldcs(A + (size_t)c * NM + r) * sg[c];
+      for (; c < NM; ++c) a0 += __ldcs(A + (size_t)c * NM + r) * g[c];
       z[(size_t)e * NM + r] = (a0 + a1) + (a2 + a3);
     }
   }
