@@ -498,9 +498,27 @@ static int launch_linearize(mhdg_ctx* c, const double* w, const double* tr, doub
       c->scratch_bytes = need;
     }
   }
+  // S assembled here (row-major into sinv), inverted by the blocked
+  // tensor-core Gauss-Jordan with its working matrix in an L2-resident
+  // global slab per CTA (NM = 175 does not fit shared memory); the unblocked
+  // in-kernel Gauss-Jordan of k_linearize took ~100x longer at k = 4
+  constexpr int NM = Dims<P>::NM;
   k_linearize<P, NT><<<grid, NT, smem, s>>>(c->geo, w, tr, weight, ptc, L->sinv, L->hw, L->hhat, L->hh,
-                                            c->d_scratch, c->d_status);
-  c->launches++;
+                                            c->d_scratch, c->d_status, 0);
+  using GB = GJB<NM>;
+  const size_t gsm = GB::bytes_gm;
+  if (set_smem(k_gj_blocked<NM, true>, gsm)) return MHDG_CUDA_ERROR;
+  // two slabs per SM keep the working set (148 x 2 x 259 KB) inside L2
+  const int ggrid = grid_for(c, c->E, std::min(2, occ(k_gj_blocked<NM, true>, GB::NT, gsm)));
+  const size_t slabs = (size_t)ggrid * GB::slab * sizeof(double);
+  if (slabs > c->scratch_bytes) {
+    if (c->d_scratch) cudaFree(c->d_scratch);
+    c->d_scratch = nullptr;
+    if (cudaMalloc(&c->d_scratch, slabs) != cudaSuccess) return MHDG_OUT_OF_MEMORY;
+    c->scratch_bytes = slabs;
+  }
+  k_gj_blocked<NM, true><<<ggrid, GB::NT, gsm, s>>>(c->E, L->sinv, c->d_status, c->d_scratch);
+  c->launches += 2;
   CK(cudaGetLastError());
   return MHDG_OK;
 }
@@ -510,7 +528,7 @@ static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
                                  const int* tidx_rem, const double* area_rem, cudaStream_t s) {
   size_t smem = PreSmem<P, NT>::bytes;
   constexpr int NB = Dims<P>::NB;
-  if constexpr (NB % 2 == 0) {   // assemble, then the blocked tensor-core Gauss-Jordan
+  if constexpr (true) {   // assemble, then the blocked tensor-core Gauss-Jordan
     if (set_smem(k_precond_factor<P, NT, false>, smem)) return MHDG_CUDA_ERROR;
     int per_sm = occ(k_precond_factor<P, NT, false>, NT, smem);
     k_precond_factor<P, NT, false><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(

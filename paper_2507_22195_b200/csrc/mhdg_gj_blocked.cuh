@@ -18,6 +18,10 @@
 
 namespace mhdg {
 
+// GM = true: the padded working matrix lives in a per-CTA global scratch
+// slab (L2-resident) instead of shared memory, for orders whose matrix does
+// not fit (N = 175 at k = 4: 248 KB); U / R / pivot candidates stay in
+// shared memory.
 template <int N>
 struct GJB {
   static constexpr int NP = (N + 7) / 8 * 8;                 // padded order
@@ -28,36 +32,39 @@ struct GJB {
   static constexpr int NW = (NP + 31) / 32;                  // one panel row per thread
   static constexpr int NT = 32 * NW;
   static constexpr size_t bytes = (size_t)(NP * S + 2 * 8 * SU + 2 * NW * 10) * 8 + (size_t)(2 * N + 4) * 4;
+  static constexpr size_t bytes_gm = (size_t)(2 * 8 * SU + 2 * NW * 10) * 8 + (size_t)(2 * N + 4) * 4;
+  static constexpr size_t slab = (size_t)NP * S;   // doubles per CTA (GM)
 };
 
-template <int N>
+template <int N, bool GM = false>
 __global__ void __launch_bounds__(GJB<N>::NT, 2)
-k_gj_blocked(int nmat, double* __restrict__ mats, unsigned long long* status) {
+k_gj_blocked(int nmat, double* __restrict__ mats, unsigned long long* status, double* __restrict__ scratch = nullptr) {
   using G = GJB<N>;
   constexpr int NP = G::NP, S = G::S, SU = G::SU, T = G::T, NT = G::NT, NW = G::NW;
   extern __shared__ __align__(16) double smem[];
-  double* A = smem;                 // NP x S
-  double* U = A + NP * S;           // [8][SU]  (k-major)
+  double* A = GM ? scratch + (size_t)blockIdx.x * G::slab : smem;   // NP x S
+  double* U = GM ? smem : A + NP * S;   // [8][SU]  (k-major)
   double* R = U + 8 * SU;           // [8][SU]
   double* cand = R + 8 * SU;        // [2][NW][10]: |a|, row index, 8 row values
   int* q = (int*)(cand + 2 * NW * 10);
   int* qi = q + N;
   int* flag = qi + N;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  static_assert(N % 2 == 0, "row pairs are loaded as double2");
   const int r = tid;                // this thread's panel row
   // padding rows / columns stay zero through every update (U and R vanish there)
   for (int idx = tid; idx < NP * S; idx += NT) A[idx] = 0.0;
   for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
     double* M = mats + (size_t)m * N * N;
     __syncthreads();
-    {
+    if constexpr (N % 2 == 0) {   // row pairs as double2
       const double2* M2 = reinterpret_cast<const double2*>(M);
 #pragma unroll 8
       for (int i = tid; i < N * N / 2; i += NT) {
         const int rr = (2 * i) / N, c = (2 * i) % N;
         *reinterpret_cast<double2*>(A + rr * S + c) = __ldcs(M2 + i);
       }
+    } else {
+      for (int i = tid; i < N * N; i += NT) A[(i / N) * S + i % N] = __ldcs(M + i);
     }
     bool used = r >= N;
     bool ok = true;
@@ -157,13 +164,21 @@ k_gj_blocked(int nmat, double* __restrict__ mats, unsigned long long* status) {
     for (int k = tid; k < N; k += NT) qi[q[k]] = k;
     __syncthreads();
     int bad = !ok;
-    double2* M2 = reinterpret_cast<double2*>(M);
+    if constexpr (N % 2 == 0) {
+      double2* M2 = reinterpret_cast<double2*>(M);
 #pragma unroll 4
-    for (int i = tid; i < N * N / 2; i += NT) {
-      const int c = (2 * i) / N, rr = (2 * i) % N, qc = qi[c];
-      const double v0 = A[q[rr] * S + qc], v1 = A[q[rr + 1] * S + qc];
-      bad |= !isfinite(v0) || !isfinite(v1);
-      M2[i] = make_double2(v0, v1);
+      for (int i = tid; i < N * N / 2; i += NT) {
+        const int c = (2 * i) / N, rr = (2 * i) % N, qc = qi[c];
+        const double v0 = A[q[rr] * S + qc], v1 = A[q[rr + 1] * S + qc];
+        bad |= !isfinite(v0) || !isfinite(v1);
+        M2[i] = make_double2(v0, v1);
+      }
+    } else {
+      for (int i = tid; i < N * N; i += NT) {
+        const double v = A[q[i % N] * S + qi[i / N]];
+        bad |= !isfinite(v);
+        M[i] = v;
+      }
     }
     if (__syncthreads_or(bad) && tid == 0) report(status, 0, 0, m);
   }

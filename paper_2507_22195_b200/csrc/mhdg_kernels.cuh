@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(NT)
 k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trace, double weight,
             double ptc, double* __restrict__ sinv, double* __restrict__ hw_out,
             double* __restrict__ hhat_out, double* __restrict__ hh_out, double* __restrict__ scratch,
-            unsigned long long* status) {
+            unsigned long long* status, int do_gj = 1) {
   using D = Dims<P>;
   using L = LinSmem<P>;
   constexpr int QC = L::QC;
@@ -810,6 +810,11 @@ k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trac
     }
     __syncthreads();
 
+    if (!do_gj) {   // S row-major for a separate (blocked) inversion
+      double* out = sinv + (size_t)e * NM * NM;
+      for (int o = tid; o < NM * NM; o += NT) out[o] = S[o];
+      continue;
+    }
     // ---- S^-1 (Gauss-Jordan) and column-major store
     bool ok = gj_inverse(S, NM, NM, sPerm, sCol, sFlag);
     int bad = 0;
