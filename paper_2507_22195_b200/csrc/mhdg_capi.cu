@@ -443,6 +443,17 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 // ---------------------------------------------------------------------------
 // linearization
 // ---------------------------------------------------------------------------
+// batched in-place inverse (row-major in, column-major out): lookahead
+// Gauss-Jordan, 8 warps for the condensed blocks S (N >= 64), 4 otherwise
+template <int N>
+static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s) {
+  constexpr int NWT = N >= 64 ? 8 : 4;
+  using GL = GJLA<N, NWT>;
+  if (set_smem(k_gj_la<N, NWT>, GL::bytes)) return MHDG_CUDA_ERROR;
+  k_gj_la<N, NWT><<<grid_for(c, nmat, occ(k_gj_la<N, NWT>, GL::NT, GL::bytes)), GL::NT, GL::bytes, s>>>(
+      nmat, mats, status);
+  return MHDG_OK;
+}
 template <int P>
 static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, const double* tr, double weight,
                              double ptc, const mhdg_lin_buffers* L, cudaStream_t s) {
@@ -471,10 +482,7 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
     c->launches++;
   }
   constexpr int NM = Dims<P>::NM;
-  const size_t gsm = GJB<NM>::bytes;
-  if (set_smem(k_gj_blocked<NM>, gsm)) return MHDG_CUDA_ERROR;
-  k_gj_blocked<NM><<<grid_for(c, c->E, occ(k_gj_blocked<NM>, GJB<NM>::NT, gsm)), GJB<NM>::NT, gsm, s>>>(
-      c->E, L->sinv, c->d_status);
+  if (gj_lookahead<NM>(c, c->E, L->sinv, c->d_status, s)) return MHDG_CUDA_ERROR;
   (void)ptc;
   c->launches++;
   CK(cudaGetLastError());
@@ -533,10 +541,7 @@ static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
     int per_sm = occ(k_precond_factor<P, NT, false>, NT, smem);
     k_precond_factor<P, NT, false><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
         c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
-    using GB = GJB<NB>;
-    if (set_smem(k_gj_blocked<NB>, GB::bytes)) return MHDG_CUDA_ERROR;
-    k_gj_blocked<NB><<<grid_for(c, c->n_owned, occ(k_gj_blocked<NB>, GB::NT, GB::bytes)), GB::NT, GB::bytes, s>>>(
-        c->n_owned, L->pinv, c->d_status + 1);
+    if (gj_lookahead<NB>(c, c->n_owned, L->pinv, c->d_status + 1, s)) return MHDG_CUDA_ERROR;
     c->launches += 2;
   } else {
     if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;
@@ -1146,9 +1151,9 @@ extern "C" double mhdg_dmma_probe(int device, void* stream) {
 // experiment builds: residual phase clocks, DFMA dependent-chain latency
 extern "C" void mhdg_debug_res_clk(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_res_clk, sizeof(unsigned long long) * 9);
+  cudaMemcpyFromSymbol(out, g_res_clk, sizeof(unsigned long long) * 16);
   if (reset) {
-    unsigned long long z[9] = {0};
+    unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_res_clk, z, sizeof(z));
   }
 }
@@ -1168,7 +1173,34 @@ __global__ void k_trans_lat(int n, double* out, long long* cyc, int which) {
   out[1] = a;
   cyc[0] = t1 - t0;
 }
+__global__ void k_dmma_lat(int n, double* out, long long* cyc, int indep) {
+  double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  const double a = out[0] + 1.0, b = 0.5;
+  const long long t0 = clock64();
+  if (indep == 1) {
+    for (int i = 0; i < n; ++i) dmma_8x8x4(c[0], a, b);
+  } else {
+    for (int i = 0; i < n; i += 4) {
+      dmma_8x8x4(c[0], a, b);
+      dmma_8x8x4(c[1], a, b);
+      dmma_8x8x4(c[2], a, b);
+      dmma_8x8x4(c[3], a, b);
+    }
+  }
+  const long long t1 = clock64();
+  out[1] = c[0][0] + c[1][1] + c[2][0] + c[3][1];
+  cyc[0] = t1 - t0;
+}
 extern "C" double mhdg_debug_latency(int which) {
+  if (which >= 3) {
+    double* d; long long* cy; long long h = 0;
+    cudaMalloc(&d, 16); cudaMalloc(&cy, 8); cudaMemset(d, 0, 16);
+    const int n = 4096;
+    k_dmma_lat<<<1, 32>>>(n, d, cy, which == 3 ? 1 : 4);
+    cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d); cudaFree(cy);
+    return (double)h / n;
+  }
   double* d; long long* cy; long long h = 0;
   cudaMalloc(&d, 16); cudaMalloc(&cy, 8); cudaMemset(d, 0, 16);
   const int n = 4096;

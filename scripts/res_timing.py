@@ -22,7 +22,8 @@ fields = disc.project(vx.initial)
 stage = StageContext(alpha=alpha, offset=(-alpha * disc.volume_quad_states(fields)).contiguous())
 lib = _native.load()
 lib.mhdg_debug_latency.restype = C.c_double
-lat = {k: lib.mhdg_debug_latency(v) for k, v in (("dfma", -1), ("log", 0), ("exp", 1), ("div", 2))}
+lat = {k: lib.mhdg_debug_latency(v) for k, v in (("dfma", -1), ("log", 0), ("exp", 1), ("div", 2),
+                                                  ("dmma_dependent", 3), ("dmma_4_chains_per_op", 4))}
 buf = (C.c_ulonglong * 9)()
 for _ in range(3):
     disc.residuals(fields, stage, sync=False)
