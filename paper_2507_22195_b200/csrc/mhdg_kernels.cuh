@@ -377,7 +377,8 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       const double* geo = GEO(m);
       const double n[3] = {geo[10 + k * 3], geo[11 + k * 3], geo[12 + k * 3]};
       double fh[5];
-      numerical_flux(FK >= 0 ? FK : g.kind, u, uh, n, gam, fh);
+      numerical_flux(FK >= 0 ? FK : g.kind, u, uh, n, gam, fh, g.form == FORM_ENTROPY ? wq : nullptr,
+                     g.form == FORM_ENTROPY ? whq : nullptr);
       const double fwq = sFW[q] * geo[22 + k];
       double* h = H(m) + kq * 5;
 #pragma unroll
@@ -762,7 +763,8 @@ k_linearize(Geo g, const double* __restrict__ w, const double* __restrict__ trac
         }
         to_conservative(wd, g.form, gam, ud);
         to_conservative(whd, g.form, gam, uhd);
-        numerical_flux(g.kind, ud, uhd, n, gam, fd);
+        numerical_flux(g.kind, ud, uhd, n, gam, fd, g.form == FORM_ENTROPY ? wd : nullptr,
+                       g.form == FORM_ENTROPY ? whd : nullptr);
         const size_t base = ((size_t)e * 4 + k) * 25 * D::NQF + q;   // ten layout (E,4,25,NQF)
         if (which == 0) {
 #pragma unroll
@@ -1192,7 +1194,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         }
         to_conservative(wd, g.form, gam, ud);
         to_conservative(whd, g.form, gam, uhd);
-        numerical_flux(FK >= 0 ? FK : g.kind, ud, uhd, n, gam, fd);
+        numerical_flux(FK >= 0 ? FK : g.kind, ud, uhd, n, gam, fd, g.form == FORM_ENTROPY ? wd : nullptr,
+                       g.form == FORM_ENTROPY ? whd : nullptr);
         if (VISC) {
           double qq[5][3];
 #pragma unroll

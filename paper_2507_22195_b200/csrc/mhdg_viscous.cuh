@@ -213,7 +213,8 @@ k_residual_visc(Geo g, ViscGeo vg, const double* __restrict__ w, const double* _
       if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e);
       const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
       double fh[5], Gv[5][3];
-      numerical_flux(g.kind, u, uh, n, gam, fh);
+      numerical_flux(g.kind, u, uh, n, gam, fh, g.form == FORM_ENTROPY ? wq : nullptr,
+                     g.form == FORM_ENTROPY ? whq : nullptr);
       visc_G(vg, g.form, wq, u, qq, gam, Gv);
       const double fwq = g.fw[qp] * sGeo[22 + k];
       double* h = sH + it * 20;
