@@ -1353,19 +1353,31 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
       }
     }
     __syncthreads();
-    // symmetry statistic (the reference logs the count of non-SPD/non-symmetric blocks)
-    if (tid < 32) {
+    // symmetry statistic (the reference logs the count of non-SPD/non-symmetric
+    // blocks): max |a| and max |a - a^T| over the whole CTA
+    {
       double amax = 0.0, dmax = 0.0;
-      for (int idx = tid; idx < NB * NB; idx += 32) {
+      for (int idx = tid; idx < NB * NB; idx += NT) {
         const int r = idx / NB, c = idx % NB;
         amax = fmax(amax, fabs(A[idx]));
-        dmax = fmax(dmax, fabs(A[idx] - A[c * NB + r]));
+        if (c > r) dmax = fmax(dmax, fabs(A[idx] - A[c * NB + r]));
       }
       for (int off = 16; off > 0; off >>= 1) {
         amax = fmax(amax, __shfl_down_sync(0xffffffffu, amax, off));
         dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, off));
       }
-      if (tid == 0 && !(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
+      if ((tid & 31) == 0) {
+        sCol[tid >> 5] = amax;
+        sRow[tid >> 5] = dmax;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < NT / 32; ++w) {
+          amax = fmax(amax, sCol[w]);
+          dmax = fmax(dmax, sRow[w]);
+        }
+        if (!(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
+      }
     }
     __syncthreads();
     if (!INV) {   // inverted afterwards by k_gj_blocked<NB>
