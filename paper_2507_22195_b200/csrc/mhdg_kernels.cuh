@@ -1292,7 +1292,12 @@ template <int P, int NT>
 struct PreSmem {
   using D = Dims<P>;
   static constexpr int NB = D::NB;
-  static constexpr size_t bytes = ((size_t)NB * NB + D::NQF * 25 + D::NQF * D::NFN + 4 * (NB + 16) + D::NQF) * 8 +
+  // side block on DMMA: C[(i,j)][(s,t)] = sum_q W[(i,j)][q] hh[q][(s,t)],
+  // W[(i,j)][q] = facet_w[q] fphi[q][i] fphi[q][j] (a reference table,
+  // lane-swizzled A fragments), times the side's area
+  static constexpr int WMT = (D::NFN * D::NFN + 7) / 8, WKS = (D::NQF + 3) / 4, WNT = 4;
+  static constexpr int WA = WMT * WKS * 32;
+  static constexpr size_t bytes = ((size_t)NB * NB + D::NQF * 25 + D::NQF * D::NFN + 4 * (NB + 16) + D::NQF + WA) * 8 +
                                   ((size_t)D::NFN + 2 * NB + 2) * 4;
 };
 
@@ -1311,12 +1316,20 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
   double* sCol = sFP + D::NQF * D::NFN;  // 2*NPR
   double* sRow = sCol + 2 * (NB + 16);   // 2*NPC
   double* sFw = sRow + 2 * (NB + 16);    // NQF
-  int* sT = (int*)(sFw + D::NQF);        // NFN
+  double* sWA = sFw + D::NQF;            // WA
+  int* sT = (int*)(sWA + PreSmem<P, NT>::WA);   // NFN
   int* sQ = sT + D::NFN;                 // NB
   int* sQi = sQ + NB;                    // NB
   int* sFlag = sQi + NB;                 // 2
-  const int tid = threadIdx.x;
+  using PS = PreSmem<P, NT>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < D::NQF * D::NFN; i += NT) sFP[i] = g.fphi[i];
+  for (int i = tid; i < PS::WA; i += NT) {   // [mt][ks][lane]
+    const int ln = i % 32, ks = (i / 32) % PS::WKS, mt = i / (32 * PS::WKS);
+    const int ij = mt * 8 + (ln >> 2), q = ks * 4 + (ln & 3);
+    sWA[i] = (ij < D::NFN * D::NFN && q < D::NQF)
+                 ? (g.fw[q] * g.fphi[q * D::NFN + ij / D::NFN]) * g.fphi[q * D::NFN + ij % D::NFN] : 0.0;
+  }
   for (int f = blockIdx.x; f < n_faces; f += gridDim.x) {
     __syncthreads();
     for (int i = tid; i < NB * NB; i += NT) A[i] = 0.0;
@@ -1329,27 +1342,36 @@ k_precond_factor(Geo g, int n_faces, const double* __restrict__ hh, const double
         for (int i = tid; i < D::NQF * 25; i += NT)   // (25, NQF) per side -> [q][u]
           sHH[(i % D::NQF) * 25 + i / D::NQF] = hh[((size_t)st * D::NQF) * 25 + i];
         for (int i = tid; i < D::NFN; i += NT) sT[i] = g.tidx[((size_t)e * 4 + k) * D::NFN + i];
-        for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * g.area[(size_t)e * 4 + k];
+        if (tid == 0) sFw[0] = g.area[(size_t)e * 4 + k];
       } else {  // remote side of a halo face (partitioned runs)
         const int r = -2 - st;
         for (int i = tid; i < D::NQF * 25; i += NT)
           sHH[(i % D::NQF) * 25 + i / D::NQF] = hh_rem[(size_t)r * D::NQF * 25 + i];
         for (int i = tid; i < D::NFN; i += NT) sT[i] = tidx_rem[(size_t)r * D::NFN + i];
-        for (int i = tid; i < D::NQF; i += NT) sFw[i] = g.fw[i] * area_rem[r];
+        if (tid == 0) sFw[0] = area_rem[r];
       }
       __syncthreads();
-      for (int o = tid; o < D::NFN * D::NFN * 5; o += NT) {   // (node pair, row component)
-        const int ij = o / 5, s = o % 5;
-        const int i = ij / D::NFN, j = ij % D::NFN;
-        double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-        for (int q = 0; q < D::NQF; ++q) {
-          const double ci = sFw[q] * sFP[q * D::NFN + i], pj = sFP[q * D::NFN + j];
+      // side block on the FP64 tensor cores: every ((i,j), (s,t)) is a
+      // distinct entry of A, so the warps add their tiles without atomics
+      const double area = sFw[0];
+      for (int job = warp; job < PS::WMT * PS::WNT; job += NT / 32) {
+        const int mt = job / PS::WNT, nt = job % PS::WNT;
+        double c[2] = {0.0, 0.0};
 #pragma unroll
-          for (int t = 0; t < 5; ++t) acc[t] += (ci * sHH[q * 25 + s * 5 + t]) * pj;
+        for (int ks = 0; ks < PS::WKS; ++ks) {
+          const int q = ks * 4 + (lane & 3), n = nt * 8 + (lane >> 2);
+          const double b = (q < D::NQF && n < 25) ? sHH[q * 25 + n] : 0.0;
+          dmma_8x8x4(c, sWA[(mt * PS::WKS + ks) * 32 + lane], b);
         }
+        const int ij = mt * 8 + (lane >> 2);
+        if (ij < D::NFN * D::NFN) {
+          const int i = ij / D::NFN, j = ij % D::NFN;
 #pragma unroll
-        for (int t = 0; t < 5; ++t) A[(sT[i] * 5 + s) * NB + sT[j] * 5 + t] += acc[t];
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int st2 = nt * 8 + (lane & 3) * 2 + h2;
+            if (st2 < 25) A[(sT[i] * 5 + st2 / 5) * NB + sT[j] * 5 + st2 % 5] += area * c[h2];
+          }
+        }
       }
     }
     __syncthreads();
