@@ -269,6 +269,7 @@ k_gj_la(int nmat, double* __restrict__ mats, unsigned long long* status) {
         }
         if (p >= N) { ok = false; p = 0; }
         pt[t] = p;
+        if (lane == 0) q[k0 + t] = p;
         const int owner = p & 31, slot = p >> 5;
         double prow[8];
 #pragma unroll
@@ -310,7 +311,8 @@ k_gj_la(int nmat, double* __restrict__ mats, unsigned long long* status) {
         }
       }
     }
-    if (lane < 8) q[k0 + lane] = pt[lane];   // pt[] is warp-uniform
+    if (lane == 0)
+      for (int t = nbp; t < 8; ++t) q[k0 + t] = -1;
   };
 
   // A[:, tile ct] += U R on all row tiles; R fragments in registers
@@ -357,19 +359,21 @@ k_gj_la(int nmat, double* __restrict__ mats, unsigned long long* status) {
     __syncthreads();
     unsigned used = 0u;   // warp 0: rows already chosen as pivots (bit i: row lane + 32 i)
     bool ok = true;
-    if (warp == 0) factor_panel(0, used, ok);
-    __syncthreads();
 #ifdef MHDG_RES_TIMING
     long long tg = clock64();
 #define GJT(k) do { const long long t_ = clock64(); if (lane == 0 && (warp == 0 || warp == 1)) atomicAdd(&g_res_clk[k], (unsigned long long)(t_ - tg)); tg = t_; } while (0)
 #else
 #define GJT(k) do { } while (0)
 #endif
-    for (int pan = 0; pan < NPAN; ++pan) {
+    // pan = -1: warp 0 factors panel 0 alone (one inlined copy of the panel
+    // factorization serves every panel)
+    for (int pan = -1; pan < NPAN; ++pan) {
       const double* U = Ub + (pan & 1) * L::UF;
       const int k0 = pan * 8, nxt = pan + 1;
       GJT(warp == 0 ? 9 : 13);
-      if (warp == 0) {
+      if (pan < 0) {
+        if (warp == 0) factor_panel(0, used, ok);
+      } else if (warp == 0) {
         if (nxt < NPAN) {
           // R_p on panel p+1's columns, update them, factor panel p+1
           const int c = nxt * 8 + nr;
