@@ -169,3 +169,47 @@ def test_integrals_vs_oracle(cuda_ok):
     want = OracleHDG(disc.tables, flux="es").integrals(z["w"])
     for k in want:
         assert abs(got[k] - want[k]) <= 1e-12 * max(1.0, abs(want[k])), k
+
+
+def test_entropy_state_error(cuda_ok):
+    """v5 >= 0 in the entropy formulation -> NonAdmissibleEntropyState (a
+    NonAdmissibleState) located in the volume, as the reference's
+    from_entropy raises it (gas.py:163-168)."""
+    from paper_2507_22195_b200 import Discretization, DissipationSpec, GasModel
+    from paper_2507_22195_b200.errors import NonAdmissibleEntropyState, NonAdmissibleState
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    gas = GasModel(1.4)
+    mesh = build_box_macro_mesh(np.array([[0.0, 1.0]] * 3), 1, 1)
+    u0 = gas.conservative(1.0, np.array([0.3, -0.2, 0.1]), 0.7)
+    disc = Discretization(mesh, p=2, gas=gas, formulation="entropy",
+                          flux=DissipationSpec("es"), device="cuda:0")
+    f = disc.project(lambda x: np.broadcast_to(u0, x.shape[:-1] + (5,)).copy())
+    w = f.w.cpu().numpy() if hasattr(f.w, "cpu") else np.array(f.w)
+    w[2, :, 4] = 0.5   # every volume point of macro 2: the volume pass fails first
+    f.w = w
+    with pytest.raises(NonAdmissibleEntropyState) as exc:
+        disc.residuals(f)
+    assert isinstance(exc.value, NonAdmissibleState)
+    assert "volume" in str(exc.value) and "macro 2" in str(exc.value)
+
+
+def test_singular_local_matrix_names_the_macro(cuda_ok):
+    """A non-finite state in one macro makes its condensed block singular:
+    SingularLocalMatrix(macro=e) for that macro (assembly.py:718-733)."""
+    from paper_2507_22195_b200 import Discretization, DissipationSpec, GasModel, StageContext
+    from paper_2507_22195_b200.errors import SingularLocalMatrix
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    gas = GasModel(1.4)
+    mesh = build_box_macro_mesh(np.array([[0.0, 1.0]] * 3), 2, 1)
+    u0 = gas.conservative(1.0, np.array([0.3, -0.2, 0.1]), 0.7)
+    disc = Discretization(mesh, p=3, gas=gas, formulation="entropy",
+                          flux=DissipationSpec("es"), device="cuda:0")
+    f = disc.project(lambda x: np.broadcast_to(u0, x.shape[:-1] + (5,)).copy())
+    w = f.w.cpu().numpy() if hasattr(f.w, "cpu") else np.array(f.w)
+    w[5, :, 0] = np.nan
+    f.w = w
+    with pytest.raises(SingularLocalMatrix) as exc:
+        disc.jacobian(f, StageContext(alpha=10.0, offset=None), ptc_weight=1.0)
+    assert exc.value.macro == 5
