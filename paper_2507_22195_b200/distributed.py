@@ -43,6 +43,15 @@ class PartitionedDiscretization:
     def _dev(self, a):
         return self.local._dev(a)
 
+    @property
+    def viscosity(self):
+        return self.local.viscosity
+
+    def solve_gradient(self, fields):
+        """Gradient unknowns of the local macros (the solve is macro-local
+        once the ghost traces are current)."""
+        return self.local.solve_gradient(self._fields(fields))
+
     def _fields(self, fields):
         """Device fields with ghost traces refreshed from their owners (the
         ghost rows are a cache of the owner's values; updates computed by

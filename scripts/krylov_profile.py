@@ -61,6 +61,7 @@ def timeit(fn, reps=20):
     return e0.elapsed_time(e1) / reps, (time.perf_counter() - t0) / reps * 1e3
 
 
+out["residual_ms"] = timeit(lambda: disc.residuals(f, stage, sync=False))
 out["matvec_ms"] = timeit(lambda: lin.matvec(x))
 out["precond_ms"] = timeit(lambda: lin.apply_preconditioner(x))
 V = torch.randn((61, x.numel()), dtype=torch.float64, device="cuda:0")
