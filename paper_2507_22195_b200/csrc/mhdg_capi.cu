@@ -228,6 +228,28 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
     c->vg.pmt = upload(c, pmt.data(), pmt.size(), err);
     c->vg.cxt = upload(c, cxt.data(), cxt.size(), err);
     c->vg.dzt = upload(c, dzt.data(), dzt.size(), err);
+    {   // fragment-ordered face-point slices (k_visc_out2 on DMMA)
+      const int NPF = 4 * NQF, MT = (NPF + 7) / 8, KX = (NFN + 3) / 4, KZ = (NN + 3) / 4;
+      std::vector<double> cxf((size_t)4 * MT * KX * 32, 0.0), dzf((size_t)3 * MT * KZ * 32, 0.0);
+      for (int k = 0; k < 4; ++k)
+        for (int mt = 0; mt < MT; ++mt)
+          for (int ks = 0; ks < KX; ++ks)
+            for (int ln = 0; ln < 32; ++ln) {
+              const int it = mt * 8 + ln / 4, jj = ks * 4 + ln % 4;
+              if (it < NPF && jj < NFN)
+                cxf[(((size_t)k * MT + mt) * KX + ks) * 32 + ln] = cxt[((size_t)k * NFN + jj) * NPT + NQ + it];
+            }
+      for (int k2 = 0; k2 < 3; ++k2)
+        for (int mt = 0; mt < MT; ++mt)
+          for (int ks = 0; ks < KZ; ++ks)
+            for (int ln = 0; ln < 32; ++ln) {
+              const int it = mt * 8 + ln / 4, i = ks * 4 + ln % 4;
+              if (it < NPF && i < NN)
+                dzf[(((size_t)k2 * MT + mt) * KZ + ks) * 32 + ln] = dzt[((size_t)k2 * NN + i) * NPT + NQ + it];
+            }
+      c->vg.cxf = upload(c, cxf.data(), cxf.size(), err);
+      c->vg.dzf = upload(c, dzf.data(), dzf.size(), err);
+    }
     c->vg.tpp = upload(c, tpp.data(), tpp.size(), err);
   }
   c->d_status = (unsigned long long*)dalloc(c, sizeof(unsigned long long) * 4, err);

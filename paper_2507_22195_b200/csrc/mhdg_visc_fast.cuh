@@ -39,7 +39,7 @@ struct VFast {
     int fid[4], tid[4 * NFN];
   };
   struct Out {
-    double W[NN * 5], Z[NM], X[4 * NFN * 5], RQ[NN * 15], Gf[NPF * 5], geo[26];
+    double W[NN * 5], Z[NM], X[4 * NFN * 5], RQ[NN * 15], Gf[NPF * 5], YQ[NPF * 15], geo[26];
     int fid[4], tid[4 * NFN];
   };
 };
@@ -282,6 +282,68 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
         S.X[i] = x[((size_t)S.fid[k] * NFN + S.tid[k * NFN + j]) * 5 + s2];
       }
     __syncthreads();
+    if (mode == 0) {
+      // gradient unknowns at the face points on the FP64 tensor cores, per
+      // (macro slot, 8-point tile):
+      //   yq = (1/det) sum_k (area n)_k (CX_k x_k) + sum_k2 Jinv[k2] (DZ_k2 z)
+      // (the point-per-thread contraction spent one shared-memory load per
+      // FMA on the broadcast x / z values)
+      constexpr int MT = (NPF + 7) / 8, KX = (NFN + 3) / 4, KZ = (NN + 3) / 4;
+      const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, nn = lane >> 2;
+      for (int job = warp; job < MB * MT; job += V::NT / 32) {
+        const int sl = job / MT, mt = job % MT;
+        if (blk * MB + sl >= g.E) continue;
+        typename V::Out& Sx = sm[sl];
+        double acc[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double c[2] = {0.0, 0.0};
+#pragma unroll
+          for (int ks = 0; ks < KX; ++ks) {
+            const int jj = ks * 4 + kq;
+            const double b = (jj < NFN && nn < 5) ? Sx.X[(k * NFN + jj) * 5 + nn] : 0.0;
+            dmma_8x8x4(c, __ldg(vg.cxf + ((k * MT + mt) * KX + ks) * 32 + lane), b);
+          }
+          const double a = Sx.geo[22 + k];
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const double an = a * Sx.geo[10 + k * 3 + b];
+            acc[0][b] += an * c[0];
+            acc[1][b] += an * c[1];
+          }
+        }
+        const double idet = 1.0 / Sx.geo[0];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) acc[h2][b] *= idet;
+#pragma unroll
+        for (int k2 = 0; k2 < 3; ++k2) {
+          double c[2] = {0.0, 0.0};
+#pragma unroll
+          for (int ks = 0; ks < KZ; ++ks) {
+            const int i = ks * 4 + kq;
+            const double b = (i < NN && nn < 5) ? Sx.Z[i * 5 + nn] : 0.0;
+            dmma_8x8x4(c, __ldg(vg.dzf + ((k2 * MT + mt) * KZ + ks) * 32 + lane), b);
+          }
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const double jb = Sx.geo[1 + k2 * 3 + b];
+            acc[0][b] += jb * c[0];
+            acc[1][b] += jb * c[1];
+          }
+        }
+        const int pt2 = mt * 8 + nn;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int t = kq * 2 + h2;
+          if (t < 5 && pt2 < NPF)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) Sx.YQ[pt2 * 15 + t * 3 + b] = acc[h2][b];
+        }
+      }
+      __syncthreads();
+    }
     if (live) {
       const int it = lt, k = it / NQF, qp = it % NQF, pt = NQ + it;
       double wq[5] = {0, 0, 0, 0, 0}, zq[5] = {0, 0, 0, 0, 0}, xq[5] = {0, 0, 0, 0, 0}, yq[5][3];
@@ -302,14 +364,20 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
           for (int t = 0; t < 5; ++t) xq[t] += b2 * S.X[(k * NFN + j) * 5 + t];
         }
       }
-      if (mode == 0) vf_add_x<P>(vg, pt, S.X, S.geo, yq);
-      if (mode == 1) vf_add_rq<P>(vg, pt, S.RQ, yq);
-      const double idet = 1.0 / S.geo[0];
+      if (mode == 0) {
 #pragma unroll
-      for (int t = 0; t < 5; ++t)
+        for (int t = 0; t < 5; ++t)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) yq[t][b] *= idet;
-      vf_add_z<P>(vg, pt, S.Z, S.geo, yq);
+          for (int b = 0; b < 3; ++b) yq[t][b] = S.YQ[it * 15 + t * 3 + b];
+      } else {
+        if (mode == 1) vf_add_rq<P>(vg, pt, S.RQ, yq);
+        const double idet = 1.0 / S.geo[0];
+#pragma unroll
+        for (int t = 0; t < 5; ++t)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) yq[t][b] *= idet;
+        vf_add_z<P>(vg, pt, S.Z, S.geo, yq);
+      }
       double u[5], Gv[5][3];
       to_conservative(wq, g.form, gam, u);
       visc_G(vg, g.form, wq, u, yq, gam, Gv);

@@ -21,6 +21,11 @@ struct ViscGeo {
   const double* dzt;               // (3, NN, NPT)   (phi_pt Mref^-1 Kref_k)^T
   const double* tpp;               // (3, NPT, NN)   phi_pt Pref_k
   const double* tst;               // (NKP, NTI*8)   test rows: dphi_kk at (q,kk), then phi_pt at face pts
+  // face-point slices of cxt / dzt as lane-swizzled DMMA A fragments:
+  // cxf [k][mt][ks][lane] = cxt[k][jj = 4 ks + lane % 4][NQ + 8 mt + lane / 4]
+  // dzf [k2][mt][ks][lane] = dzt[k2][i = 4 ks + lane % 4][NQ + 8 mt + lane / 4]
+  const double* cxf;
+  const double* dzf;
 };
 
 // velocity / temperature gradients from the working variables (gas.py:229-262)
