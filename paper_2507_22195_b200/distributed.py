@@ -243,6 +243,11 @@ class DistVectors:
         t = pdisc.local.tables
         self.n_owned = pdisc.part.n_owned * t.fphi.shape[1] * 5
         self.h = self.torch.zeros(256, dtype=self.torch.float64, device=pdisc.device)
+        import torch.distributed as dist
+
+        part = pdisc.part
+        self.single = (getattr(part, "world", 1) == 1 and part.n_owned == part.n_local_faces
+                       and not (dist.is_initialized() and dist.get_world_size() > 1))
 
     def _dot_dev(self, x, y, out):
         self.inner.dot_into(x[: self.n_owned], y[: self.n_owned], out)
@@ -262,6 +267,8 @@ class DistVectors:
         self.inner.combine(Z, k, y, x)
 
     def mgs(self, V, j, w):
+        if self.single:   # one rank, no ghost rows: the fused single-device MGS
+            return self.inner.mgs(V, j, w)
         h = self.h
         for i in range(j + 1):
             self._dot_dev(V[i], w, h[i:i + 1])
