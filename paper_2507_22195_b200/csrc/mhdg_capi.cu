@@ -249,6 +249,15 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
             }
       c->vg.cxf = upload(c, cxf.data(), cxf.size(), err);
       c->vg.dzf = upload(c, dzf.data(), dzf.size(), err);
+      const int TM = (NFN + 7) / 8, TK = (NQF + 3) / 4;
+      std::vector<double> fpf((size_t)TM * TK * 32, 0.0);
+      for (int mt = 0; mt < TM; ++mt)
+        for (int ks = 0; ks < TK; ++ks)
+          for (int ln = 0; ln < 32; ++ln) {
+            const int q = ks * 4 + ln % 4, j = mt * 8 + ln / 4;
+            if (q < NQF && j < NFN) fpf[((size_t)mt * TK + ks) * 32 + ln] = t->fphi[(size_t)q * NFN + j];
+          }
+      c->vg.fpf = upload(c, fpf.data(), fpf.size(), err);
     }
     c->vg.tpp = upload(c, tpp.data(), tpp.size(), err);
   }

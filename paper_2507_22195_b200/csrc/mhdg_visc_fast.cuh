@@ -397,14 +397,35 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
       }
     }
     __syncthreads();
-    if (live)
-      for (int o = lt; o < 4 * NFN * 5; o += NPF) {
-        const int k = o / (NFN * 5), j = (o / 5) % NFN, s2 = o % 5;
-        double acc = 0.0;
+    // trace tests on DMMA, per (macro slot, face): C[j][s] = sum_qp fphi[qp][j] Gf[qp][s]
+    // (A fragments of fphi from the fragment-ordered table vg.fpf)
+    {
+      constexpr int TM = (NFN + 7) / 8, TK = (NQF + 3) / 4;
+      const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, nn = lane >> 2;
+      for (int job = warp; job < MB * 4; job += V::NT / 32) {
+        const int sl = job / 4, k = job % 4;
+        if (blk * MB + sl >= g.E) continue;
+        const typename V::Out& Sx = sm[sl];
+        double c[TM][2];
 #pragma unroll
-        for (int qp = 0; qp < NQF; ++qp) acc += __ldg(g.fphi + qp * NFN + j) * S.Gf[(k * NQF + qp) * 5 + s2];
-        atomicAdd(&y[((size_t)S.fid[k] * NFN + S.tid[k * NFN + j]) * 5 + s2], acc);
+        for (int t = 0; t < TM; ++t) c[t][0] = c[t][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < TK; ++ks) {
+          const int qp = ks * 4 + kq;
+          const double b = (qp < NQF && nn < 5) ? Sx.Gf[(k * NQF + qp) * 5 + nn] : 0.0;
+#pragma unroll
+          for (int t = 0; t < TM; ++t) dmma_8x8x4(c[t], __ldg(vg.fpf + (t * TK + ks) * 32 + lane), b);
+        }
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int j = t * 8 + nn, s2 = kq * 2 + h2;
+            if (j < NFN && s2 < 5)
+              atomicAdd(&y[((size_t)Sx.fid[k] * NFN + Sx.tid[k * NFN + j]) * 5 + s2], c[t][h2]);
+          }
       }
+    }
   }
 }
 

@@ -26,6 +26,7 @@ struct ViscGeo {
   // dzf [k2][mt][ks][lane] = dzt[k2][i = 4 ks + lane % 4][NQ + 8 mt + lane / 4]
   const double* cxf;
   const double* dzf;
+  const double* fpf;               // fphi as A fragments [mt][ks][lane] = fphi[q = 4 ks + lane % 4][j = 8 mt + lane / 4]
 };
 
 // velocity / temperature gradients from the working variables (gas.py:229-262)
