@@ -26,20 +26,29 @@ from paper_2507_22195_b200.time_march import DIRKIntegrator  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=16)
 ap.add_argument("--p", type=int, default=3)
+ap.add_argument("--case", default="vortex")
+ap.add_argument("--dt", type=float, default=0.01)
 a = ap.parse_args()
 gas = GasModel(1.4)
-case = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, center=(5.0, 5.0), gas=gas)
-mesh = build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), a.n, 1)
-disc = Discretization(mesh, p=a.p, gas=gas, flux=DissipationSpec("es"), device="cuda:0")
+if a.case == "vortex":
+    case = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, center=(5.0, 5.0), gas=gas)
+    mesh = build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), a.n, 1)
+    flux = "es"
+else:
+    from paper_2507_22195_b200.cases import TaylorGreen
+    case = TaylorGreen(mach=0.1, gas=gas)
+    mesh = build_box_macro_mesh(case.box, a.n, 1)
+    flux = "kepes"
+disc = Discretization(mesh, p=a.p, gas=gas, flux=DissipationSpec(flux), device="cuda:0")
 fields0 = disc.project(case.initial)
 
 # unsynchronised reference timing (second step of a warm run)
 integ = DIRKIntegrator(disc)
-f1, _ = integ.run(fields0, t_final=0.01, dt=0.01)
+f1, _ = integ.run(fields0, t_final=a.dt, dt=a.dt)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 integ2 = DIRKIntegrator(disc)
-integ2.run(fields0, t_final=0.01, dt=0.01)
+integ2.run(fields0, t_final=a.dt, dt=a.dt)
 torch.cuda.synchronize()
 wall = time.perf_counter() - t0
 
@@ -69,7 +78,7 @@ for name in ("mgs", "norm", "combine", "div_into", "axpby"):
 torch.cuda.synchronize()
 t0 = time.perf_counter()
 integ3 = DIRKIntegrator(disc)
-integ3.run(fields0, t_final=0.01, dt=0.01)
+integ3.run(fields0, t_final=a.dt, dt=a.dt)
 torch.cuda.synchronize()
 wall_sync = time.perf_counter() - t0
 out = {"wall_s": wall, "wall_synced_s": wall_sync,
