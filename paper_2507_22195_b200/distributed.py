@@ -72,6 +72,8 @@ class PartitionedDiscretization:
         nt = self.part.n_owned * res.r_trace.shape[1] * res.r_trace.shape[2]
         rt = res.r_trace.reshape(-1)[:nt]
         local = self.local.vdot(res.r_w, res.r_w) + self.local.vdot(rt, rt)
+        if res.r_q is not None:   # viscous: gradient-equation residual of the local macros
+            local += self.local.vdot(res.r_q, res.r_q)
         return math.sqrt(self.allreduce([local])[0])
 
     # -- operators -----------------------------------------------------------
@@ -88,7 +90,7 @@ class PartitionedDiscretization:
         if not self.overlap:
             res = self.local.residuals(self._fields(fields), stage, check, sync=sync)
             self.exchange.reduce_partials(res.r_trace)
-            return ResidualSet(res.r_w, res.r_trace, None, _disc=self)
+            return ResidualSet(res.r_w, res.r_trace, res.r_q, _disc=self)
         # ghost traces in flight while the interior macros run; halo macros
         # after them; then the ghost-face partial sums go to their owners
         torch = __import__("torch")
@@ -197,7 +199,9 @@ class PartitionedLinearizedSystem:
     def condensed_rhs(self, res):
         torch = __import__("torch")
         zero = torch.zeros(self.trace_shape, dtype=torch.float64, device=self.disc.device)
-        part = self.lin.condensed_rhs(ResidualSet(res.r_w, zero))     # = -(local A_hv z)
+        # macro contributions only (zero trace residual): -(local A_hv z) and,
+        # viscous, the r_q terms of the level-1 condensation
+        part = self.lin.condensed_rhs(ResidualSet(res.r_w, zero, res.r_q))
         self.pdisc.exchange.reduce_partials(part)
         return (-self.disc._dev(res.r_trace)) + part
 

@@ -1,10 +1,12 @@
 """Partitioned operator with real processes: two ranks (torch.distributed,
 gloo backend, halo staged through host memory) share one GPU, each running
 PartitionedDiscretization / PartitionedLinearizedSystem on its macro range.
-Owned rows of the residual, condensed matvec and face-block preconditioner
-must equal the single-device results bit for bit, and the distributed
-FGMRES (DistVectors, all-reduced dots) must reproduce the single-device
-iteration count and solution.  The x-slab split leaves one rank owning no
+Owned rows of the residual (and, viscous, the gradient unknowns and r_q),
+condensed matvec, condensed rhs and face-block preconditioner must equal
+the single-device results bit for bit, and the distributed FGMRES
+(DistVectors, all-reduced dots) must reproduce the single-device iteration
+count, solution and recovered local update.  Inviscid ES and viscous KEPES
+(config-4 parameters).  The x-slab split leaves one rank owning no
 halo face, which exercises the asymmetric exchanges."""
 
 import os
@@ -24,8 +26,8 @@ def _free_port():
     return port
 
 
-def _problem():
-    from paper_2507_22195_b200 import DissipationSpec, GasModel
+def _problem(visc=False):
+    from paper_2507_22195_b200 import DissipationSpec, GasModel, ViscousParams
     from paper_2507_22195_b200.mesh import build_box_macro_mesh
     from paper_2507_22195_b200.tables import HDGTables
 
@@ -42,10 +44,12 @@ def _problem():
 
     w, tr = st(E * nc).reshape(E, nc, 5), st(F * nt).reshape(F, nt, 5)
     x = rng.standard_normal(tr.shape)
-    return gas, mesh, t, DissipationSpec("es"), w, tr, x
+    if visc:   # config-4 viscous parameters (Re 1600 / M 0.1 -> 16000, Pr 0.71), KEPES
+        return gas, mesh, t, DissipationSpec("kepes"), w, tr, x, ViscousParams(16000.0, 0.1, 0.71, 1.0)
+    return gas, mesh, t, DissipationSpec("es"), w, tr, x, None
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, visc=False):
     import torch
     import torch.distributed as dist
 
@@ -58,14 +62,16 @@ def _worker(rank, world, port, out_dir):
         from paper_2507_22195_b200.solver import solve_condensed
 
         torch.cuda.set_device(0)
-        gas, mesh, t, spec, w, tr, x = _problem()
+        gas, mesh, t, spec, w, tr, x, vp = _problem(visc)
         pd = PartitionedDiscretization(mesh, 3, rank, world, device="cuda:0", full_tables=t,
-                                       gas=gas, flux=spec)
+                                       gas=gas, flux=spec, viscosity=vp)
         part = pd.part
         lo, hi = part.macro_lo, part.macro_hi
         wl, trl = part.local_fields(w, tr)
         alpha = 120.0
         fl = FieldSet(torch.from_numpy(wl.copy()).cuda(), torch.from_numpy(trl.copy()).cuda())
+        if visc:
+            fl.q = pd.solve_gradient(fl)
         off = -alpha * pd.volume_quad_states(fl)
         stage = StageContext(alpha, off)
         res = pd.residuals(fl, stage)
@@ -73,20 +79,26 @@ def _worker(rank, world, port, out_dir):
         xl = torch.from_numpy(x[part.global_faces].copy()).cuda()
         y = lin.matvec(xl)
         z = lin.apply_preconditioner(xl)
+        b = lin.condensed_rhs(res)
         d_trace, stats = solve_condensed(lin, res, rel_tol=1e-8, restart=20, max_outer=80)
+        dw, dq = lin.recover(res, d_trace)
         own = part.n_owned
+        extra = {}
+        if visc:
+            extra = dict(r_q=res.r_q.cpu().numpy(), q=fl.q.cpu().numpy(), dq=dq.cpu().numpy())
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), lo=lo, hi=hi,
                  faces=part.global_faces[:own], r_w=res.r_w.cpu().numpy(),
                  r_t=res.r_trace[:own].cpu().numpy(), y=y[:own].cpu().numpy(),
-                 z=z[:own].cpu().numpy(), d=d_trace[:own].cpu().numpy(),
-                 its=stats.outer_iterations, inner=stats.inner_iterations,
-                 n_remote=part.n_remote_sides)
+                 z=z[:own].cpu().numpy(), b=b[:own].cpu().numpy(), d=d_trace[:own].cpu().numpy(),
+                 dw=dw.cpu().numpy(), its=stats.outer_iterations, inner=stats.inner_iterations,
+                 n_remote=part.n_remote_sides, **extra)
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.timeout(900)
-def test_two_processes_share_one_gpu(cuda_ok, tmp_path):
+@pytest.mark.parametrize("visc", [False, True], ids=["inviscid_es", "viscous_kepes"])
+def test_two_processes_share_one_gpu(cuda_ok, tmp_path, visc):
     import torch
     import torch.multiprocessing as mp
 
@@ -95,12 +107,14 @@ def test_two_processes_share_one_gpu(cuda_ok, tmp_path):
     from paper_2507_22195_b200.solver import solve_condensed
 
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), visc), nprocs=world,
                        join=True, start_method="spawn")
-    gas, mesh, t, spec, w, tr, x = _problem()
-    full = Discretization(mesh, p=3, gas=gas, flux=spec, device="cuda:0", tables=t)
+    gas, mesh, t, spec, w, tr, x, vp = _problem(visc)
+    full = Discretization(mesh, p=3, gas=gas, flux=spec, device="cuda:0", tables=t, viscosity=vp)
     alpha = 120.0
     f = FieldSet(torch.from_numpy(w).cuda(), torch.from_numpy(tr).cuda())
+    if visc:
+        f.q = full.solve_gradient(f)
     off = -alpha * full.volume_quad_states(f)
     stage = StageContext(alpha, off)
     ref = full.residuals(f, stage)
@@ -108,7 +122,9 @@ def test_two_processes_share_one_gpu(cuda_ok, tmp_path):
     xd = torch.from_numpy(x).cuda()
     y_ref = lin.matvec(xd).cpu().numpy()
     z_ref = lin.apply_preconditioner(xd).cpu().numpy()
+    b_ref = lin.condensed_rhs(ref).cpu().numpy()
     d_ref, st_ref = solve_condensed(lin, ref, rel_tol=1e-8, restart=20, max_outer=80)
+    dw_ref, dq_ref = lin.recover(ref, d_ref)
     d_ref = d_ref.cpu().numpy()
     rw_ref, rt_ref = ref.r_w.cpu().numpy(), ref.r_trace.cpu().numpy()
     n_remote = []
@@ -120,8 +136,17 @@ def test_two_processes_share_one_gpu(cuda_ok, tmp_path):
         assert np.array_equal(o["r_t"], rt_ref[faces])
         assert np.array_equal(o["y"], y_ref[faces])
         assert np.array_equal(o["z"], z_ref[faces])
+        assert np.array_equal(o["b"], b_ref[faces])
+        if visc:
+            assert np.array_equal(o["q"], f.q.cpu().numpy()[lo:hi])
+            assert np.array_equal(o["r_q"], ref.r_q.cpu().numpy()[lo:hi])
         assert int(o["its"]) == st_ref.outer_iterations
         assert int(o["inner"]) == st_ref.inner_iterations
         err = np.abs(o["d"] - d_ref[faces]).max() / np.abs(d_ref).max()
         assert err <= 1e-10, err
+        dw = dw_ref.cpu().numpy()[lo:hi]
+        assert np.abs(o["dw"] - dw).max() <= 1e-9 * np.abs(dw).max()
+        if visc:
+            dq = dq_ref.cpu().numpy()[lo:hi]
+            assert np.abs(o["dq"] - dq).max() <= 1e-9 * np.abs(dq).max()
     assert min(n_remote) == 0
