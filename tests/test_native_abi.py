@@ -56,3 +56,30 @@ def test_product_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*", "", src).replace('"""', "") or \
                     "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_unsupported_configurations_raise_invalid_config():
+    """Configurations off the B200 path are rejected at construction with the
+    reference's InvalidConfig (errors.py:4), before any device work: m > 1,
+    p outside 1..4, non-default quadrature, SUPG, unknown formulation, 2D."""
+    import numpy as np
+
+    from paper_2507_22195_b200 import Discretization, DissipationSpec, GasModel
+    from paper_2507_22195_b200.errors import InvalidConfig
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    gas, es = GasModel(1.4), DissipationSpec("es")
+    box3 = np.array([[0.0, 1.0]] * 3)
+    m1 = build_box_macro_mesh(box3, 1, 1)
+    cases = [
+        (build_box_macro_mesh(box3, 1, 2), dict(p=2)),
+        (m1, dict(p=5)),
+        (m1, dict(p=0)),
+        (m1, dict(p=2, quad_degree=4)),
+        (m1, dict(p=2, supg=True)),
+        (m1, dict(p=2, formulation="primitive")),
+        (build_box_macro_mesh(np.array([[0.0, 1.0]] * 2), 2, 1), dict(p=2)),
+    ]
+    for mesh, kw in cases:
+        with pytest.raises(InvalidConfig):
+            Discretization(mesh, gas=gas, flux=es, **kw)
