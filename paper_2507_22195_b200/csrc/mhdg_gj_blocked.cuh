@@ -430,3 +430,239 @@ k_gj_la(int nmat, double* __restrict__ mats, unsigned long long* status) {
 }
 
 }  // namespace mhdg
+
+namespace mhdg {
+
+// ===========================================================================
+// Lookahead Gauss-Jordan with NPW panel warps: the panel rows are split over
+// NPW warps (rows 32 (pw + NPW i) + lane), so each pivot step handles
+// RPL = NP / (32 NPW) rows per lane; the warps' argmax candidates and the
+// pivot row meet in shared memory behind a named barrier of the panel
+// warps.  A pivot step's dependent chain shortens with the rows per lane
+// (measured ~1100 cycles at 4 rows / lane, ~480 at 2).
+// ===========================================================================
+template <int N, int NWT, int NPW>
+struct GJLA2 {
+  using G = GJB<N>;
+  static constexpr int NP = G::NP, S = G::S, T = G::T, NPAN = G::NPAN;
+  static constexpr int RPL = (NP + 32 * NPW - 1) / (32 * NPW);
+  static constexpr int NT = 32 * NWT;
+  static constexpr int UF = T * 2 * 32;
+  static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 8 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
+};
+
+template <int N, int NWT, int NPW>
+__global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, 2)
+k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
+  using L = GJLA2<N, NWT, NPW>;
+  constexpr int NP = L::NP, S = L::S, T = L::T, NPAN = L::NPAN, RPL = L::RPL, NT = L::NT;
+  extern __shared__ __align__(16) double smem[];
+  double* A = smem;                        // NP x S
+  double* Ub = A + NP * S;                 // 2 x UF
+  double* sProw = Ub + 2 * L::UF;          // 8: pivot row of the current step
+  unsigned* sCand = reinterpret_cast<unsigned*>(sProw + 8);   // [NPW][3]: hi, lo, row
+  int* q = (int*)(sCand + 4 * NPW);        // NP: pivot row of step k
+  int* qi = q + NP;
+  int* flag = qi + NP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kq = lane & 3, nr = lane >> 2;
+  const bool panel = warp < NPW;
+  const int pw = warp;
+  auto psync = [&]() {
+    if (NPW > 1) asm volatile("bar.sync 1, %0;" ::"r"(32 * NPW) : "memory");
+    else __syncwarp();
+  };
+  for (int idx = tid; idx < NP * S; idx += NT) A[idx] = 0.0;
+
+  auto row_of = [&](int i) { return 32 * (pw + NPW * i) + lane; };
+  auto factor_panel = [&](int pan, unsigned& used, bool& ok) {
+    const int k0 = pan * 8, nbp = min(8, N - k0);
+    double a[RPL][8];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = row_of(i);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[i][j] = r < NP ? A[r * S + k0 + j] : 0.0;
+    }
+    int pt[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      pt[t] = -1;
+      if (t < nbp) {
+        unsigned bhi = 0u, blo = 0u;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = row_of(i);
+          const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(a[i][t]));
+          const bool cand = r < N && !((used >> i) & 1u);
+          const unsigned hi = cand ? (unsigned)(bits >> 32) + 1u : 0u, lo = cand ? (unsigned)bits : 0u;
+          if (hi > bhi || (hi == bhi && lo > blo)) { bhi = hi; blo = lo; bi = r; }
+        }
+        // warp argmax: largest (hi, lo), smallest row on ties
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, bhi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, bhi == mhi ? blo : 0u);
+        const int wp = (int)__reduce_min_sync(0xffffffffu, (bhi == mhi && blo == mlo) ? (unsigned)bi : 0x7fffffffu);
+        int p = wp;
+        if (NPW > 1) {
+          if (lane == 0) {
+            sCand[pw * 3 + 0] = mhi;
+            sCand[pw * 3 + 1] = mlo;
+            sCand[pw * 3 + 2] = (unsigned)wp;
+          }
+          psync();
+          unsigned ghi = sCand[0], glo = sCand[1];
+          p = (int)sCand[2];
+#pragma unroll
+          for (int w2 = 1; w2 < NPW; ++w2) {
+            const unsigned h2 = sCand[w2 * 3], l2 = sCand[w2 * 3 + 1];
+            const int r2 = (int)sCand[w2 * 3 + 2];
+            if (h2 > ghi || (h2 == ghi && (l2 > glo || (l2 == glo && r2 < p)))) { ghi = h2; glo = l2; p = r2; }
+          }
+          if (ghi == 0u) p = 0x7fffffff;
+        } else if (mhi == 0u) {
+          p = 0x7fffffff;
+        }
+        if (p >= N) { ok = false; p = 0; }
+        pt[t] = p;
+        if (pw == 0 && lane == 0) q[k0 + t] = p;
+        const int owner = p & 31, oslot = (p >> 5) / NPW, ow = (p >> 5) % NPW;
+        double prow[8];
+        if (NPW > 1) {
+          if (pw == ow && lane == owner)
+#pragma unroll
+            for (int i = 0; i < RPL; ++i)
+              if (i == oslot)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) sProw[j] = a[i][j];
+          psync();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) prow[j] = sProw[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            double v = a[0][j];
+#pragma unroll
+            for (int i = 1; i < RPL; ++i) v = oslot == i ? a[i][j] : v;
+            prow[j] = __shfl_sync(0xffffffffu, v, owner);
+          }
+        }
+        const double piv = prow[t];
+        if (!(fabs(piv) > 0.0) || !isfinite(piv)) ok = false;
+        const double pinv = 1.0 / piv;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) prow[j] = (j == t ? 1.0 : prow[j]) * pinv;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const bool isp = (pw == ow) && (lane == owner) && (oslot == i);
+          const double cr = a[i][t];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const double v = (j == t ? 0.0 : a[i][j]) - cr * prow[j];
+            a[i][j] = isp ? prow[j] : v;
+          }
+          if (isp) used |= 1u << i;
+        }
+      }
+    }
+    double* U = Ub + (pan & 1) * L::UF;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = row_of(i);
+      if (r < NP) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          A[r * S + k0 + j] = a[i][j];
+          const double u = (pt[j] >= 0) ? a[i][j] - (r == pt[j] ? 1.0 : 0.0) : 0.0;
+          U[((r >> 3) * 2 + (j >> 2)) * 32 + (r & 7) * 4 + (j & 3)] = u;
+        }
+      }
+    }
+    if (pw == 0 && lane == 0)
+      for (int t = nbp; t < 8; ++t) q[k0 + t] = -1;
+  };
+
+  auto update_tile = [&](const double* U, int ct, double r0, double r1, int rt0, int rt1, int rts) {
+    for (int rt = rt0; rt < rt1; rt += rts) {
+      double* cp = A + (rt * 8 + nr) * S + ct * 8 + kq * 2;
+      const double2 cv = *reinterpret_cast<const double2*>(cp);
+      double c[2] = {cv.x, cv.y};
+      dmma_8x8x4(c, U[(rt * 2 + 0) * 32 + lane], r0);
+      dmma_8x8x4(c, U[(rt * 2 + 1) * 32 + lane], r1);
+      *reinterpret_cast<double2*>(cp) = make_double2(c[0], c[1]);
+    }
+  };
+
+  for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
+    double* M = mats + (size_t)m * N * N;
+    __syncthreads();
+    if constexpr (N % 2 == 0) {
+      const double2* M2 = reinterpret_cast<const double2*>(M);
+      for (int i = tid; i < N * N / 2; i += NT) {
+        const int rr = (2 * i) / N, c = (2 * i) % N;
+        *reinterpret_cast<double2*>(A + rr * S + c) = __ldcs(M2 + i);
+      }
+    } else {
+      for (int i = tid; i < N * N; i += NT) A[(i / N) * S + i % N] = __ldcs(M + i);
+    }
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    unsigned used = 0u;
+    bool ok = true;
+    for (int pan = -1; pan < NPAN; ++pan) {
+      const double* U = Ub + (pan & 1) * L::UF;
+      const int k0 = pan * 8, nxt = pan + 1;
+      if (pan < 0) {
+        if (panel) factor_panel(0, used, ok);
+      } else if (panel) {
+        if (nxt < NPAN) {
+          // R_p on panel p+1's columns (read by all panel warps before any
+          // of them updates those columns), update them, factor panel p+1
+          const int c = nxt * 8 + nr;
+          const double r0 = q[k0 + kq] >= 0 ? A[q[k0 + kq] * S + c] : 0.0;
+          const double r1 = q[k0 + kq + 4] >= 0 ? A[q[k0 + kq + 4] * S + c] : 0.0;
+          psync();
+          update_tile(U, nxt, r0, r1, pw, T, NPW);
+          psync();
+          factor_panel(nxt, used, ok);
+        }
+      } else {
+        const int uw = warp - NPW, nuw = NWT - NPW;
+        const int pr0 = q[k0 + kq], pr1 = q[k0 + kq + 4];
+        int slot = 0;
+        for (int ct = 0; ct < T; ++ct) {
+          if (ct == pan || ct == nxt) continue;
+          if ((slot++ % nuw) != uw) continue;
+          const int c = ct * 8 + nr;
+          const double r0 = pr0 >= 0 ? A[pr0 * S + c] : 0.0;
+          const double r1 = pr1 >= 0 ? A[pr1 * S + c] : 0.0;
+          __syncwarp();
+          update_tile(U, ct, r0, r1, 0, T, 1);
+        }
+      }
+      __syncthreads();
+    }
+    if (panel && !ok && lane == 0) *flag = 1;
+    for (int k = tid; k < N; k += NT) qi[q[k]] = k;
+    __syncthreads();
+    int bad = *flag;
+    if constexpr (N % 2 == 0) {
+      double2* M2 = reinterpret_cast<double2*>(M);
+      for (int i = tid; i < N * N / 2; i += NT) {
+        const int c = (2 * i) / N, rr = (2 * i) % N, qc = qi[c];
+        const double v0 = A[q[rr] * S + qc], v1 = A[q[rr + 1] * S + qc];
+        bad |= !isfinite(v0) || !isfinite(v1);
+        M2[i] = make_double2(v0, v1);
+      }
+    } else {
+      for (int i = tid; i < N * N; i += NT) {
+        const double v = A[q[i % N] * S + qi[i / N]];
+        bad |= !isfinite(v);
+        M[i] = v;
+      }
+    }
+    if (__syncthreads_or(bad) && tid == 0) report(status, 0, 0, m);
+  }
+}
+
+}  // namespace mhdg
