@@ -484,7 +484,13 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 #endif
 template <int N>
 static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s) {
-  constexpr int NWT = N >= 64 ? 8 : 4;
+#ifndef MHDG_GJ_NWT
+#define MHDG_GJ_NWT 8
+#endif
+#ifndef MHDG_GJ_NWT_SMALL
+#define MHDG_GJ_NWT_SMALL 4
+#endif
+  constexpr int NWT = N >= 64 ? MHDG_GJ_NWT : MHDG_GJ_NWT_SMALL;
   constexpr int NPWS = N >= 64 ? MHDG_GJ_NPW : MHDG_GJ_NPW_SMALL;
   if constexpr (NPWS > 1) {   // panel rows split over NPW warps
     constexpr int NPW = NPWS;
