@@ -1030,6 +1030,12 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
   // padding lanes of C (st >= 25) stay zero
   for (int i = tid; i < L::C_; i += NT) sC[i] = 0.0;
 
+#ifdef MHDG_RES_TIMING
+  long long tl = clock64();
+#define LIN_T(k) do { const long long t_ = clock64(); if (tid == 0) atomicAdd(&g_res_clk[k], (unsigned long long)(t_ - tl)); tl = t_; } while (0)
+#else
+#define LIN_T(k) do { } while (0)
+#endif
   for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
     if (tid == 0) bulk_wait_read();   // previous macro's S left shared memory
     __syncthreads();
@@ -1050,6 +1056,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
       const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
       sTR[i] = trace[((size_t)sFid[k] * NFN + sTid[k * NFN + j]) * 5 + s2];
     }
+    LIN_T(0);
     // ---- pointwise duals for all volume quadrature points
     for (int it = tid; it < NQ * 5; it += NT) {
       const int q = it / 5, t = it % 5;
@@ -1097,6 +1104,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
       for (int s2 = 0; s2 < 5; ++s2) C[3 * CS + s2 * 5 + t] = weight * (vw * ud[s2].d);
     }
     __syncthreads();
+    LIN_T(1);
     // ---- S volume blocks on the tensor cores
     double acc[L::PPW][IT][2];
 #pragma unroll
@@ -1168,6 +1176,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     // ---- face tiles: hw, hhat, hh tensors of all four tiles in one pass,
     //      then the S face blocks tile by tile (fixed accumulation order)
     __syncthreads();
+    LIN_T(2);
     for (int it4 = tid; it4 < 4 * NQF * 10; it4 += NT) {
       {
         const int k = it4 / (NQF * 10), it = it4 % (NQF * 10);
@@ -1255,6 +1264,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         }
       }
     }
+    __syncthreads();
+    LIN_T(3);
     for (int k = 0; k < 4; ++k) {
       __syncthreads();
       const double* sHWk = sHW + k * NQF * 25;
@@ -1280,6 +1291,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     //      k = 3); k_gj_blocked inverts it in place
     fence_proxy_async();
     __syncthreads();
+    LIN_T(4);
     if (tid == 0) bulk_s2g(sinv + (size_t)e * NM * NM, S, (uint32_t)(NM * NM * sizeof(double)));
   }
   if (tid == 0) bulk_wait_all();
