@@ -482,28 +482,20 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 #ifndef MHDG_GJ_NPW_SMALL
 #define MHDG_GJ_NPW_SMALL 1  // panel warps for the face blocks (N < 64)
 #endif
-template <int N>
-static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s) {
 #ifndef MHDG_GJ_NWT
 #define MHDG_GJ_NWT 8
 #endif
 #ifndef MHDG_GJ_NWT_SMALL
 #define MHDG_GJ_NWT_SMALL 4
 #endif
+template <int N>
+static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s) {
   constexpr int NWT = N >= 64 ? MHDG_GJ_NWT : MHDG_GJ_NWT_SMALL;
-  constexpr int NPWS = N >= 64 ? MHDG_GJ_NPW : MHDG_GJ_NPW_SMALL;
-  if constexpr (NPWS > 1) {   // panel rows split over NPW warps
-    constexpr int NPW = NPWS;
-    using GL = GJLA2<N, NWT, NPW>;
-    if (set_smem(k_gj_la2<N, NWT, NPW>, GL::bytes)) return MHDG_CUDA_ERROR;
-    k_gj_la2<N, NWT, NPW><<<grid_for(c, nmat, occ(k_gj_la2<N, NWT, NPW>, GL::NT, GL::bytes)), GL::NT, GL::bytes,
-                            s>>>(nmat, mats, status);
-    return MHDG_OK;
-  }
-  using GL = GJLA<N, NWT>;
-  if (set_smem(k_gj_la<N, NWT>, GL::bytes)) return MHDG_CUDA_ERROR;
-  k_gj_la<N, NWT><<<grid_for(c, nmat, occ(k_gj_la<N, NWT>, GL::NT, GL::bytes)), GL::NT, GL::bytes, s>>>(
-      nmat, mats, status);
+  constexpr int NPW = N >= 64 ? MHDG_GJ_NPW : MHDG_GJ_NPW_SMALL;
+  using GL = GJLA2<N, NWT, NPW>;
+  if (set_smem(k_gj_la2<N, NWT, NPW>, GL::bytes)) return MHDG_CUDA_ERROR;
+  k_gj_la2<N, NWT, NPW><<<grid_for(c, nmat, occ(k_gj_la2<N, NWT, NPW>, GL::NT, GL::bytes)), GL::NT, GL::bytes,
+                          s>>>(nmat, mats, status);
   return MHDG_OK;
 }
 template <int P>

@@ -189,252 +189,21 @@ k_gj_blocked(int nmat, double* __restrict__ mats, unsigned long long* status, do
 namespace mhdg {
 
 // ===========================================================================
-// Gauss-Jordan inverse with one-panel lookahead.
+// Gauss-Jordan inverse with one-panel lookahead (k_gj_la2).
 //
 // Same arithmetic as k_gj_blocked (8-column panels, implicit partial
 // pivoting, composite panel transform A += U R on the FP64 tensor cores) but
 // the serial pivot search no longer stops the whole CTA at a barrier per
-// pivot: warp 0 factors panel p + 1 alone, warp-synchronously (its 4 rows
-// per lane x 8 columns in registers, argmax by redux.sync, pivot row by
-// shuffles), while warps 1.. apply panel p's update to every other column.
-// Between two CTA barriers:
-//   warp 0      : R_p on panel p+1's columns, A[:, p+1] += U_p R_p, factor
+// pivot: the panel warps factor panel p + 1 while the update warps apply
+// panel p's update to every other column.  Between two CTA barriers:
+//   panel warps : R_p on panel p+1's columns, A[:, p+1] += U_p R_p, factor
 //                 panel p+1 -> U_{p+1} (double-buffered), pivots
-//   update warps: R_p (pivot rows, all columns but panels p, p+1) into a
-//                 fragment-ordered buffer, then A[:, c] += U_p R_p[:, c]
-// Panel p+1's columns therefore hold every update < p+1 when warp 0 factors
-// them, and no two warps touch the same column in one interval.
-// ===========================================================================
-template <int N, int NWT>
-struct GJLA {
-  using G = GJB<N>;
-  static constexpr int NP = G::NP, S = G::S, T = G::T, NPAN = G::NPAN;
-  static constexpr int RPL = (NP + 31) / 32;            // panel rows per lane (warp 0)
-  static constexpr int NT = 32 * NWT;
-  static constexpr int UF = T * 2 * 32;                 // U fragments [rt][ks][lane]
-  static constexpr int RF = T * 2 * 32;                 // R fragments [ct][ks][lane]
-  static constexpr size_t bytes = (size_t)(NP * S + 2 * UF) * 8 + (size_t)(2 * NP + 4) * 4;
-};
-
-template <int N, int NWT>
-__global__ void __launch_bounds__(GJLA<N, NWT>::NT, 2)
-k_gj_la(int nmat, double* __restrict__ mats, unsigned long long* status) {
-  using L = GJLA<N, NWT>;
-  constexpr int NP = L::NP, S = L::S, T = L::T, NPAN = L::NPAN, RPL = L::RPL, NT = L::NT;
-  extern __shared__ __align__(16) double smem[];
-  double* A = smem;                        // NP x S
-  double* Ub = A + NP * S;                 // 2 x UF
-  int* q = (int*)(Ub + 2 * L::UF);         // NP: pivot row of step k
-  int* qi = q + NP;                        // NP
-  int* flag = qi + NP;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kq = lane & 3, nr = lane >> 2;
-  for (int idx = tid; idx < NP * S; idx += NT) A[idx] = 0.0;
-
-  // warp 0: factor panel `pan` (columns k0..k0+7) held in registers
-  auto factor_panel = [&](int pan, unsigned& used, bool& ok) {
-    const int k0 = pan * 8, nbp = min(8, N - k0);
-    double a[RPL][8];
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) a[i][j] = r < NP ? A[r * S + k0 + j] : 0.0;
-    }
-    int pt[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      pt[t] = -1;
-      if (t < nbp) {
-        // lane-local best unused row (largest |a|, first index on ties)
-        unsigned bhi = 0u, blo = 0u;
-        int bi = 0x7fffffff;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const int r = lane + 32 * i;
-          const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(a[i][t]));
-          const bool cand = r < N && !((used >> i) & 1u);
-          const unsigned hi = cand ? (unsigned)(bits >> 32) + 1u : 0u, lo = cand ? (unsigned)bits : 0u;
-          if (hi > bhi || (hi == bhi && lo > blo)) { bhi = hi; blo = lo; bi = r; }
-        }
-        const unsigned mhi = __reduce_max_sync(0xffffffffu, bhi);
-        const unsigned tie = __ballot_sync(0xffffffffu, bhi == mhi && mhi != 0u);
-        int p;
-        if (__popc(tie) == 1) {   // one lane holds the largest high word: its row
-          p = __shfl_sync(0xffffffffu, bi, __ffs(tie) - 1);
-        } else {
-          const unsigned mlo = __reduce_max_sync(0xffffffffu, bhi == mhi ? blo : 0u);
-          p = (int)__reduce_min_sync(0xffffffffu, (bhi == mhi && blo == mlo && mhi != 0u) ? (unsigned)bi
-                                                                                      : 0x7fffffffu);
-        }
-        if (p >= N) { ok = false; p = 0; }
-        pt[t] = p;
-        if (lane == 0) q[k0 + t] = p;
-        const int owner = p & 31, slot = p >> 5;
-        double prow[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          double v = a[0][j];
-#pragma unroll
-          for (int i = 1; i < RPL; ++i) v = slot == i ? a[i][j] : v;
-          prow[j] = __shfl_sync(0xffffffffu, v, owner);
-        }
-        const double piv = prow[t];
-        if (!(fabs(piv) > 0.0) || !isfinite(piv)) ok = false;
-        const double pinv = drcp(piv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) prow[j] = (j == t ? 1.0 : prow[j]) * pinv;
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const bool isp = (lane == owner) && (slot == i);
-          const double cr = a[i][t];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const double v = (j == t ? 0.0 : a[i][j]) - cr * prow[j];
-            a[i][j] = isp ? prow[j] : v;
-          }
-          if (isp) used |= 1u << i;
-        }
-      }
-    }
-    // final panel values, U = panel - E in fragment order, pivots
-    double* U = Ub + (pan & 1) * L::UF;
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      if (r < NP) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          A[r * S + k0 + j] = a[i][j];
-          const double u = (pt[j] >= 0) ? a[i][j] - (r == pt[j] ? 1.0 : 0.0) : 0.0;
-          U[((r >> 3) * 2 + (j >> 2)) * 32 + (r & 7) * 4 + (j & 3)] = u;
-        }
-      }
-    }
-    if (lane == 0)
-      for (int t = nbp; t < 8; ++t) q[k0 + t] = -1;
-  };
-
-  // A[:, tile ct] += U R on all row tiles; R fragments in registers
-  auto update_tile = [&](const double* U, int ct, double r0, double r1, int rt0, int rt1) {
-    int rt = rt0;
-    for (; rt + 1 < rt1; rt += 2) {   // two independent row tiles in flight
-      double* cp0 = A + (rt * 8 + nr) * S + ct * 8 + kq * 2;
-      double* cp1 = cp0 + 8 * S;
-      const double2 v0 = *reinterpret_cast<const double2*>(cp0);
-      const double2 v1 = *reinterpret_cast<const double2*>(cp1);
-      const double u00 = U[(rt * 2 + 0) * 32 + lane], u01 = U[(rt * 2 + 1) * 32 + lane];
-      const double u10 = U[(rt * 2 + 2) * 32 + lane], u11 = U[(rt * 2 + 3) * 32 + lane];
-      double c0[2] = {v0.x, v0.y}, c1[2] = {v1.x, v1.y};
-      dmma_8x8x4(c0, u00, r0);
-      dmma_8x8x4(c1, u10, r0);
-      dmma_8x8x4(c0, u01, r1);
-      dmma_8x8x4(c1, u11, r1);
-      *reinterpret_cast<double2*>(cp0) = make_double2(c0[0], c0[1]);
-      *reinterpret_cast<double2*>(cp1) = make_double2(c1[0], c1[1]);
-    }
-    if (rt < rt1) {
-      double* cp = A + (rt * 8 + nr) * S + ct * 8 + kq * 2;
-      const double2 cv = *reinterpret_cast<const double2*>(cp);
-      double c[2] = {cv.x, cv.y};
-      dmma_8x8x4(c, U[(rt * 2 + 0) * 32 + lane], r0);
-      dmma_8x8x4(c, U[(rt * 2 + 1) * 32 + lane], r1);
-      *reinterpret_cast<double2*>(cp) = make_double2(c[0], c[1]);
-    }
-  };
-
-  for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
-    double* M = mats + (size_t)m * N * N;
-    __syncthreads();
-    if constexpr (N % 2 == 0) {
-      const double2* M2 = reinterpret_cast<const double2*>(M);
-      for (int i = tid; i < N * N / 2; i += NT) {
-        const int rr = (2 * i) / N, c = (2 * i) % N;
-        *reinterpret_cast<double2*>(A + rr * S + c) = __ldcs(M2 + i);
-      }
-    } else {
-      for (int i = tid; i < N * N; i += NT) A[(i / N) * S + i % N] = __ldcs(M + i);
-    }
-    if (tid == 0) *flag = 0;
-    __syncthreads();
-    unsigned used = 0u;   // warp 0: rows already chosen as pivots (bit i: row lane + 32 i)
-    bool ok = true;
-#ifdef MHDG_RES_TIMING
-    long long tg = clock64();
-#define GJT(k) do { const long long t_ = clock64(); if (lane == 0 && (warp == 0 || warp == 1)) atomicAdd(&g_res_clk[k], (unsigned long long)(t_ - tg)); tg = t_; } while (0)
-#else
-#define GJT(k) do { } while (0)
-#endif
-    // pan = -1: warp 0 factors panel 0 alone (one inlined copy of the panel
-    // factorization serves every panel)
-    for (int pan = -1; pan < NPAN; ++pan) {
-      const double* U = Ub + (pan & 1) * L::UF;
-      const int k0 = pan * 8, nxt = pan + 1;
-      GJT(warp == 0 ? 9 : 13);
-      if (pan < 0) {
-        if (warp == 0) factor_panel(0, used, ok);
-      } else if (warp == 0) {
-        if (nxt < NPAN) {
-          // R_p on panel p+1's columns, update them, factor panel p+1
-          const int c = nxt * 8 + nr;
-          const double r0 = q[k0 + kq] >= 0 ? A[q[k0 + kq] * S + c] : 0.0;
-          const double r1 = (kq + 4 < 8 && q[k0 + kq + 4] >= 0) ? A[q[k0 + kq + 4] * S + c] : 0.0;
-          __syncwarp();
-          update_tile(U, nxt, r0, r1, 0, T);
-          __syncwarp();
-          GJT(10);
-          factor_panel(nxt, used, ok);
-          GJT(11);
-        }
-      } else {
-        // each update warp owns whole column tiles (all but panels p, p+1):
-        // it reads R_p for its columns straight from the pivot rows, which
-        // no other warp writes in this interval
-        const int uw = warp - 1, nuw = NWT - 1;
-        const int pr0 = q[k0 + kq], pr1 = q[k0 + kq + 4];
-        int slot = 0;
-        for (int ct = 0; ct < T; ++ct) {
-          if (ct == pan || ct == nxt) continue;
-          if ((slot++ % nuw) != uw) continue;
-          const int c = ct * 8 + nr;
-          const double r0 = pr0 >= 0 ? A[pr0 * S + c] : 0.0;
-          const double r1 = pr1 >= 0 ? A[pr1 * S + c] : 0.0;
-          __syncwarp();
-          update_tile(U, ct, r0, r1, 0, T);
-        }
-        GJT(12);
-      }
-      __syncthreads();
-    }
-    if (warp == 0 && !ok && lane == 0) *flag = 1;
-    for (int k = tid; k < N; k += NT) qi[q[k]] = k;
-    __syncthreads();
-    int bad = *flag;
-    if constexpr (N % 2 == 0) {
-      double2* M2 = reinterpret_cast<double2*>(M);
-      for (int i = tid; i < N * N / 2; i += NT) {
-        const int c = (2 * i) / N, rr = (2 * i) % N, qc = qi[c];
-        const double v0 = A[q[rr] * S + qc], v1 = A[q[rr + 1] * S + qc];
-        bad |= !isfinite(v0) || !isfinite(v1);
-        M2[i] = make_double2(v0, v1);
-      }
-    } else {
-      for (int i = tid; i < N * N; i += NT) {
-        const double v = A[q[i % N] * S + qi[i / N]];
-        bad |= !isfinite(v);
-        M[i] = v;
-      }
-    }
-    if (__syncthreads_or(bad) && tid == 0) report(status, 0, 0, m);
-  }
-}
-
-}  // namespace mhdg
-
-namespace mhdg {
-
-// ===========================================================================
-// Lookahead Gauss-Jordan with NPW panel warps: the panel rows are split over
+//   update warps: A[:, c] += U_p R_p[:, c] on their own column tiles (all but
+//                 panels p, p+1), R_p read straight from the pivot rows
+// Panel p+1's columns therefore hold every update < p+1 when it is factored,
+// and no two warps touch the same column in one interval.
+//
+// With NPW panel warps the panel rows are split over
 // NPW warps (rows 32 (pw + NPW i) + lane), so each pivot step handles
 // RPL = NP / (32 NPW) rows per lane; the warps' argmax candidates and the
 // pivot row meet in shared memory behind a named barrier of the panel
