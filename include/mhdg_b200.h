@@ -222,6 +222,18 @@ double mhdg_dmma_probe(int device, void* stream);
    algebra against libm; replaces no reference symbol (numpy's exp / log /
    true_divide inside gas.py / fluxes.py) */
 int mhdg_math_eval(int fn, int64_t n, const double* x, double* y, void* stream);
+/* Host (CPU) topology kernels of the table builder; no device work.
+ * mhdg_pair_sides: skeleton pairing (reference mesh.py:226-299): sides with
+ * identical canonical quantised vertex keys (n_sides x key_width int64) are
+ * paired, partner[s] = other side or -1; returns the number of key groups
+ * with more than two sides (TopologyError when > 0).
+ * mhdg_match_points: trace-node matching (reference assembly.py:299-322):
+ * match[f][a] = first b minimising |pts_nb[f][a] - pts_own[f][b]|; returns
+ * the largest matched distance, or -1 when a face's matching is not a
+ * permutation. */
+int64_t mhdg_pair_sides(int64_t n_sides, int key_width, const int64_t* keys, int64_t* partner);
+double mhdg_match_points(int64_t n_faces, int nt, int dim, const double* pts_nb,
+                         const double* pts_own, int64_t* match);
 const char* mhdg_version(void);
 
 #ifdef __cplusplus

@@ -100,6 +100,8 @@ _SIGS = {
     "mhdg_fp64_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_dmma_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_math_eval": (C.c_int, [C.c_int, C.c_int64, dptr, dptr, C.c_void_p]),
+    "mhdg_pair_sides": (C.c_int64, [C.c_int64, C.c_int, dptr, dptr]),
+    "mhdg_match_points": (C.c_double, [C.c_int64, C.c_int, C.c_int, dptr, dptr, dptr]),
     "mhdg_version": (C.c_char_p, []),
 }
 
@@ -187,6 +189,15 @@ def math_eval(fn, x):
     y = torch.empty_like(x)
     raise_for(lib.mhdg_math_eval(fn, x.numel(), ptr(x), ptr(y), stream_handle()), context="(math_eval)")
     return y
+
+
+def host_library():
+    """The library for its host-only entry points (table builder); None when
+    it is not built (the numpy builder is then used)."""
+    try:
+        return load()
+    except NativeUnavailable:
+        return None
 
 
 def fp64_probe(device=0):

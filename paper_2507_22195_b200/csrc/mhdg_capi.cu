@@ -16,6 +16,7 @@
 #include "mhdg_viscous.cuh"
 #include "mhdg_visc_fast.cuh"
 #include "mhdg_gj_blocked.cuh"
+#include "mhdg_host_mesh.cuh"
 
 using namespace mhdg;
 
@@ -71,6 +72,15 @@ static void* dalloc(mhdg_ctx* c, size_t bytes, int* err) {
   if (cudaMalloc(&d, bytes) != cudaSuccess) { *err = MHDG_OUT_OF_MEMORY; return nullptr; }
   c->allocs.push_back(d);
   return d;
+}
+
+extern "C" int64_t mhdg_pair_sides(int64_t n_sides, int key_width, const int64_t* keys, int64_t* partner) {
+  return mhdg_host::pair_sides(n_sides, key_width, keys, partner);
+}
+
+extern "C" double mhdg_match_points(int64_t n_faces, int nt, int dim, const double* pts_nb, const double* pts_own,
+                                    int64_t* match) {
+  return mhdg_host::match_points(n_faces, nt, dim, pts_nb, pts_own, match);
 }
 
 extern "C" const char* mhdg_version(void) { return "mhdg_b200 0.1 (sm_100a, fp64, m=1, P=1..4)"; }

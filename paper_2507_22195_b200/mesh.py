@@ -19,6 +19,8 @@ from __future__ import annotations
 
 import itertools
 import math
+import os
+from ctypes import c_void_p as _c_void_p
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -212,6 +214,16 @@ def build_box_macro_mesh(box, n_per_dim, m, periodic=True):
     return mesh
 
 
+def _host_lib():
+    """libmhdg_b200.so for its host-side topology entry points, or None when
+    the library is not built (numpy builder; identical results)."""
+    if os.environ.get("MHDG_NUMPY_TABLES"):
+        return None
+    from . import _native
+
+    return _native.host_library()
+
+
 def skeleton_arrays(mesh):
     """Pair macro sides into skeleton faces (mesh.py:226-299 semantics).
 
@@ -249,22 +261,35 @@ def skeleton_arrays(mesh):
                 decided |= gt | lt
             kk[swap, j - 1], kk[swap, j] = cur[swap], prev[swap]
             j -= 1
-    flat = kk.reshape(len(kk), d * d)
-    _, group, counts = np.unique(flat, axis=0, return_inverse=True,
-                                 return_counts=True)
-    group = group.ravel()
-    if counts.max() > 2:
-        raise TopologyError(f"{int((counts > 2).sum())} face groups have "
-                            "more than two sides")
-    n_groups = len(counts)
-    first = np.full(n_groups, np.iinfo(np.int64).max, dtype=np.int64)
-    second = np.full(n_groups, -1, dtype=np.int64)
-    sides = np.arange(len(group), dtype=np.int64)
-    np.minimum.at(first, group, sides)
-    is_second = sides != first[group]
-    second[group[is_second]] = sides[is_second]
-    face_order = np.argsort(first, kind="stable")
-    first, second = first[face_order], second[face_order]
+    flat = np.ascontiguousarray(kk.reshape(len(kk), d * d))
+    lib = _host_lib()
+    if lib is not None:
+        # native pairing (csrc/mhdg_host_mesh.cuh): sort by key, pair equal
+        # neighbours; faces in increasing owner-side order as below
+        partner = np.empty(len(flat), dtype=np.int64)
+        bad = lib.mhdg_pair_sides(len(flat), d * d, flat.ctypes.data_as(_c_void_p),
+                                  partner.ctypes.data_as(_c_void_p))
+        if bad > 0:
+            raise TopologyError(f"{int(bad)} face groups have more than two sides")
+        sides = np.arange(len(flat), dtype=np.int64)
+        first = sides[(partner < 0) | (sides < partner)]
+        second = partner[first]
+    else:
+        _, group, counts = np.unique(flat, axis=0, return_inverse=True,
+                                     return_counts=True)
+        group = group.ravel()
+        if counts.max() > 2:
+            raise TopologyError(f"{int((counts > 2).sum())} face groups have "
+                                "more than two sides")
+        n_groups = len(counts)
+        first = np.full(n_groups, np.iinfo(np.int64).max, dtype=np.int64)
+        second = np.full(n_groups, -1, dtype=np.int64)
+        sides = np.arange(len(group), dtype=np.int64)
+        np.minimum.at(first, group, sides)
+        is_second = sides != first[group]
+        second[group[is_second]] = sides[is_second]
+        face_order = np.argsort(first, kind="stable")
+        first, second = first[face_order], second[face_order]
 
     owner, owner_face = np.divmod(first, d + 1)
     has_nb = second >= 0

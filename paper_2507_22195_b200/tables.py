@@ -14,6 +14,7 @@ reference's per-face cdist loop, and produces the identical permutation.
 from __future__ import annotations
 
 import math
+from ctypes import c_void_p as _c_void_p
 
 import numpy as np
 
@@ -172,20 +173,33 @@ class HDGTables:
         has_nb = skel.neighbor >= 0
         boundary[own_e[~has_nb], own_f[~has_nb]] = True
         nbf = fids[has_nb]
-        chunk = max(1, 4_000_000 // max(1, nt * nt))
+        from .mesh import _host_lib
+
+        lib = _host_lib()
+        chunk = max(1, 4_000_000 // max(1, nt * nt)) if lib is None else max(1, len(nbf))
         for c0 in range(0, len(nbf), chunk):
             fs = nbf[c0:c0 + chunk]
             ne, nf = skel.neighbor[fs], skel.neighbor_face[fs]
             nb_pts = (mesh.macro_origins[ne][:, None, :]
                       + np.einsum("fnb,fab->fna", fun[nf], mesh.macro_jacobians[ne]))
             nb_pts = nb_pts - skel.shift[fs][:, None, :]
-            dist = np.sqrt(((nb_pts[:, :, None, :] - own_pts[fs][:, None, :, :]) ** 2)
-                           .sum(-1))                        # (c, nt_nb, nt_own)
-            match = dist.argmin(axis=2)
-            best = np.take_along_axis(dist, match[:, :, None], 2)[..., 0]
-            srt = np.sort(match, axis=1)
-            if best.max() > tol or np.any(srt[:, 1:] == srt[:, :-1]):
-                raise InvalidConfig("trace nodes of a skeleton face do not match")
+            if lib is not None:   # native nearest-point matching, same argmin
+                nbp = np.ascontiguousarray(nb_pts)
+                owp = np.ascontiguousarray(own_pts[fs])
+                match = np.empty((len(fs), nt), dtype=np.int64)
+                worst = lib.mhdg_match_points(len(fs), nt, d, nbp.ctypes.data_as(_c_void_p),
+                                              owp.ctypes.data_as(_c_void_p),
+                                              match.ctypes.data_as(_c_void_p))
+                if worst < 0 or worst > tol:
+                    raise InvalidConfig("trace nodes of a skeleton face do not match")
+            else:
+                dist = np.sqrt(((nb_pts[:, :, None, :] - own_pts[fs][:, None, :, :]) ** 2)
+                               .sum(-1))                    # (c, nt_nb, nt_own)
+                match = dist.argmin(axis=2)
+                best = np.take_along_axis(dist, match[:, :, None], 2)[..., 0]
+                srt = np.sort(match, axis=1)
+                if best.max() > tol or np.any(srt[:, 1:] == srt[:, :-1]):
+                    raise InvalidConfig("trace nodes of a skeleton face do not match")
             face_id[ne, nf] = fs
             side_of[ne, nf] = 1
             trace_perm[ne, nf] = match
