@@ -149,11 +149,12 @@ int mhdg_precond_factor(mhdg_ctx* ctx, const mhdg_lin_buffers* lin,
  * interior macros and then for the halo macros gives results bit-identical
  * to the whole-range call (two contributions per trace node, 0 + a + b),
  * which lets the trace halo exchange overlap the interior work.  matvec
- * stages: bit 0 = face-in + local solve, bit 1 = face-out.  Inviscid only
- * (MHDG_INVALID_CONFIG for a viscous context). */
-int mhdg_residual_range(mhdg_ctx* ctx, const double* w, const double* trace, int has_stage,
-                        double alpha, const double* offset, int check, double* r_w,
-                        double* r_trace, int64_t e_begin, int64_t e_end, int zero,
+ * stages: bit 0 = face-in + local solve, bit 1 = face-out.  q / r_q: the
+ * gradient unknowns and their residual of a viscous context (NULL
+ * otherwise). */
+int mhdg_residual_range(mhdg_ctx* ctx, const double* w, const double* trace, const double* q,
+                        int has_stage, double alpha, const double* offset, int check, double* r_w,
+                        double* r_trace, double* r_q, int64_t e_begin, int64_t e_end, int zero,
                         void* stream);
 int mhdg_matvec_range(mhdg_ctx* ctx, const mhdg_lin_buffers* lin, const double* x, double* y,
                       int64_t e_begin, int64_t e_end, int stages, int zero, void* stream);

@@ -76,8 +76,8 @@ _SIGS = {
     "mhdg_matvec": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, C.c_void_p]),
     "mhdg_matvec_range": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, C.c_int64,
                                     C.c_int64, C.c_int, C.c_int, C.c_void_p]),
-    "mhdg_residual_range": (C.c_int, [C.c_void_p, dptr, dptr, C.c_int, C.c_double, dptr, C.c_int,
-                                      dptr, dptr, C.c_int64, C.c_int64, C.c_int, C.c_void_p]),
+    "mhdg_residual_range": (C.c_int, [C.c_void_p, dptr, dptr, dptr, C.c_int, C.c_double, dptr, C.c_int,
+                                      dptr, dptr, dptr, C.c_int64, C.c_int64, C.c_int, C.c_void_p]),
     "mhdg_condensed_rhs": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, dptr,
                                      C.c_void_p]),
     "mhdg_recover": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, dptr, dptr,

@@ -405,11 +405,20 @@ extern "C" int mhdg_status_fetch(mhdg_ctx* c, mhdg_status* st, void* stream) {
 template <int P>
 static int launch_residual_visc(mhdg_ctx* c, const double* w, const double* q, const double* tr, int has_stage,
                                 double alpha, const double* off, int check, double* rw, double* rt, double* rq,
-                                cudaStream_t s) {
+                                cudaStream_t s, int e0 = 0, int e1 = -1) {
+  if (e1 < 0) e1 = c->E;
+  if (e1 <= e0) return MHDG_OK;
+  const Geo gv = geo_range(c->geo, e0, e1, c->nfn);
+  const size_t NMe = (size_t)c->nn * 5, NQe = (size_t)c->nq * 5;
+  w += e0 * NMe;
+  rw += e0 * NMe;
+  q += e0 * NMe * 3;
+  rq += e0 * NMe * 3;
+  if (off) off += e0 * NQe;
   const size_t smem = ResVisc<P>::bytes;
   if (set_smem(k_residual_visc<P>, smem)) return MHDG_CUDA_ERROR;
-  k_residual_visc<P><<<grid_for(c, c->E, occ(k_residual_visc<P>, 128, smem)), 128, smem, s>>>(
-      c->geo, c->vg, w, q, tr, has_stage, alpha, off, check, rw, rt, rq, c->d_status);
+  k_residual_visc<P><<<grid_for(c, e1 - e0, occ(k_residual_visc<P>, 128, smem)), 128, smem, s>>>(
+      gv, c->vg, w, q, tr, has_stage, alpha, off, check, rw, rt, rq, c->d_status);
   c->launches++;
   CK(cudaGetLastError());
   return MHDG_OK;
@@ -430,18 +439,27 @@ extern "C" int mhdg_solve_gradient(mhdg_ctx* c, const double* w, const double* t
   return MHDG_OK;
 }
 
-extern "C" int mhdg_residual_range(mhdg_ctx* c, const double* w, const double* trace, int has_stage,
-                                   double alpha, const double* offset, int check, double* r_w,
-                                   double* r_trace, int64_t e_begin, int64_t e_end, int zero,
+extern "C" int mhdg_residual_range(mhdg_ctx* c, const double* w, const double* trace, const double* q,
+                                   int has_stage, double alpha, const double* offset, int check, double* r_w,
+                                   double* r_trace, double* r_q, int64_t e_begin, int64_t e_end, int zero,
                                    void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
-  if (c->visc || e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
+  if (e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
   if (zero) {
     CK(cudaMemsetAsync(c->d_status, 0xff, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(r_trace, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   }
   const int e0 = (int)e_begin, e1 = (int)e_end;
+  if (c->visc) {
+    if (!q || !r_q) return MHDG_INVALID_CONFIG;
+    switch (c->p) {
+      case 1: return launch_residual_visc<1>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s, e0, e1);
+      case 2: return launch_residual_visc<2>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s, e0, e1);
+      case 3: return launch_residual_visc<3>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s, e0, e1);
+      default: return launch_residual_visc<4>(c, w, q, trace, has_stage, alpha, offset, check, r_w, r_trace, r_q, s, e0, e1);
+    }
+  }
   switch (c->p) {
     case 1: return launch_residual<1>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s, e0, e1);
     case 2: return launch_residual<2>(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s, e0, e1);
@@ -728,24 +746,36 @@ static int condensed_face2(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, con
 }
 
 template <int P>
+// macros [e0, e1); stages: bit 0 = face-in + local solve, bit 1 = face-out
 static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* rw,
-                          const double* rq, double* y, double* dw, cudaStream_t s) {
+                          const double* rq, double* y, double* dw, cudaStream_t s, int e0 = 0, int e1 = -1,
+                          int stages = 3) {
   using D = Dims<P>;
   using V = VFast<P>;
+  if (e1 < 0) e1 = c->E;
+  if (e1 <= e0) return MHDG_OK;
   const size_t ism = sizeof(typename V::In) * V::MBI, osm = sizeof(typename V::Out) * V::MBO;
   if (set_smem(k_visc_in2<P>, ism) || set_smem(k_visc_out2<P>, osm)) return MHDG_CUDA_ERROR;
-  double* gbuf = c->d_gbuf;
-  double* zbuf = (mode == 2) ? dw : c->d_zbuf;
-  const int nbi = (c->E + V::MBI - 1) / V::MBI, nbo = (c->E + V::MBO - 1) / V::MBO;
-  k_visc_in2<P><<<grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s>>>(c->geo, c->vg, mode, L->wlin,
-                                                                                 L->hhat, x, rw, rq, gbuf);
-  using LS = LocalSolveCfg<D::NM>;
-  k_local_solve<D::NM, LS::NT><<<grid_for(c, (c->E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)),
-                                 LS::NT, 0, s>>>(c->E, L->sinv, gbuf, 0, zbuf);
-  c->launches += 2;
-  if (mode != 2) {
+  const Geo gv = geo_range(c->geo, e0, e1, c->nfn);
+  const int E = e1 - e0;
+  const size_t vm = (size_t)e0 * D::NM, ten = (size_t)e0 * 4 * c->nqf * 25;
+  double* gbuf = c->d_gbuf + vm;
+  double* zbuf = ((mode == 2) ? dw : c->d_zbuf) + vm;
+  const double* wlin = L->wlin + vm;
+  const double* rwv = rw ? rw + vm : nullptr;
+  const double* rqv = rq ? rq + vm * 3 : nullptr;
+  const int nbi = (E + V::MBI - 1) / V::MBI, nbo = (E + V::MBO - 1) / V::MBO;
+  if (stages & 1) {
+    k_visc_in2<P><<<grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s>>>(gv, c->vg, mode, wlin,
+                                                                                   L->hhat + ten, x, rwv, rqv, gbuf);
+    using LS = LocalSolveCfg<D::NM>;
+    k_local_solve<D::NM, LS::NT><<<grid_for(c, (E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)),
+                                   LS::NT, 0, s>>>(E, L->sinv + vm * D::NM, gbuf, 0, zbuf);
+    c->launches += 2;
+  }
+  if ((stages & 2) && mode != 2) {
     k_visc_out2<P><<<grid_for(c, nbo, occ(k_visc_out2<P>, 128, osm)), 128, osm, s>>>(
-        c->geo, c->vg, mode, L->wlin, L->hh, L->hw, x, zbuf, rq, y);
+        gv, c->vg, mode, wlin, L->hh + ten, L->hw + ten, x, zbuf, rqv, y);
     c->launches++;
   }
   CK(cudaGetLastError());
@@ -774,9 +804,17 @@ extern "C" int mhdg_matvec_range(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
                                  int64_t e_begin, int64_t e_end, int stages, int zero, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
-  if (c->visc || e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
+  if (e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
   if (zero) CK(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   const int e0 = (int)e_begin, e1 = (int)e_end;
+  if (c->visc) {
+    switch (c->p) {
+      case 1: return condensed_visc<1>(c, 0, L, x, nullptr, nullptr, y, nullptr, s, e0, e1, stages);
+      case 2: return condensed_visc<2>(c, 0, L, x, nullptr, nullptr, y, nullptr, s, e0, e1, stages);
+      case 3: return condensed_visc<3>(c, 0, L, x, nullptr, nullptr, y, nullptr, s, e0, e1, stages);
+      default: return MHDG_INVALID_CONFIG;
+    }
+  }
   switch (c->p) {
     case 1: return condensed_face2<1>(c, 0, L, x, nullptr, y, nullptr, s, e0, e1, stages);
     case 2: return condensed_face2<2>(c, 0, L, x, nullptr, y, nullptr, s, e0, e1, stages);

@@ -156,8 +156,8 @@ k_residual_visc(Geo g, ViscGeo vg, const double* __restrict__ w, const double* _
         }
       }
       double u[5];
-      if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e);
-      if (check && !admissible(u, gam)) report(status, 0, 2, e);
+      if (!to_conservative(wq, g.form, gam, u)) report(status, 0, 0, e + g.e_base);
+      if (check && !admissible(u, gam)) report(status, 0, 2, e + g.e_base);
       double F[5][3], Gv[5][3];
       flux(u, gam, F);
       visc_G(vg, g.form, wq, u, qq, gam, Gv);
@@ -207,10 +207,10 @@ k_residual_visc(Geo g, ViscGeo vg, const double* __restrict__ w, const double* _
         }
       }
       double u[5], uh[5];
-      if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e);
-      if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e);
-      if (check && !admissible(u, gam)) report(status, 1 + k, 2, e);
-      if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e);
+      if (!to_conservative(wq, g.form, gam, u)) report(status, 1 + k, 0, e + g.e_base);
+      if (!to_conservative(whq, g.form, gam, uh)) report(status, 1 + k, 1, e + g.e_base);
+      if (check && !admissible(u, gam)) report(status, 1 + k, 2, e + g.e_base);
+      if (check && !admissible(uh, gam)) report(status, 1 + k, 3, e + g.e_base);
       const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
       double fh[5], Gv[5][3];
       numerical_flux(g.kind, u, uh, n, gam, fh, g.form == FORM_ENTROPY ? wq : nullptr,

@@ -80,11 +80,10 @@ class PartitionedDiscretization:
     @property
     def overlap(self):
         """Halo exchange overlapped with the interior macros' kernels: an
-        asynchronous transport (start / finish), an inviscid operator and a
-        non-empty contiguous interior range."""
+        asynchronous transport (start / finish) and a non-empty contiguous
+        interior range."""
         i0, i1 = self.part.interior
-        return (hasattr(self.exchange, "fill_ghosts_start") and self.local.viscosity is None
-                and i1 > i0)
+        return hasattr(self.exchange, "fill_ghosts_start") and i1 > i0
 
     def residuals(self, fields, stage=None, check=True, sync=True):
         if not self.overlap:
@@ -97,13 +96,15 @@ class PartitionedDiscretization:
         d = self.local
         w, tr = d._fields(fields)
         fields.w, fields.trace = w, tr
+        q = d._q(fields)
         h = self.exchange.fill_ghosts_start(tr)
         r_w, r_tr = torch.empty_like(w), torch.empty_like(tr)
+        r_q = torch.empty_like(q) if q is not None else None
         off = None
         if stage is not None and stage.offset is not None:
             off = d._dev(stage.offset)
-        args = (int(stage is not None), float(stage.alpha) if stage is not None else 0.0,
-                N.ptr(off), int(bool(check)), N.ptr(r_w), N.ptr(r_tr))
+        args = (N.ptr(q), int(stage is not None), float(stage.alpha) if stage is not None else 0.0,
+                N.ptr(off), int(bool(check)), N.ptr(r_w), N.ptr(r_tr), N.ptr(r_q))
         i0, i1 = self.part.interior
         rc = d._lib.mhdg_residual_range(d._ctx, N.ptr(w), N.ptr(tr), *args, i0, i1, 1,
                                         N.stream_handle())
@@ -117,7 +118,7 @@ class PartitionedDiscretization:
             st = N.Status()
             N.raise_for(d._lib.mhdg_status_fetch(d._ctx, C.byref(st), N.stream_handle()), st)
         self.exchange.reduce_partials(r_tr)
-        return ResidualSet(r_w, r_tr, None, _disc=self)
+        return ResidualSet(r_w, r_tr, r_q, _disc=self)
 
     def jacobian(self, fields, stage=None, ptc_weight=0.0):
         return PartitionedLinearizedSystem(self, self._fields(fields), stage, ptc_weight)

@@ -116,8 +116,8 @@ def test_macro_range_entry_points_bitwise(p):
     r_w, r_tr = torch.empty_like(wd), torch.empty_like(td)
     cuts = [(E // 3, 2 * E // 3), (0, E // 3), (2 * E // 3, E)]
     for i, (a, b) in enumerate(cuts):
-        rc = lib.mhdg_residual_range(ctx, N.ptr(wd), N.ptr(td), 1, alpha, N.ptr(od), 1, N.ptr(r_w),
-                                     N.ptr(r_tr), a, b, int(i == 0), N.stream_handle())
+        rc = lib.mhdg_residual_range(ctx, N.ptr(wd), N.ptr(td), None, 1, alpha, N.ptr(od), 1,
+                                     N.ptr(r_w), N.ptr(r_tr), None, a, b, int(i == 0), N.stream_handle())
         assert rc == 0
     y2 = torch.empty_like(xd)
     buf = C.byref(lin._buf)
@@ -128,4 +128,59 @@ def test_macro_range_entry_points_bitwise(p):
     assert lib.mhdg_matvec_range(ctx, buf, N.ptr(xd), N.ptr(y2), a0, b0, 2, 0, N.stream_handle()) == 0
     torch.cuda.synchronize()
     assert torch.equal(r_w, res.r_w) and torch.equal(r_tr, res.r_trace)
+    assert torch.equal(y2, y)
+
+
+def test_macro_range_entry_points_bitwise_viscous():
+    """As above for a viscous context (KEPES, config-4 parameters): the range
+    residual returns r_w / r_trace / r_q and the range matvec the viscous
+    condensed operator, bit for bit against the whole-range calls."""
+    import torch
+
+    from paper_2507_22195_b200 import (Discretization, DissipationSpec, GasModel, StageContext,
+                                       ViscousParams)
+    from paper_2507_22195_b200 import _native as N
+    from paper_2507_22195_b200.assembly import FieldSet
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    gas = GasModel(1.4)
+    mesh = build_box_macro_mesh(np.array([[0.0, 1.0]] * 3), (3, 2, 2), 1)
+    disc = Discretization(mesh, p=3, gas=gas, flux=DissipationSpec("kepes"),
+                          viscosity=ViscousParams(16000.0, 0.1, 0.71, 1.0), device="cuda:0")
+    t = disc.tables
+    rng = np.random.default_rng(5)
+    E, nc, F, nt = mesh.n_macros, t.layout.n_unique, t.n_faces, t.n_trace
+
+    def st(n):
+        return gas.entropy_vars(gas.conservative(rng.uniform(0.9, 1.1, n),
+                                                 rng.uniform(-0.5, 0.5, (n, 3)),
+                                                 rng.uniform(0.9, 1.1, n)))
+
+    f = FieldSet(st(E * nc).reshape(E, nc, 5), st(F * nt).reshape(F, nt, 5))
+    f.q = disc.solve_gradient(f)
+    alpha = 150.0
+    off = -alpha * disc.volume_quad_states(f)
+    stage = StageContext(alpha=alpha, offset=off)
+    res = disc.residuals(f, stage)
+    lin = disc.jacobian(f, stage, ptc_weight=1.0)
+    xd = torch.as_tensor(rng.standard_normal((F, nt, 5)), device="cuda:0")
+    y = lin.matvec(xd)
+    lib, ctx = disc._lib, disc._ctx
+    wd, td = disc._fields(f)
+    qd, od = disc._q(f), disc._dev(off)
+    r_w, r_tr, r_q = torch.empty_like(wd), torch.empty_like(td), torch.empty_like(qd)
+    cuts = [(E // 3, 2 * E // 3), (0, E // 3), (2 * E // 3, E)]
+    for i, (a, b) in enumerate(cuts):
+        assert lib.mhdg_residual_range(ctx, N.ptr(wd), N.ptr(td), N.ptr(qd), 1, alpha, N.ptr(od), 1,
+                                       N.ptr(r_w), N.ptr(r_tr), N.ptr(r_q), a, b, int(i == 0),
+                                       N.stream_handle()) == 0
+    y2 = torch.empty_like(xd)
+    buf = C.byref(lin._buf)
+    (a0, b0), (a1, b1), (a2, b2) = cuts
+    assert lib.mhdg_matvec_range(ctx, buf, N.ptr(xd), N.ptr(y2), a0, b0, 1, 1, N.stream_handle()) == 0
+    assert lib.mhdg_matvec_range(ctx, buf, N.ptr(xd), N.ptr(y2), a1, b1, 3, 0, N.stream_handle()) == 0
+    assert lib.mhdg_matvec_range(ctx, buf, N.ptr(xd), N.ptr(y2), a2, b2, 3, 0, N.stream_handle()) == 0
+    assert lib.mhdg_matvec_range(ctx, buf, N.ptr(xd), N.ptr(y2), a0, b0, 2, 0, N.stream_handle()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(r_w, res.r_w) and torch.equal(r_tr, res.r_trace) and torch.equal(r_q, res.r_q)
     assert torch.equal(y2, y)
