@@ -21,8 +21,10 @@ global mesh is n*N x n x n cells (N x-slabs of the config-2 mesh, weak
 scaling), every rank runs the partitioned operator (local kernels + trace
 halo exchange of partial face sums / ghost values over NCCL + all-reduced
 dots), and value = all ranks' DoF-applications / the max-over-ranks device
-time.  --replicas keeps the older independent-replica mode.  Rank 0 prints
-the JSON line.
+time.  The halo exchange runs asynchronously, overlapped with the interior
+macros' kernels.  --replicas keeps the older independent-replica mode.
+Both modes also time one implicit DIRK(3,3) step (`implicit_step`, max over
+ranks; --no-implicit skips it).  Rank 0 prints the JSON line.
 """
 
 from __future__ import annotations
