@@ -220,8 +220,11 @@ struct GJLA2 {
   static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 8 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
 };
 
+#ifndef MHDG_GJ_MINB_SMALL
+#define MHDG_GJ_MINB_SMALL 6   // face blocks: 6 CTAs / SM (measured best)
+#endif
 template <int N, int NWT, int NPW>
-__global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, 2)
+__global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, (N < 64 ? MHDG_GJ_MINB_SMALL : 2))
 k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
   using L = GJLA2<N, NWT, NPW>;
   constexpr int NP = L::NP, S = L::S, T = L::T, NPAN = L::NPAN, RPL = L::RPL, NT = L::NT;
