@@ -2,6 +2,7 @@
 import argparse
 import json
 import math
+import os
 import sys
 import time
 
@@ -18,6 +19,15 @@ from paper_2507_22195_b200.assembly import StageContext  # noqa: E402
 from paper_2507_22195_b200.cases import TaylorGreen  # noqa: E402
 from paper_2507_22195_b200.mesh import build_box_macro_mesh  # noqa: E402
 from paper_2507_22195_b200 import solver as S  # noqa: E402
+
+if os.environ.get("SOLVER_FILE"):  # A/B another solver.py
+    import importlib.util
+
+    _spec = importlib.util.spec_from_file_location("paper_2507_22195_b200._solver_ab",
+                                                   os.environ["SOLVER_FILE"])
+    S = importlib.util.module_from_spec(_spec)
+    sys.modules[_spec.name] = S
+    _spec.loader.exec_module(S)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=16)
