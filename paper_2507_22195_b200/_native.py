@@ -139,17 +139,28 @@ def require_cuda():
 
 
 def ptr(t):
-    return None if t is None else C.c_void_p(t.data_ptr())
+    # plain ints: every pointer parameter is declared c_void_p, so ctypes
+    # converts without a wrapper object per argument
+    return None if t is None else t.data_ptr()
 
 
 def np_ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def stream_handle():
-    import torch
+_raw_stream = None
 
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+def stream_handle():
+    """Raw cudaStream_t of the current device's current stream (the cheap
+    torch binding: this is called once per kernel-level entry point)."""
+    global _raw_stream
+    if _raw_stream is None:
+        import torch
+
+        get, dev = torch._C._cuda_getCurrentRawStream, torch._C._cuda_getDevice
+        _raw_stream = lambda: get(dev())  # noqa: E731
+    return _raw_stream()
 
 
 def raise_for(code, st=None, context=""):

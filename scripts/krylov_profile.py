@@ -84,4 +84,23 @@ pc = lambda v: lin.apply_preconditioner(v.view(shape)).view(-1)
 out["inner20_ms"] = timeit(lambda: S.fgmres(op, b, precond=pc, rel_tol=1e-30, restart=20,
                                            max_iters=20, raise_on_stagnation=False, vec=vec),
                            reps=5)
+
+
+def host_us(fn, reps=50):
+    """Host-side cost per call while the GPU queue is kept full."""
+    fn()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(2_000_000_000)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    return (t1 - t0) / reps * 1e6
+
+
+out["host_us"] = {"matvec": host_us(lambda: lin.matvec(x)),
+                  "precond": host_us(lambda: lin.apply_preconditioner(x)),
+                  "combine": host_us(lambda: vec.combine(V, 10, np.ones(10), w), reps=20),
+                  "div_into": host_us(lambda: vec.div_into(w, 2.0, V[0]))}
 print(json.dumps(out))
