@@ -608,7 +608,19 @@ static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
                                  const int* tidx_rem, const double* area_rem, cudaStream_t s) {
   size_t smem = PreSmem<P, NT>::bytes;
   constexpr int NB = Dims<P>::NB;
-  if constexpr (true) {   // assemble, then the blocked tensor-core Gauss-Jordan
+#ifndef MHDG_PRECOND_FUSED
+#define MHDG_PRECOND_FUSED 1
+#endif
+  if constexpr (MHDG_PRECOND_FUSED != 0) {   // assembled inside the Gauss-Jordan CTA
+    constexpr int NWT = NB >= 64 ? MHDG_GJ_NWT : MHDG_GJ_NWT_SMALL;
+    constexpr int NPW = NB >= 64 ? MHDG_GJ_NPW : MHDG_GJ_NPW_SMALL;
+    const size_t fsm = (GJLA2<NB, NWT, NPW>::bytes + 15) / 16 * 16 + FaceBlockSrc<P, 32 * NWT>::extra_bytes;
+    if (set_smem(k_precond_gj<P, NWT, NPW>, fsm)) return MHDG_CUDA_ERROR;
+    k_precond_gj<P, NWT, NPW><<<grid_for(c, c->n_owned, occ(k_precond_gj<P, NWT, NPW>, 32 * NWT, fsm)), 32 * NWT,
+                                fsm, s>>>(c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv,
+                                          c->d_status + 1, c->d_unsym);
+    c->launches++;
+  } else if constexpr (true) {   // assemble, then the blocked tensor-core Gauss-Jordan
     if (set_smem(k_precond_factor<P, NT, false>, smem)) return MHDG_CUDA_ERROR;
     int per_sm = occ(k_precond_factor<P, NT, false>, NT, smem);
     k_precond_factor<P, NT, false><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(

@@ -223,9 +223,31 @@ struct GJLA2 {
 #ifndef MHDG_GJ_MINB_SMALL
 #define MHDG_GJ_MINB_SMALL 6   // face blocks: 6 CTAs / SM (measured best)
 #endif
-template <int N, int NWT, int NPW>
-__global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, (N < 64 ? MHDG_GJ_MINB_SMALL : 2))
-k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
+// Matrix sources for the lookahead Gauss-Jordan: load(m, A, S, ...) fills the
+// N x N block of working matrix A (row stride S, padding untouched) for item
+// m; every thread of the CTA calls it.  The inverse is written to mats[m].
+template <int N>
+struct GjGlobalSrc {   // the matrix is read from mats[m] and overwritten
+  static constexpr size_t extra_bytes = 0;
+  const double* mats;
+  __device__ __forceinline__ void init(double*, int, int) const {}
+  __device__ __forceinline__ void load(int m, double* A, int S, double*, double*, int tid, int NT) const {
+    const double* M = mats + (size_t)m * N * N;
+    if constexpr (N % 2 == 0) {
+      const double2* M2 = reinterpret_cast<const double2*>(M);
+      for (int i = tid; i < N * N / 2; i += NT) {
+        const int rr = (2 * i) / N, c = (2 * i) % N;
+        *reinterpret_cast<double2*>(A + rr * S + c) = __ldcs(M2 + i);
+      }
+    } else {
+      for (int i = tid; i < N * N; i += NT) A[(i / N) * S + i % N] = __ldcs(M + i);
+    }
+  }
+};
+
+template <int N, int NWT, int NPW, class Src>
+__device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats, unsigned long long* status,
+                                            const Src& src) {
   using L = GJLA2<N, NWT, NPW>;
   constexpr int NP = L::NP, S = L::S, T = L::T, NPAN = L::NPAN, RPL = L::RPL, NT = L::NT;
   extern __shared__ __align__(16) double smem[];
@@ -365,18 +387,12 @@ k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
     }
   };
 
+  double* ex = smem + (L::bytes + 15) / 16 * 2;   // the source's scratch
+  src.init(ex, tid, NT);
   for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
     double* M = mats + (size_t)m * N * N;
     __syncthreads();
-    if constexpr (N % 2 == 0) {
-      const double2* M2 = reinterpret_cast<const double2*>(M);
-      for (int i = tid; i < N * N / 2; i += NT) {
-        const int rr = (2 * i) / N, c = (2 * i) % N;
-        *reinterpret_cast<double2*>(A + rr * S + c) = __ldcs(M2 + i);
-      }
-    } else {
-      for (int i = tid; i < N * N; i += NT) A[(i / N) * S + i % N] = __ldcs(M + i);
-    }
+    src.load(m, A, S, ex, Ub, tid, NT);   // Ub is free until the first panel
     if (tid == 0) *flag = 0;
     __syncthreads();
     unsigned used = 0u;
@@ -435,6 +451,141 @@ k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
     }
     if (__syncthreads_or(bad) && tid == 0) report(status, 0, 0, m);
   }
+}
+
+template <int N, int NWT, int NPW>
+__global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, (N < 64 ? MHDG_GJ_MINB_SMALL : 2))
+k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
+  gj_la2_body<N, NWT, NPW>(nmat, mats, status, GjGlobalSrc<N>{mats});
+}
+
+// K4 face blocks assembled in place (assembly.py:994-1026): the face block
+// sum_sides area_side * sum_q fw fphi_i fphi_j hh_q is built in the
+// Gauss-Jordan CTA's working matrix (same DMMA contraction and the same
+// accumulation order as k_precond_factor<.., INV = false>), so the block
+// never round-trips through HBM before its inversion.  Also counts the
+// non-symmetric blocks (the reference's Cholesky / LU choice statistic).
+template <int P, int NT>
+struct FaceBlockSrc {
+  using D = Dims<P>;
+  static constexpr int NB = D::NB, NQF = D::NQF, NFN = D::NFN;
+  static constexpr int WMT = (NFN * NFN + 7) / 8, WKS = (NQF + 3) / 4, WNT = 4;
+  // persistent tables in the extra shared memory; per-face staging in the
+  // (then idle) U panel buffers
+  static constexpr size_t extra_bytes = (size_t)(NQF * NFN + NQF + 2 * (NT / 32) + 2 + NFN) * 8;
+  static constexpr int tmp_doubles = 2 * NQF * 25;
+  Geo g;
+  const double* hh;
+  const double* hh_rem;
+  const int* tidx_rem;
+  const double* area_rem;
+  int* n_unsym;
+  __device__ __forceinline__ void init(double* ex, int tid, int nt) const {
+    double* sFP = ex;
+    double* sFw = sFP + NQF * NFN;
+    for (int i = tid; i < NQF * NFN; i += nt) sFP[i] = g.fphi[i];
+    for (int i = tid; i < NQF; i += nt) sFw[i] = g.fw[i];
+  }
+  __device__ __forceinline__ void load(int f, double* A, int S, double* ex, double* tmp, int tid, int nt) const {
+    const double* sFP = ex;
+    const double* sFw = sFP + NQF * NFN;
+    double* sHH = tmp;                                // 2 sides x NQF x 25
+    double* sRed = const_cast<double*>(sFw) + NQF;    // 2 * warps
+    double* sArea = sRed + 2 * (NT / 32);
+    int* sT = reinterpret_cast<int*>(sArea + 2);
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < NB * NB; i += nt) A[(i / NB) * S + i % NB] = 0.0;
+    // both sides staged at once; every entry of the block receives exactly
+    // one term per side (tidx is a bijection per side), so the two sides'
+    // shared-memory atomics add x + y onto a zero in either order and the
+    // block is bit-identical to the side-by-side accumulation
+    for (int side = 0; side < 2; ++side) {
+      const int st = g.fsides[f * 2 + side];
+      double* hs = sHH + side * NQF * 25;
+      int* ts = sT + side * NFN;
+      if (st >= 0) {
+        const int e = st / 4, k = st % 4;
+        for (int i = tid; i < NQF * 25; i += nt) hs[(i % NQF) * 25 + i / NQF] = hh[((size_t)st * NQF) * 25 + i];
+        for (int i = tid; i < NFN; i += nt) ts[i] = g.tidx[((size_t)e * 4 + k) * NFN + i];
+        if (tid == 0) sArea[side] = g.area[(size_t)e * 4 + k];
+      } else if (st != -1) {   // remote side of a halo face (partitioned runs)
+        const int r = -2 - st;
+        for (int i = tid; i < NQF * 25; i += nt) hs[(i % NQF) * 25 + i / NQF] = hh_rem[(size_t)r * NQF * 25 + i];
+        for (int i = tid; i < NFN; i += nt) ts[i] = tidx_rem[(size_t)r * NFN + i];
+        if (tid == 0) sArea[side] = area_rem[r];
+      }
+    }
+    __syncthreads();
+    // a warp owns whole (side, M tile) tasks: the A fragment (a table entry)
+    // of each K step feeds the four N tiles' independent accumulator chains
+    for (int task = warp; task < 2 * WMT; task += NT / 32) {
+      const int side = task & 1, mt = task >> 1;
+      if (g.fsides[f * 2 + side] == -1) continue;
+      const double* hs = sHH + side * NQF * 25;
+      const int* ts = sT + side * NFN;
+      const double area = sArea[side];
+      const int ija = mt * 8 + (lane >> 2);
+      const bool rowok = ija < NFN * NFN;
+      const int ia = rowok ? ija / NFN : 0, ja = rowok ? ija % NFN : 0;
+      double c[WNT][2];
+#pragma unroll
+      for (int ntl = 0; ntl < WNT; ++ntl) c[ntl][0] = c[ntl][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < WKS; ++ks) {
+        const int qa = ks * 4 + (lane & 3);
+        const double a = (rowok && qa < NQF) ? (sFw[qa] * sFP[qa * NFN + ia]) * sFP[qa * NFN + ja] : 0.0;
+#pragma unroll
+        for (int ntl = 0; ntl < WNT; ++ntl) {
+          const int n = ntl * 8 + (lane >> 2);
+          const double b = (qa < NQF && n < 25) ? hs[qa * 25 + n] : 0.0;
+          dmma_8x8x4(c[ntl], a, b);
+        }
+      }
+      if (rowok) {
+        const int rb = ts[ia] * 5, cb = ts[ja] * 5;
+#pragma unroll
+        for (int ntl = 0; ntl < WNT; ++ntl)
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int st2 = ntl * 8 + (lane & 3) * 2 + h2;
+            if (st2 < 25) atomicAdd(&A[(rb + st2 / 5) * S + cb + st2 % 5], area * c[ntl][h2]);
+          }
+      }
+    }
+    __syncthreads();
+    double amax = 0.0, dmax = 0.0;
+    for (int idx = tid; idx < NB * NB; idx += nt) amax = fmax(amax, fabs(A[(idx / NB) * S + idx % NB]));
+    // |a_rc - a_cr| along the diagonals c - r = d: the lanes of a warp walk
+    // one diagonal, so both reads stride S + 1 (no bank conflicts)
+    for (int d = 1 + warp; d < NB; d += NT / 32)
+      for (int r = lane; r < NB - d; r += 32) dmax = fmax(dmax, fabs(A[r * S + r + d] - A[(r + d) * S + r]));
+    for (int off = 16; off > 0; off >>= 1) {
+      amax = fmax(amax, __shfl_down_sync(0xffffffffu, amax, off));
+      dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, off));
+    }
+    if (lane == 0) {
+      sRed[warp] = amax;
+      sRed[NT / 32 + warp] = dmax;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < NT / 32; ++w) {
+        amax = fmax(amax, sRed[w]);
+        dmax = fmax(dmax, sRed[NT / 32 + w]);
+      }
+      if (!(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
+    }
+  }
+};
+
+template <int P, int NWT, int NPW>
+__global__ void __launch_bounds__(32 * NWT, (Dims<P>::NB < 64 ? MHDG_GJ_MINB_SMALL : 2))
+k_precond_gj(Geo g, int n_faces, const double* __restrict__ hh, const double* __restrict__ hh_rem,
+             const int* __restrict__ tidx_rem, const double* __restrict__ area_rem, double* __restrict__ pinv,
+             unsigned long long* status, int* n_unsym) {
+  static_assert(FaceBlockSrc<P, 32 * NWT>::tmp_doubles <= 2 * GJLA2<Dims<P>::NB, NWT, NPW>::UF, "staging");
+  gj_la2_body<Dims<P>::NB, NWT, NPW>(n_faces, pinv, status,
+                                     FaceBlockSrc<P, 32 * NWT>{g, hh, hh_rem, tidx_rem, area_rem, n_unsym});
 }
 
 }  // namespace mhdg
