@@ -14,6 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from helpers import CPUVectors
 from paper_2507_22195_b200.mesh import build_box_macro_mesh
 from paper_2507_22195_b200.partition import LocalPartition, TorchDistExchange
 from paper_2507_22195_b200.tables import HDGTables
@@ -71,41 +72,6 @@ def _free_port():
     port = s.getsockname()[1]
     s.close()
     return port
-
-
-class CPUVectors:
-    """Test double of the device vector kernels (torch CPU ops)."""
-
-    def __init__(self):
-        self.torch = torch
-
-    def dot_into(self, x, y, out):
-        out[0] = torch.dot(x, y)
-
-    def norm(self, x):
-        return float(torch.linalg.vector_norm(x))
-
-    def div_into(self, x, a, out):
-        out.copy_(x / a)
-
-    def axpby(self, a, x, b, y, out):
-        out.copy_(a * x + b * y)
-
-    def axpy_dev(self, a, x, y):
-        y.sub_(a[0] * x)
-
-    def combine(self, Z, k, yv, x):
-        x.add_(torch.from_numpy(np.ascontiguousarray(yv[:k])) @ Z[:k])
-
-    def mgs(self, V, j, w):
-        h = np.zeros(j + 2)
-        for i in range(j + 1):
-            h[i] = float(V[i] @ w)
-            w.sub_(h[i] * V[i])
-        h[j + 1] = float(torch.linalg.vector_norm(w))
-        if h[j + 1] > 1e-300:
-            V[j + 1].copy_(w / h[j + 1])
-        return h
 
 
 def _states(gas, rng, n):
