@@ -99,3 +99,28 @@ def test_face_block_preconditioner_reduces_iterations(cuda_ok):
     # the condition number times that
     xr = (pre.x - plain.x).abs().max() / pre.x.abs().max()
     assert not plain.converged or float(xr) <= 1e-4
+
+
+def test_ptc_weight_shifts_alpha_and_damps_trace(cuda_ok):
+    """ptc_weight adds to alpha inside the local blocks and contributes a
+    trace damping that is linear in the weight and absent from recovery
+    (the reference's test_assembly.py:374-394)."""
+    import torch
+
+    from paper_2507_22195_b200.assembly import StageContext
+
+    case, disc = _disc()
+    f = disc.project(case.initial)
+    lin_a = disc.jacobian(f, StageContext(alpha=1.0, dt=0.1), ptc_weight=0.7)
+    lin_b = disc.jacobian(f, StageContext(alpha=1.7, dt=0.1))
+    lin_c = disc.jacobian(f, StageContext(alpha=0.3, dt=0.1), ptc_weight=1.4)
+    x = torch.from_numpy(np.random.default_rng(1).standard_normal(lin_a.trace_shape)).cuda()
+    ya, yb, yc = lin_a.matvec(x), lin_b.matvec(x), lin_c.matvec(x)
+    scale = max(1.0, float(yb.abs().max()))
+    damp = ya - yb
+    assert float(damp.abs().max()) > 1e-3 * scale
+    assert float(((yc - yb) - 2.0 * damp).abs().max()) <= 1e-11 * scale
+    res = disc.residuals(f, StageContext(alpha=1.0, dt=0.1))
+    dw_a, _ = lin_a.recover(res, x)
+    dw_b, _ = lin_b.recover(res, x)
+    assert float((dw_a - dw_b).abs().max()) <= 1e-12 * max(1.0, float(dw_b.abs().max()))
