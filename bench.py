@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--ncells", type=int, default=16, help="cells per axis (config 2: 16)")
     ap.add_argument("--p", type=int, default=3)
     ap.add_argument("--flux", default="es")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-implicit", action="store_true", help="skip the implicit-step timing")
     ap.add_argument("--cpu-sample-n", type=int, default=4)
@@ -351,6 +351,21 @@ def run_b200(args, rank, local_rank, world):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     e2e_value = world * per_step * args.e2e_steps / (e2e_ms * 1e-3)
+    # the host link's own pinned H2D rate: the e2e pipeline is bound by the
+    # step's upload, so this is its roofline
+    probe_h = torch.empty(h2d // 8, dtype=torch.float64).pin_memory()
+    probe_d = torch.empty(h2d // 8, dtype=torch.float64, device=dev)
+    probe_d.copy_(probe_h, non_blocking=True)
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s_in):
+        p0.record(s_in)
+        for _ in range(5):
+            probe_d.copy_(probe_h, non_blocking=True)
+        p1.record(s_in)
+    torch.cuda.synchronize()
+    h2d_link_gbs = 5 * h2d / (p0.elapsed_time(p1) * 1e-3) / 1e9
+    del probe_h, probe_d
 
     # ---- roofline of each kernel; dominant one in the headline
     peaks = {}
@@ -449,7 +464,9 @@ def run_b200(args, rank, local_rank, world):
                              % (8 * E * NM * NM / 1e9)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                    "pipeline": "H2D / compute / D2H on three streams, double-buffered"},
+                    "pipeline": "H2D / compute / D2H on three streams, double-buffered",
+                    "h2d_link_gbs": h2d_link_gbs,
+                    "frac_of_link": (h2d / h2d_link_gbs / 1e9) / (e2e_ms * 1e-3 / args.e2e_steps)},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "kernels": kern,
