@@ -532,8 +532,8 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
   size_t smem = Lin2<P>::bytes;
   if (c->visc) {
     if (set_smem(k_linearize2<P, true>, smem)) return MHDG_CUDA_ERROR;
-    int grid = grid_for(c, c->E, occ(k_linearize2<P, true>, 256, smem));
-    k_linearize2<P, true><<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat,
+    int grid = grid_for(c, c->E, occ(k_linearize2<P, true>, Lin2<P>::NT, smem));
+    k_linearize2<P, true><<<grid, Lin2<P>::NT, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat,
                                                   L->hh, c->d_status);
     const size_t csm = SCorr2<P>::bytes;
     if (set_smem(k_visc_scorr2<P>, csm)) return MHDG_CUDA_ERROR;
@@ -544,8 +544,8 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
   } else {
     auto go = [&](auto kern) -> int {
       if (set_smem(kern, smem)) return MHDG_CUDA_ERROR;
-      int grid = grid_for(c, c->E, occ(kern, 256, smem));
-      kern<<<grid, 256, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat, L->hh,
+      int grid = grid_for(c, c->E, occ(kern, Lin2<P>::NT, smem));
+      kern<<<grid, Lin2<P>::NT, smem, s>>>(c->geo, c->vg, w, q, tr, weight, ptc, L->sinv, L->hw, L->hhat, L->hh,
                                    c->d_status);
       return MHDG_OK;
     };

@@ -966,10 +966,13 @@ __device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, doub
 //   faces     : hw/hhat/hh tensors + face blocks of S (as in v1)
 //   inverse   : k_gj_blocked (mhdg_gj_blocked.cuh), implicit pivoting
 // ===========================================================================
+#ifndef MHDG_LIN2_NW
+#define MHDG_LIN2_NW 8   // 10 warps (whole dual passes) measured slower: 168-register cap spills
+#endif
 template <int P>
 struct Lin2 {
   using D = Dims<P>;
-  static constexpr int NW = 8, NT = 256;
+  static constexpr int NW = MHDG_LIN2_NW, NT = 32 * NW;
   static constexpr int NNP = (D::NN + 7) / 8 * 8;      // padded nodes
   static constexpr int IT = NNP / 8;                    // node tiles
   static constexpr int QC = 8;                          // q chunk (2 k-steps)
@@ -988,7 +991,7 @@ struct Lin2 {
 };
 
 template <int P, bool VISC, int FK = -1>   // FK: flux kind fixed at compile time (-1: run time)
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(32 * MHDG_LIN2_NW, 1)
 k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __restrict__ qn,
              const double* __restrict__ trace, double weight,
              double ptc, double* __restrict__ sinv, double* __restrict__ hw_out,

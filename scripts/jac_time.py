@@ -6,7 +6,7 @@ from paper_2507_22195_b200.cases import TaylorGreen
 from paper_2507_22195_b200.mesh import build_box_macro_mesh
 gas = GasModel(1.4); case = TaylorGreen(mach=0.1, gas=gas)
 mesh = build_box_macro_mesh(case.box, int(os.environ.get("JAC_N", 16)), 1)
-disc = Discretization(mesh, p=3, gas=gas, flux=DissipationSpec("kepes"), device="cuda:0")
+disc = Discretization(mesh, p=3, gas=gas, flux=DissipationSpec(os.environ.get("JAC_FLUX", "kepes")), device="cuda:0")
 f = disc.project(case.initial); alpha = 0.4358665215 / 0.57
 stage = StageContext(alpha=alpha, offset=-alpha * disc.volume_quad_states(f))
 lin = disc.jacobian(f, stage, ptc_weight=1.0); del lin; torch.cuda.synchronize()
