@@ -220,6 +220,9 @@ struct GJLA2 {
   static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 8 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
 };
 
+#ifndef MHDG_GJ_FASTRCP
+#define MHDG_GJ_FASTRCP 1
+#endif
 #ifndef MHDG_GJ_MINB_SMALL
 #define MHDG_GJ_MINB_SMALL 6   // face blocks: 6 CTAs / SM (measured best)
 #endif
@@ -343,7 +346,11 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
         }
         const double piv = prow[t];
         if (!(fabs(piv) > 0.0) || !isfinite(piv)) ok = false;
+        #if MHDG_GJ_FASTRCP
+        const double pinv = drcp(piv);   // branch-free reciprocal on the pivot chain
+#else
         const double pinv = 1.0 / piv;
+#endif
 #pragma unroll
         for (int j = 0; j < 8; ++j) prow[j] = (j == t ? 1.0 : prow[j]) * pinv;
 #pragma unroll
