@@ -220,6 +220,9 @@ struct GJLA2 {
   static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 8 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
 };
 
+#ifndef MHDG_GJ_TILE_STORE
+#define MHDG_GJ_TILE_STORE 1
+#endif
 #ifndef MHDG_GJ_FASTRCP
 #define MHDG_GJ_FASTRCP 1
 #endif
@@ -441,6 +444,24 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
     for (int k = tid; k < N; k += NT) qi[q[k]] = k;
     __syncthreads();
     int bad = *flag;
+#if MHDG_GJ_TILE_STORE
+    // column-major inverse in 4-row x 8-column tiles per warp: the gathered
+    // rows q[r] / columns qi[c] spread over the banks (a column walk hits
+    // only the two bank pairs of the row stride S = 8 mod 16), and each
+    // column's 4 rows are one 32-byte sector of the output
+    {
+      constexpr int RT = (N + 3) / 4, CT = (N + 7) / 8;
+      const int r4 = lane & 3, c8 = lane >> 2;
+      for (int t = warp; t < RT * CT; t += NT / 32) {
+        const int r = (t % RT) * 4 + r4, c = (t / RT) * 8 + c8;
+        if (r < N && c < N) {
+          const double v = A[q[r] * S + qi[c]];
+          bad |= !isfinite(v);
+          M[(size_t)c * N + r] = v;
+        }
+      }
+    }
+#else
     if constexpr (N % 2 == 0) {
       double2* M2 = reinterpret_cast<double2*>(M);
       for (int i = tid; i < N * N / 2; i += NT) {
@@ -456,6 +477,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
         M[i] = v;
       }
     }
+#endif
     if (__syncthreads_or(bad) && tid == 0) report(status, 0, 0, m);
   }
 }
