@@ -210,10 +210,20 @@ namespace mhdg {
 // warps.  A pivot step's dependent chain shortens with the rows per lane
 // (measured ~1100 cycles at 4 rows / lane, ~480 at 2).
 // ===========================================================================
+#ifndef MHDG_GJ_STRIDE2
+#define MHDG_GJ_STRIDE2 0   // measured slower (18.57 vs 18.42 ms): the C-tile accesses lose more
+#endif
 template <int N, int NWT, int NPW>
 struct GJLA2 {
   using G = GJB<N>;
+  // row stride S = 2 (mod 4) doubles: the panel warps' row-per-lane loads /
+  // stores and the permuted gathers then spread over 8 bank pairs instead of
+  // the 2 of a stride = 8 (mod 16); even, so the double2 C tiles stay aligned
+#if MHDG_GJ_STRIDE2
+  static constexpr int NP = G::NP, S = G::NP + 2, T = G::T, NPAN = G::NPAN;
+#else
   static constexpr int NP = G::NP, S = G::S, T = G::T, NPAN = G::NPAN;
+#endif
   static constexpr int RPL = (NP + 32 * NPW - 1) / (32 * NPW);
   static constexpr int NT = 32 * NWT;
   static constexpr int UF = T * 2 * 32;
