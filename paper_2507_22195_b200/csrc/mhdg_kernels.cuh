@@ -966,6 +966,12 @@ __device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, doub
 //   faces     : hw/hhat/hh tensors + face blocks of S (as in v1)
 //   inverse   : k_gj_blocked (mhdg_gj_blocked.cuh), implicit pivoting
 // ===========================================================================
+#ifndef MHDG_LIN2_PAD
+#define MHDG_LIN2_PAD 1
+#endif
+// C row kk rotated by 8 columns for odd kk: the stage-1 B-fragment loads of
+// the four kk rows then hit two bank pairs per lane octet instead of one
+#define LIN2_CI(kk, col) ((kk) * CS + (MHDG_LIN2_PAD ? (((col) + 8 * ((kk) & 1)) & 31) : (col)))
 #ifndef MHDG_LIN2_NW
 #define MHDG_LIN2_NW 8   // 10 warps (whole dual passes) measured slower: 168-register cap spills
 #endif
@@ -978,12 +984,16 @@ struct Lin2 {
   static constexpr int QC = 8;                          // q chunk (2 k-steps)
   static constexpr int NCH = (D::NQ + QC - 1) / QC;
   static constexpr int CS = 32;                          // C row (st padded)
+  // D row stride (doubles): NNP + 4, so the stage-1 stores of the four
+  // (lane & 3) st columns and the stage-2 loads of the four q rows fall on
+  // distinct bank pairs (NNP = 0 mod 8 put all four on one)
+  static constexpr int DS = MHDG_LIN2_PAD ? NNP + 4 : NNP;
   static constexpr int NPAIR = 25 * IT;                  // (st, i-tile) pairs
   static constexpr int PPW = (NPAIR + NW - 1) / NW;      // pairs per warp
   // shared memory (doubles)
   static constexpr int S_ = D::NM * D::NM;
   static constexpr int C_ = D::NQ * 4 * CS;
-  static constexpr int DD_ = QC * 25 * NNP;
+  static constexpr int DD_ = QC * 25 * DS;
   static constexpr int doubles = S_ + C_ + DD_ + D::NN * 5 + 4 * D::NFN * 5 + 4 * D::NQF * D::FS +
                                  D::NQF * D::FS + D::NQ + D::NQF + 4 * D::NQF * 25 + 4 * D::NM + 32;
   static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + 2 * D::NM + 4;
@@ -1003,7 +1013,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
   extern __shared__ __align__(16) double smem[];
   double* S = smem;                          // NM*NM
   double* sC = S + L::S_;                    // NQ*4*CS
-  double* sD = sC + L::C_;                   // QC*25*NNP   [qq][st][i]
+  double* sD = sC + L::C_;                   // QC*25*DS   [qq][st][i]
   double* sW = sD + L::DD_;                  // NN*5
   double* sTR = sW + NN * 5;                 // 4*NFN*5
   double* sPF = sTR + 4 * NFN * 5;           // 4*NQF*FS
@@ -1101,10 +1111,10 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
 #pragma unroll
         for (int s2 = 0; s2 < 5; ++s2)
-          C[kk * CS + s2 * 5 + t] = -(vw * ((j0 * F[s2][0].d + j1 * F[s2][1].d) + j2 * F[s2][2].d));
+          C[LIN2_CI(kk, s2 * 5 + t)] = -(vw * ((j0 * F[s2][0].d + j1 * F[s2][1].d) + j2 * F[s2][2].d));
       }
 #pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) C[3 * CS + s2 * 5 + t] = weight * (vw * ud[s2].d);
+      for (int s2 = 0; s2 < 5; ++s2) C[LIN2_CI(3, s2 * 5 + t)] = weight * (vw * ud[s2].d);
     }
     __syncthreads();
     LIN_T(1);
@@ -1126,13 +1136,13 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           const double a = (q < NQ && i < NN) ? __ldg(Bt + ((size_t)q * 4 + kk) * NN + i) : 0.0;
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
-            const double b = q < NQ ? sC[(size_t)q * 4 * CS + kk * CS + nt * 8 + r8] : 0.0;
+            const double b = q < NQ ? sC[(size_t)q * 4 * CS + LIN2_CI(kk, nt * 8 + r8)] : 0.0;
             double c2[2] = {0.0, 0.0};
             dmma_8x8x4(c2, a, b);
             const int ii = itl * 8 + r8, st0 = nt * 8 + (lane & 3) * 2;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              if (st0 + h < 25) sD[((size_t)qq * 25 + st0 + h) * NNP + ii] = c2[h];
+              if (st0 + h < 25) sD[((size_t)qq * 25 + st0 + h) * L::DS + ii] = c2[h];
           }
         }
       }
@@ -1152,7 +1162,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           const int pr = warp + L::NW * c;
           if (pr < L::NPAIR) {
             const int st = pr / IT, itl = pr % IT;
-            const double a = sD[((size_t)qq * 25 + st) * NNP + itl * 8 + (lane >> 2)];
+            const double a = sD[((size_t)qq * 25 + st) * L::DS + itl * 8 + (lane >> 2)];
 #pragma unroll
             for (int jt = 0; jt < IT; ++jt) dmma_8x8x4(acc[c][jt], a, bf[jt]);
           }
