@@ -969,9 +969,9 @@ __device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, doub
 #ifndef MHDG_LIN2_PAD
 #define MHDG_LIN2_PAD 1
 #endif
-// C row kk rotated by 8 columns for odd kk: the stage-1 B-fragment loads of
-// the four kk rows then hit two bank pairs per lane octet instead of one
-#define LIN2_CI(kk, col) ((kk) * CS + (MHDG_LIN2_PAD ? (((col) + 8 * ((kk) & 1)) & 31) : (col)))
+// C row kk rotated by 4 kk columns: a half-warp's stage-1 B-fragment loads
+// (four kk rows x four columns) then hit 16 distinct bank pairs
+#define LIN2_CI(kk, col) ((kk) * CS + (MHDG_LIN2_PAD ? (((col) + 4 * (kk)) & 31) : (col)))
 #ifndef MHDG_LIN2_NW
 #define MHDG_LIN2_NW 8   // 10 warps (whole dual passes) measured slower: 168-register cap spills
 #endif
