@@ -48,7 +48,6 @@ k_gj_blocked(int nmat, double* __restrict__ mats, unsigned long long* status, do
   double* cand = R + 8 * SU;        // [2][NW][10]: |a|, row index, 8 row values
   int* q = (int*)(cand + 2 * NW * 10);
   int* qi = q + N;
-  int* flag = qi + N;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r = tid;                // this thread's panel row
   // padding rows / columns stay zero through every update (U and R vanish there)

@@ -1008,7 +1008,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
              double* __restrict__ hhat_out, double* __restrict__ hh_out, unsigned long long* status) {
   using D = Dims<P>;
   using L = Lin2<P>;
-  constexpr int NN = D::NN, NQ = D::NQ, NM = D::NM, NFN = D::NFN, NQF = D::NQF, NNP = L::NNP;
+  constexpr int NN = D::NN, NQ = D::NQ, NM = D::NM, NFN = D::NFN, NQF = D::NQF;
   constexpr int NT = L::NT, QC = L::QC, CS = L::CS, IT = L::IT;
   extern __shared__ __align__(16) double smem[];
   double* S = smem;                          // NM*NM
