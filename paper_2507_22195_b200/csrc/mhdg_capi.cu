@@ -330,6 +330,23 @@ static Geo geo_range(const Geo& g0, int e0, int e1, int nfn) {
   return g;
 }
 
+// launch with programmatic stream serialization (MHDG_PDL, see pdl_wait in
+// mhdg_kernels.cuh): the kernel may start while its producer drains
+template <typename... KA, typename... A>
+static cudaError_t launch_pdl(void (*k)(KA...), int grid, int block, size_t smem, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = MHDG_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, ((KA)args)...);
+}
+
 static int grid_for(mhdg_ctx* c, int items, int per_sm) {
   return std::max(1, std::min(items, c->n_sms * per_sm));
 }
@@ -739,18 +756,19 @@ static int condensed_face2(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, con
   const double* rwv = rw ? rw + vm : nullptr;
   if (stages & 1) {
     if (mode != 1) {
-      k_face2<P, 0><<<grid_for(c, nb, occ(k_face2<P, 0>, 128, fsm)), 128, fsm, s>>>(gv, mode, L->hhat + ten, nullptr,
-                                                                                    x, nullptr, rwv, gbuf);
+      CK(launch_pdl(k_face2<P, 0>, grid_for(c, nb, occ(k_face2<P, 0>, 128, fsm)), 128, fsm, s, gv, mode, L->hhat + ten,
+                 nullptr, x, nullptr, rwv, gbuf));
       c->launches++;
     }
     using LS = LocalSolveCfg<D::NM>;
-    k_local_solve<D::NM, LS::NT><<<grid_for(c, (E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)),
-                                   LS::NT, 0, s>>>(E, L->sinv + vm * D::NM, mode == 1 ? rwv : gbuf, mode == 1, zbuf);
+    CK(launch_pdl(k_local_solve<D::NM, LS::NT>,
+               grid_for(c, (E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)), LS::NT, 0, s, E,
+               L->sinv + vm * D::NM, mode == 1 ? rwv : gbuf, (int)(mode == 1), zbuf));
     c->launches++;
   }
   if ((stages & 2) && mode != 2) {
-    k_face2<P, 1><<<grid_for(c, nb, occ(k_face2<P, 1>, 128, fsm)), 128, fsm, s>>>(gv, mode, L->hw + ten, L->hh + ten,
-                                                                                  x, zbuf, nullptr, y);
+    CK(launch_pdl(k_face2<P, 1>, grid_for(c, nb, occ(k_face2<P, 1>, 128, fsm)), 128, fsm, s, gv, mode, L->hw + ten,
+               L->hh + ten, x, (const double*)zbuf, nullptr, y));
     c->launches++;
   }
   CK(cudaGetLastError());
@@ -885,10 +903,10 @@ extern "C" int mhdg_precond(mhdg_ctx* c, const mhdg_lin_buffers* L, const double
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
   switch (c->p) {
-    case 1: k_precond_apply<1, 32><<<grid_for(c, c->n_owned, 32), 32, 0, s>>>(c->n_owned, L->pinv, r, z); break;
-    case 2: k_precond_apply<2, 32><<<grid_for(c, c->n_owned, 32), 32, 0, s>>>(c->n_owned, L->pinv, r, z); break;
-    case 3: k_precond_apply<3, 64><<<grid_for(c, c->n_owned, 24), 64, 0, s>>>(c->n_owned, L->pinv, r, z); break;
-    default: k_precond_apply<4, 96><<<grid_for(c, c->n_owned, 16), 96, 0, s>>>(c->n_owned, L->pinv, r, z); break;
+    case 1: CK(launch_pdl(k_precond_apply<1, 32>, grid_for(c, c->n_owned, 32), 32, 0, s, c->n_owned, (const double*)L->pinv, r, z)); break;
+    case 2: CK(launch_pdl(k_precond_apply<2, 32>, grid_for(c, c->n_owned, 32), 32, 0, s, c->n_owned, (const double*)L->pinv, r, z)); break;
+    case 3: CK(launch_pdl(k_precond_apply<3, 64>, grid_for(c, c->n_owned, 24), 64, 0, s, c->n_owned, (const double*)L->pinv, r, z)); break;
+    default: CK(launch_pdl(k_precond_apply<4, 96>, grid_for(c, c->n_owned, 16), 96, 0, s, c->n_owned, (const double*)L->pinv, r, z)); break;
   }
   c->launches++;
   CK(cudaGetLastError());

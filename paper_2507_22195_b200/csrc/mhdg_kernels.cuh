@@ -20,6 +20,25 @@
 #include "mhdg_tma.cuh"
 #include "mhdg_visc_math.cuh"
 
+// Programmatic dependent launch on the condensed-matvec chain (k_face2<0> ->
+// k_local_solve -> k_face2<1>) and the face-block preconditioner: each
+// kernel launches while its producer drains, stages what does not depend on
+// it (basis tables, face metadata), then blocks in pdl_wait() until the
+// producer grid has completed and flushed.  Producers release at exit:
+// measured at config 2, matvec 0.519 -> 0.512 ms; an explicit
+// griddepcontrol.launch_dependents at each CTA's last batch was slower
+// (0.521 ms: the early dependents hold SM slots), an L2 prefetch of the first
+// S^-1 columns before the wait was neutral.  Without the launch attribute the
+// wait is a no-op.
+#ifndef MHDG_PDL
+#define MHDG_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if MHDG_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 namespace mhdg {
 
 template <int P>
@@ -1485,6 +1504,7 @@ k_local_solve(int E, const double* __restrict__ sinv, const double* __restrict__
   constexpr int MB = LocalSolveCfg<NM>::MB;
   __shared__ double sg[MB * NM];
   const int ml = threadIdx.x / NM, rr = threadIdx.x % NM;
+  pdl_wait();
   for (int e0 = blockIdx.x * MB; e0 < E; e0 += gridDim.x * MB) {
     const int nm = min(MB, E - e0);
     __syncthreads();
@@ -1637,6 +1657,7 @@ k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restri
       }
     }
   };
+  pdl_wait();
   if (e00 < g.E) prefetch(e00, 0);
   int slot = 0;
   for (int e0 = e00; e0 < g.E; e0 += G, slot = (slot + 1) % 3) {
@@ -1772,6 +1793,7 @@ k_precond_apply(int F, const double* __restrict__ pinv, const double* __restrict
                 double* __restrict__ z) {
   constexpr int NB = Dims<P>::NB;
   __shared__ double sR[NB];
+  pdl_wait();
   for (int f = blockIdx.x; f < F; f += gridDim.x) {
     __syncthreads();
     for (int i = threadIdx.x; i < NB; i += NT) sR[i] = r[(size_t)f * NB + i];
