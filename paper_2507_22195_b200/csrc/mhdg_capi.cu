@@ -796,16 +796,17 @@ static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, cons
   const double* rqv = rq ? rq + vm * 3 : nullptr;
   const int nbi = (E + V::MBI - 1) / V::MBI, nbo = (E + V::MBO - 1) / V::MBO;
   if (stages & 1) {
-    k_visc_in2<P><<<grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s>>>(gv, c->vg, mode, wlin,
-                                                                                   L->hhat + ten, x, rwv, rqv, gbuf);
+    CK(launch_pdl(k_visc_in2<P>, grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s, gv, c->vg, mode, wlin,
+                  (const double*)(L->hhat + ten), x, rwv, rqv, gbuf));
     using LS = LocalSolveCfg<D::NM>;
-    k_local_solve<D::NM, LS::NT><<<grid_for(c, (E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)),
-                                   LS::NT, 0, s>>>(E, L->sinv + vm * D::NM, gbuf, 0, zbuf);
+    CK(launch_pdl(k_local_solve<D::NM, LS::NT>,
+                  grid_for(c, (E + LS::MB - 1) / LS::MB, occ(k_local_solve<D::NM, LS::NT>, LS::NT, 0)), LS::NT, 0, s,
+                  E, (const double*)(L->sinv + vm * D::NM), (const double*)gbuf, 0, zbuf));
     c->launches += 2;
   }
   if ((stages & 2) && mode != 2) {
-    k_visc_out2<P><<<grid_for(c, nbo, occ(k_visc_out2<P>, 128, osm)), 128, osm, s>>>(
-        gv, c->vg, mode, wlin, L->hh + ten, L->hw + ten, x, zbuf, rqv, y);
+    CK(launch_pdl(k_visc_out2<P>, grid_for(c, nbo, occ(k_visc_out2<P>, 128, osm)), 128, osm, s, gv, c->vg, mode,
+                  wlin, (const double*)(L->hh + ten), (const double*)(L->hw + ten), x, (const double*)zbuf, rqv, y));
     c->launches++;
   }
   CK(cudaGetLastError());
