@@ -28,7 +28,6 @@ import math
 from dataclasses import dataclass
 
 import numpy as np
-from numpy.polynomial import legendre as npleg
 from scipy.special import roots_jacobi
 
 from .errors import InvalidConfig
@@ -94,20 +93,17 @@ def gauss_lobatto(p):
     return np.concatenate([[-1.0], np.sort(inner), [1.0]])
 
 
-def _orthonormal_legendre(n_max, x):
-    """Columns sqrt((2k+1)/2) P_k(x), k = 0..n_max."""
-    v = npleg.legvander(np.asarray(x, dtype=float), n_max)
-    return v * np.sqrt((2 * np.arange(n_max + 1) + 1) / 2.0)
-
-
 def _edge_warp(p, r):
     """Warburton's 1D warp factor: interpolant of (LGL - equispaced) at r,
     divided by the edge bubble 1-r^2 away from the end points."""
     lgl = gauss_lobatto(p)
     req = np.linspace(-1.0, 1.0, p + 1)
-    veq = _orthonormal_legendre(p, req)            # (p+1 nodes, p+1 modes)
-    pr = _orthonormal_legendre(p, r)               # (npts, p+1)
-    lag = np.linalg.solve(veq.T, pr.T)             # Lagrange values (p+1, npts)
+    # Legendre modes by the orthonormal Jacobi recurrence (the reference's
+    # evaluation, fem.py:33-66, 280-291): the numpy legvander values differ in
+    # the last bit and moved the p >= 3 facet nodes by up to 1.1e-16
+    veq = np.column_stack([jacobi_orthonormal(j, 0, 0, req) for j in range(p + 1)])
+    pr = np.vstack([jacobi_orthonormal(j, 0, 0, r) for j in range(p + 1)])   # (p+1, npts)
+    lag = np.linalg.solve(veq.T, pr)               # Lagrange values (p+1, npts)
     warp = lag.T @ (lgl - req)
     inside = (np.abs(r) < 1.0 - 1e-10).astype(float)
     bubble = 1.0 - (inside * r) ** 2

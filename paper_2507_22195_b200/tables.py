@@ -165,8 +165,12 @@ class HDGTables:
         trace_perm = np.zeros((E, d + 1, nt), dtype=np.int64)
         fids = np.arange(F)
         own_e, own_f = skel.owner, skel.owner_face
+        # origin + X @ J^T per face, as the reference's mesh.to_physical
+        # (mesh.py:115-117): a batched matmul runs the same BLAS product per
+        # face, so the coordinates (and the projected trace state) are
+        # bit-identical; an einsum here differed in the last bit at p >= 3
         own_pts = (mesh.macro_origins[own_e][:, None, :]
-                   + np.einsum("fnb,fab->fna", fun[own_f], mesh.macro_jacobians[own_e]))
+                   + np.matmul(fun[own_f], mesh.macro_jacobians[own_e].transpose(0, 2, 1)))
         self.trace_coords = own_pts                         # (F, nt, d)
         face_id[own_e, own_f] = fids
         trace_perm[own_e, own_f] = np.arange(nt)

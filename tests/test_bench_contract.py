@@ -26,7 +26,8 @@ def _run(args, timeout):
 
 @pytest.mark.timeout(600)
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-sample-n", "2"], 600)
+    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "1", "--cpu-sample-n", "2",
+              "--cpu-workers", "2"], 600)
     for k in BASE_KEYS:
         assert k in d, k
     assert d["impl"] == "reference"

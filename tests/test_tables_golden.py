@@ -1,0 +1,39 @@
+"""Host tables and index / scatter maps bit-exact against the reference.
+
+tests/golden/table_digests.json holds SHA-256 digests of every table the
+operator consumes, produced by running the reference (macrohdg) itself at
+n = 4, 8, 16 cells per axis and p = 1..4 (tests/golden/table_digests.py).
+Here the same arrays come from this package's builders (mesh.py, fem.py,
+tables.py) and must hash identically: integer maps AND float tables equal
+bit for bit (north_star "mesh and index/scatter maps
+bit-exact").
+"""
+
+import json
+import os
+
+import pytest
+
+from golden.table_digests import CASES, OUT, collect
+
+with open(OUT) as f:
+    GOLD = json.load(f)["cases"]
+
+
+def _ours(mesh, p):
+    from paper_2507_22195_b200.tables import HDGTables
+
+    return HDGTables(mesh, p)
+
+
+@pytest.mark.parametrize("n,p", CASES)
+def test_tables_bit_exact(n, p):
+    if n == 16 and os.environ.get("MHDG_QUICK"):
+        pytest.skip("MHDG_QUICK")
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    got = collect(build_box_macro_mesh, _ours, n, p)
+    want = GOLD[f"n{n}_p{p}"]
+    assert set(got) == set(want)
+    bad = {k: (got[k], want[k]) for k in want if got[k] != want[k]}
+    assert not bad, f"{len(bad)} tables differ from the reference: {sorted(bad)}"
