@@ -212,6 +212,43 @@ int mhdg_axpby(mhdg_ctx* ctx, int64_t n, double a, const double* x, double b,
 int mhdg_axpy_dev(mhdg_ctx* ctx, int64_t n, const double* a_dev,
                   const double* x, double* y, void* stream);
 
+/* Device-resident condensed solve: solver.solve_condensed (solver.py:121-170)
+ * = FGMRES(restart, rel_tol, max_outer) preconditioned by an inner
+ * GMRES(inner_iters, inner_rtol) sweep that is itself preconditioned by the
+ * face-block solve (inner_precond = 0: face-block solve only), all as one
+ * CUDA graph with conditional WHILE / IF nodes (no host round trip inside
+ * the solve).  The caller allocates the workspace (mhdg_krylov_workspace
+ * doubles of device memory).  mhdg_krylov_solve: x = solution for the
+ * condensed right-hand side b (both (F, nt, 5) device buffers); the stats
+ * are copied to `stats` at the end of the solve: sync = 1 waits for them,
+ * sync = 0 returns at once (stats must then be pinned host memory, valid once
+ * the stream reaches that point).  The graph is (re)built when `lin` differs
+ * from the previous call's buffers. */
+typedef struct {
+  double rel_tol;
+  int restart;
+  int max_outer;
+  double inner_rtol;
+  int inner_iters;
+  int inner_precond;
+} mhdg_krylov_params;
+
+typedef struct {
+  int outer_iterations;  /* SolveStats.outer_iterations */
+  int inner_iterations;  /* SolveStats.inner_iterations */
+  int converged;         /* SolveStats.converged        */
+  int updated;           /* x received a correction      */
+  double rel_residual;   /* SolveStats.rel_residual     */
+} mhdg_krylov_stats;
+
+typedef struct mhdg_krylov mhdg_krylov;
+int64_t mhdg_krylov_workspace(const mhdg_ctx* ctx, const mhdg_krylov_params* prm);
+mhdg_krylov* mhdg_krylov_create(mhdg_ctx* ctx, const mhdg_krylov_params* prm,
+                                double* workspace, int64_t workspace_len, int* err);
+int mhdg_krylov_solve(mhdg_krylov* k, const mhdg_lin_buffers* lin, const double* b,
+                      double* x, mhdg_krylov_stats* stats, int sync, void* stream);
+void mhdg_krylov_destroy(mhdg_krylov* k);
+
 /* number of library kernels launched since creation (evidence counter) */
 int64_t mhdg_launch_count(const mhdg_ctx* ctx);
 /* FP64 FMA throughput probe (roofline denominator), returns GFLOP/s */

@@ -53,6 +53,16 @@ class Tables(C.Structure):
     ]
 
 
+class KrylovParams(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("restart", C.c_int), ("max_outer", C.c_int),
+                ("inner_rtol", C.c_double), ("inner_iters", C.c_int), ("inner_precond", C.c_int)]
+
+
+class KrylovStats(C.Structure):
+    _fields_ = [("outer_iterations", C.c_int), ("inner_iterations", C.c_int),
+                ("converged", C.c_int), ("updated", C.c_int), ("rel_residual", C.c_double)]
+
+
 class LinBuffers(C.Structure):
     _fields_ = [("sinv", dptr), ("hw", dptr), ("hhat", dptr), ("hh", dptr), ("pinv", dptr),
                 ("wlin", dptr)]
@@ -96,6 +106,12 @@ _SIGS = {
                              C.c_void_p]),
     "mhdg_axpby": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, dptr, C.c_double, dptr, dptr,
                              C.c_void_p]),
+    "mhdg_krylov_workspace": (C.c_int64, [C.c_void_p, C.POINTER(KrylovParams)]),
+    "mhdg_krylov_create": (C.c_void_p, [C.c_void_p, C.POINTER(KrylovParams), dptr, C.c_int64,
+                                        C.POINTER(C.c_int)]),
+    "mhdg_krylov_solve": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, C.c_int,
+                                    C.c_void_p]),
+    "mhdg_krylov_destroy": (None, [C.c_void_p]),
     "mhdg_launch_count": (C.c_int64, [C.c_void_p]),
     "mhdg_fp64_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_dmma_probe": (C.c_double, [C.c_int, C.c_void_p]),

@@ -71,6 +71,9 @@ class ResidualSet:
     _disc: object = None
 
     def norm(self):
+        cached = self.__dict__.get("_norm")
+        if cached is not None:
+            return cached
         if self._disc is not None:
             return self._disc.residual_norm(self)
         parts = [self.r_w, self.r_trace] + ([self.r_q] if self.r_q is not None else [])
@@ -204,6 +207,11 @@ class Discretization:
         self.lin_sizes = tuple(int(s) for s in sizes)
 
     def __del__(self):
+        # device engines built on this context go first (they hold graphs
+        # with this context's buffers)
+        engines = self.__dict__.pop("_krylov_engines", None)
+        if engines:
+            engines.clear()
         ctx = getattr(self, "_ctx", None)
         if ctx:
             try:
@@ -348,6 +356,49 @@ class Discretization:
             N.ptr(r_w), N.ptr(r_tr), N.ptr(r_q), int(bool(sync)), C.byref(st), N.stream_handle())
         N.raise_for(rc, st)
         return ResidualSet(r_w=r_w, r_trace=r_tr, r_q=r_q, _disc=self)
+
+    def residual_and_norm(self, fields, stage=None):
+        """(residuals, ||R||) with ONE device round trip: the residual
+        kernels, the admissibility status and the three deterministic dot
+        products are queued, then status and dots come back together
+        (ResidualSet.norm order: r_w, r_trace, r_q).  Raises like
+        residuals()."""
+        res = self.residuals(fields, stage, check=True, sync=False)
+        parts = [res.r_w, res.r_trace] + ([res.r_q] if res.r_q is not None else [])
+        stream = N.stream_handle()
+        for i, p in enumerate(parts):
+            N.raise_for(self._lib.mhdg_dot(self._ctx, p.numel(), N.ptr(p), N.ptr(p),
+                                           N.ptr(self._scalar) + 8 * i, stream))
+        host = self.__dict__.get("_host_scalar")
+        if host is None:
+            host = self._host_scalar = _torch().zeros(8, dtype=_torch().float64).pin_memory()
+        host[: len(parts)].copy_(self._scalar[: len(parts)], non_blocking=True)
+        st = N.Status()
+        N.raise_for(self._lib.mhdg_status_fetch(self._ctx, C.byref(st), stream), st)
+        sq = host.tolist()
+        norm = math.sqrt(sum(sq[: len(parts)]))
+        res._norm = norm
+        return res, norm
+
+    def apply_update(self, fields, d_w, d_trace, d_q=None):
+        """New FieldSet w + d_w, trace + d_trace (, q + d_q) on the device
+        (library axpby, one rounding per entry like numpy's +)."""
+        torch = _torch()
+        stream = N.stream_handle()
+
+        def add(a, b):
+            a, b = self._dev(a), self._dev(b)
+            out = torch.empty_like(a)
+            N.raise_for(self._lib.mhdg_axpby(self._ctx, a.numel(), 1.0, N.ptr(a), 1.0, N.ptr(b),
+                                             N.ptr(out), stream))
+            return out
+
+        q = None
+        if d_q is not None:
+            q = add(fields.q, d_q)
+        elif fields.q is not None:
+            q = self._dev(fields.q).clone()
+        return FieldSet(add(fields.w, d_w), add(fields.trace, d_trace), q)
 
     def jacobian(self, fields, stage=None, ptc_weight=0.0, sparse_local_threshold=2048):
         return LinearizedSystem(self, fields, stage, ptc_weight)

@@ -286,9 +286,13 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
 
 extern "C" void mhdg_destroy(mhdg_ctx* c) {
   if (!c) return;
+  int cur = -1;
+  cudaGetDevice(&cur);
   cudaSetDevice(c->device);
   for (void* p : c->allocs) cudaFree(p);
   if (c->d_scratch) cudaFree(c->d_scratch);
+  if (cur >= 0) cudaSetDevice(cur);
+  cudaGetLastError();   // leave no error for the next call's cudaGetLastError
   delete c;
 }
 
@@ -1127,22 +1131,30 @@ extern "C" int mhdg_mgs(mhdg_ctx* c, int64_t n, int j, double* V, double* w, dou
   return MHDG_OK;
 }
 
+// x += Z^T y, acc summed in row order r = 0..k-1 (any k: y is staged in
+// shared memory 128 coefficients at a time, the running sum stays in the
+// same order)
 __global__ void k_combine(int64_t n, int k, const double* __restrict__ Z, const double* __restrict__ y,
                           double* __restrict__ x) {
   __shared__ double sy[128];
-  for (int i = threadIdx.x; i < k; i += blockDim.x) sy[i] = y[i];
-  __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
     double acc = 0.0;
-    for (int r = 0; r < k; ++r) acc += Z[(int64_t)r * n + i] * sy[r];
-    x[i] = x[i] + acc;
+    for (int r0 = 0; r0 < k; r0 += 128) {
+      const int kc = min(128, k - r0);
+      __syncthreads();
+      for (int t = threadIdx.x; t < kc; t += blockDim.x) sy[t] = y[r0 + t];
+      __syncthreads();
+      if (i < n)
+        for (int r = 0; r < kc; ++r) acc += Z[(int64_t)(r0 + r) * n + i] * sy[r];
+    }
+    if (i < n) x[i] = x[i] + acc;
   }
 }
 
 extern "C" int mhdg_combine(mhdg_ctx* c, int64_t n, int k, const double* Z, const double* y_dev, double* x,
                             void* stream) {
   if (k <= 0) return MHDG_OK;
-  if (k > 128) return MHDG_INVALID_CONFIG;
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
   k_combine<<<RED_BLOCKS, RED_THREADS, 0, s>>>(n, k, Z, y_dev, x);
@@ -1359,3 +1371,5 @@ extern "C" double mhdg_fp64_probe(int device, void* stream) {
   const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
   return flops / (ms * 1e-3) / 1e9;
 }
+
+#include "mhdg_krylov.cuh"

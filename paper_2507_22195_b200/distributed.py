@@ -23,8 +23,52 @@ import numpy as np
 
 from . import _native as N
 from .assembly import Discretization, LinearizedSystem, ResidualSet
+from .errors import NonAdmissibleEntropyState, NonAdmissibleState, SingularBlock, SingularLocalMatrix
 from .partition import LocalPartition, TorchDistExchange
 from .tables import HDGTables
+
+
+# status codes of the library (include/mhdg_b200.h) for the rank-local
+# failures that must be agreed on collectively
+_CODES = ((NonAdmissibleEntropyState, 2), (NonAdmissibleState, 1), (SingularLocalMatrix, 3),
+          (SingularBlock, 4))
+
+
+def _code_of(exc):
+    for cls, code in _CODES:
+        if isinstance(exc, cls):
+            return code
+    return 0
+
+
+def collective(exchange, fn, rank=0):
+    """Run the rank-local part `fn`; agree on its failure status across all
+    ranks (max of the status codes) and raise on EVERY rank if any failed:
+    the rank that saw the failure re-raises its own exception (with the
+    macro / face / location), the others raise the same class naming the
+    remote rank's failure.  The reference's NonAdmissibleState on a trial
+    state is routine (Newton shrinks tau and retries), so every rank must
+    take that branch together."""
+    exc, out = None, None
+    try:
+        out = fn()
+    except tuple(cls for cls, _ in _CODES) as e:
+        exc = e
+    mine = _code_of(exc) if exc is not None else 0
+    code = exchange.agree(mine)
+    if code == 0:
+        return out
+    if exc is not None and mine == code:
+        raise exc
+    msg = f"failure on another rank (seen from rank {rank})"
+    if code == 1:
+        raise NonAdmissibleState("non-admissible state " + msg, where="remote rank")
+    if code == 2:
+        raise NonAdmissibleEntropyState("non-positive inverse temperature " + msg,
+                                        where="remote rank")
+    if code == 3:
+        raise SingularLocalMatrix("singular condensed block " + msg)
+    raise SingularBlock("singular trace block " + msg)
 
 
 class PartitionedDiscretization:
@@ -87,7 +131,10 @@ class PartitionedDiscretization:
 
     def residuals(self, fields, stage=None, check=True, sync=True):
         if not self.overlap:
-            res = self.local.residuals(self._fields(fields), stage, check, sync=sync)
+            flds = self._fields(fields)   # ghost fill: every rank, before any failure
+            res = collective(self.exchange,
+                             lambda: self.local.residuals(flds, stage, check, sync=True),
+                             self.rank)
             self.exchange.reduce_partials(res.r_trace)
             return ResidualSet(res.r_w, res.r_trace, res.r_q, _disc=self)
         # ghost traces in flight while the interior macros run; halo macros
@@ -114,9 +161,13 @@ class PartitionedDiscretization:
             rc = d._lib.mhdg_residual_range(d._ctx, N.ptr(w), N.ptr(tr), *args, a, b, 0,
                                             N.stream_handle())
             N.raise_for(rc)
-        if sync:
+        # the status is always fetched: the admissibility verdict must be
+        # agreed on by all ranks before the partial-sum exchange
+        def status():
             st = N.Status()
             N.raise_for(d._lib.mhdg_status_fetch(d._ctx, C.byref(st), N.stream_handle()), st)
+
+        collective(self.exchange, status, self.rank)
         self.exchange.reduce_partials(r_tr)
         return ResidualSet(r_w, r_tr, r_q, _disc=self)
 
@@ -127,7 +178,7 @@ class PartitionedDiscretization:
         return self.local.volume_quad_states(fields)
 
     def to_conservative(self, w, where=""):
-        return self.local.to_conservative(w, where)
+        return collective(self.exchange, lambda: self.local.to_conservative(w, where), self.rank)
 
     def from_conservative(self, u):
         return self.local.from_conservative(u)
@@ -156,17 +207,25 @@ class PartitionedLinearizedSystem:
         q = d._q(fields)
         alpha = float(stage.alpha) if stage is not None else 0.0
         st = N.Status()
-        rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(w), N.ptr(tr), N.ptr(q), alpha,
-                                         float(ptc_weight), C.byref(lin._buf), C.byref(st),
-                                         N.stream_handle())
-        N.raise_for(rc, st)
+
+        def local():
+            rc = d._lib.mhdg_linearize_local(d._ctx, N.ptr(w), N.ptr(tr), N.ptr(q), alpha,
+                                             float(ptc_weight), C.byref(lin._buf), C.byref(st),
+                                             N.stream_handle())
+            N.raise_for(rc, st)
+
+        collective(pdisc.exchange, local, pdisc.rank)
         # ... then the owned face blocks, with halo sides from the neighbours
         hh_r, tidx_r, area_r = gather_remote_sides(pdisc, lin)
         n_rem = 0 if area_r is None else int(area_r.numel())
-        rc = d._lib.mhdg_precond_factor(d._ctx, C.byref(lin._buf), n_rem,
-                                        N.ptr(hh_r), N.ptr(tidx_r), N.ptr(area_r),
-                                        C.byref(st), N.stream_handle())
-        N.raise_for(rc, st)
+
+        def factor():
+            rc = d._lib.mhdg_precond_factor(d._ctx, C.byref(lin._buf), n_rem,
+                                            N.ptr(hh_r), N.ptr(tidx_r), N.ptr(area_r),
+                                            C.byref(st), N.stream_handle())
+            N.raise_for(rc, st)
+
+        collective(pdisc.exchange, factor, pdisc.rank)
 
     def matvec(self, xh):
         pd = self.pdisc
@@ -247,7 +306,7 @@ class DistVectors:
         self.exchange = pdisc.exchange
         t = pdisc.local.tables
         self.n_owned = pdisc.part.n_owned * t.fphi.shape[1] * 5
-        self.h = self.torch.zeros(256, dtype=self.torch.float64, device=pdisc.device)
+        self.h = self.torch.zeros(66, dtype=self.torch.float64, device=pdisc.device)
         import torch.distributed as dist
 
         part = pdisc.part
@@ -274,6 +333,8 @@ class DistVectors:
     def mgs(self, V, j, w):
         if self.single:   # one rank, no ghost rows: the fused single-device MGS
             return self.inner.mgs(V, j, w)
+        if self.h.numel() < j + 2:   # grown with the restart length (no fixed cap)
+            self.h = self.torch.zeros(2 * (j + 2), dtype=self.torch.float64, device=self.h.device)
         h = self.h
         for i in range(j + 1):
             self._dot_dev(V[i], w, h[i:i + 1])

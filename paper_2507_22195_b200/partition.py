@@ -310,6 +310,22 @@ class TorchDistExchange:
             trace_like[torch.as_tensor(ids, device=trace_like.device)] = recvs[h]
         return trace_like
 
+    def agree(self, code):
+        """Global maximum of an integer status code over the ranks (one tiny
+        all-reduce).  Every rank calls it at the same point, so a failure
+        detected on one rank is raised on all of them before the next halo
+        exchange or all-reduce (otherwise the ranks' collective sequences
+        diverge and NCCL hangs)."""
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_initialized() or dist.get_world_size(self.group) == 1:
+            return int(code)
+        dev = "cpu" if self.host_staged else torch.device("cuda", torch.cuda.current_device())
+        t = torch.tensor([int(code)], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
     def allreduce_sum(self, t):
         import torch.distributed as dist
 
@@ -347,6 +363,9 @@ class LoopbackExchange:
 
     def __init__(self, parts):
         self.parts = parts
+
+    def agree(self, code):
+        return int(code)
 
     def reduce_partials(self, traces):
         import torch

@@ -27,6 +27,9 @@ Cases
                    10 steps
   cons_k2_lf       conservative formulation, LF flux (format coverage)
   fs_k2_es         free-stream boundary on a non-periodic box (ghost flux)
+  cfg3_*           config 3 (Taylor-Green KEPES k=3): operator at n=4, first
+                   accepted step at n=2 through the dt-halving path
+  cfg2_step_n8     config 2 at n=8: one DIRK step
   visc_*           viscous operator (gradient unknowns q, level-1 condensation):
                    perturbed states with q = solve_gradient + 0.05 N(0,1) at
                    Re=100, M=0.5; and the config-4 Taylor-Green parameters
@@ -184,7 +187,81 @@ def main_viscous_steps():
          newton=newton, dt=0.57)
 
 
+class _FirstStep(Exception):
+    pass
+
+
+def main_cfg3():
+    """Config 3 (inviscid Taylor-Green M=0.1, KEPES, k=3):
+    cfg3_ops_n4   operator outputs on the projected IC at n=4 (384 macros),
+                  alpha = d00/0.57 (the paper's dt), ptc 1, x ~ N(0,1) seed 333
+    cfg3_step_n2  the first accepted DIRK(3,3) step at n=2 with dt=2.28 and
+                  NewtonParams(max_iters=16): stage 1 needs 17 iterations at
+                  2.28, so the step is rejected and retried with dt/2 twice
+                  (the integrator's dt-halving path, time_march.py:380-400)"""
+    from macrohdg.time_march import NewtonParams
+
+    tg = TaylorGreen(mach=0.1, gas=GAS)
+    d00 = dirk33_tableau().d[0, 0]
+    mesh = build_box_macro_mesh(tg.box, 4, 1)
+    disc = Discretization(mesh, p=3, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("kepes"))
+    fields = disc.project(tg.initial)
+    alpha = d00 / 0.57
+    offset = -alpha * disc.volume_quad_states(fields)
+    x = np.random.default_rng(333).standard_normal(fields.trace.shape)
+    out = operator_case(disc, fields, alpha, offset, 1.0, x)
+    sens = sensitivity(disc, fields, alpha, offset, 1.0, x, out)
+    keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+    save("cfg3_ops_n4", w=fields.w, trace=fields.trace, offset=offset, alpha=alpha, ptc=1.0, x=x, **out, **sens,
+         integrals=np.array([disc.integrals(fields)[k] for k in keys]),
+         **meta(disc, "kepes", "entropy", tg.box, 4, 1, 3))
+
+    mesh = build_box_macro_mesh(tg.box, 2, 1)
+    disc = Discretization(mesh, p=3, gas=GAS, formulation="entropy",
+                          flux=DissipationSpec("kepes"))
+    f0 = disc.project(tg.initial)
+    integ = DIRKIntegrator(disc, params=NewtonParams(max_iters=16))
+    got = {}
+
+    def on_step(step, t, flds, reports):
+        got.update(t=t, w=flds.w.copy(), trace=flds.trace.copy())
+        raise _FirstStep
+
+    try:
+        integ.run(f0, t_final=2.28, dt=2.28, on_step=on_step)
+    except _FirstStep:
+        pass
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"], r["fgmres_iters"],
+                        r["jacobian_builds"]] for r in integ.records])
+    save("cfg3_step_n2", w0=f0.w, trace0=f0.trace, w1=got["w"], trace1=got["trace"], t1=got["t"], newton=newton,
+         dt=2.28, max_iters=16,
+         integrals=np.array([[disc.integrals(f)[k] for k in keys]
+                             for f in (f0, FieldSet(got["w"], got["trace"]))]))
+
+
+def main_cfg2_step():
+    """Config 2 (isentropic vortex, ES, k=3) at n=8 (3,072 macros): one
+    DIRK(3,3) step with dt=0.01 from the projected IC."""
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          angle=0.0, center=(5.0, 5.0), gas=GAS)
+    disc = Discretization(build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), 8, 1), p=3,
+                          gas=GAS, formulation="entropy", flux=DissipationSpec("es"))
+    f0 = disc.project(vx.initial)
+    integ = DIRKIntegrator(disc)
+    f1, _ = integ.run(f0, t_final=0.01, dt=0.01)
+    keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"], r["fgmres_iters"],
+                        r["jacobian_builds"]] for r in integ.records])
+    save("cfg2_step_n8", w1=f1.w, trace1=f1.trace, newton=newton, dt=0.01,
+         integrals=np.array([[disc.integrals(f)[k] for k in keys] for f in (f0, f1)]))
+
+
 def main():
+    if "--only-cfg3" in sys.argv:
+        return main_cfg3()
+    if "--only-cfg2-step" in sys.argv:
+        return main_cfg2_step()
     if "--only-viscous" in sys.argv:
         return main_viscous()
     if "--only-visc-steps" in sys.argv:
@@ -292,6 +369,8 @@ def main():
          integrals=hist_arr, newton=newton, dt=dt, tableau_d=tab.d, tableau_e=tab.e)
     main_viscous()
     main_viscous_steps()
+    main_cfg3()
+    main_cfg2_step()
     print(f"done in {time.time() - t0:.1f} s")
 
 

@@ -173,3 +173,68 @@ def test_gloo_world2_partitioned_operator_and_fgmres(flux):
         assert err_mv <= 1e-14
         assert it == it_ref
         assert err_x <= 1e-10
+
+
+def _agree_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2507_22195_b200.distributed import collective
+        from paper_2507_22195_b200.errors import NonAdmissibleState, SingularLocalMatrix
+
+        t = small_tables()
+        ex = TorchDistExchange(LocalPartition(t, rank, world))
+        out = []
+        # 1. a non-admissible trial state on rank 1 only: both ranks raise
+        #    NonAdmissibleState (rank 1 its own, with the location), and the
+        #    exchange afterwards still pairs up (no hang)
+
+        def trial():
+            if rank == 1:
+                raise NonAdmissibleState("non-admissible state at volume sub 0", where="volume sub 0")
+            return "ok"
+
+        try:
+            collective(ex, trial, rank)
+            out.append("no raise")
+        except NonAdmissibleState as e:
+            out.append(("nonadm", e.where))
+        buf = torch.full((4,), float(rank))
+        ex.allreduce_sum(buf)
+        out.append(float(buf[0]))
+        # 2. a singular local matrix on rank 0 and a non-admissible state on
+        #    rank 1: the larger code (singular) wins everywhere
+        def lin():
+            if rank == 0:
+                raise SingularLocalMatrix("singular condensed block on macro 3", macro=3)
+            raise NonAdmissibleState("x", where="face tile 1")
+
+        try:
+            collective(ex, lin, rank)
+        except SingularLocalMatrix as e:
+            out.append(("singular", e.macro))
+        except NonAdmissibleState:
+            out.append("wrong class")
+        # 3. no failure anywhere: the value passes through
+        out.append(collective(ex, lambda: rank * 10, rank))
+        results[rank] = out
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_failure_is_collective():
+    """a rank-local NonAdmissibleState / SingularLocalMatrix must
+    be raised on every rank at the same point, so the Newton loop takes the
+    tau/4 retry branch on all ranks and the halo sequence stays paired."""
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.start_processes(_agree_worker, args=(world, _free_port(), results), nprocs=world,
+                       join=True, start_method="spawn")
+    r0, r1 = results[0], results[1]
+    assert r0[0] == ("nonadm", "remote rank") and r1[0] == ("nonadm", "volume sub 0")
+    assert r0[1] == r1[1] == 1.0
+    assert r0[2] == ("singular", 3) and r1[2] == ("singular", None)
+    assert r0[3] == 0 and r1[3] == 10
