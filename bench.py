@@ -484,8 +484,9 @@ def run_b200(args, rank, local_rank, world):
                     "fgmres_inner": sum(r["inner_iters_total"] for r in rec),
                     "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
                     "dt": args.implicit_dt, "tableau": "DIRK(3,3)",
-                    "halvings": getattr(integ, "halvings", None),
-                    "engine": getattr(integ, "engine_name", "host")}
+                    "halvings": integ.halvings,
+                    "krylov": ("host loop" if os.environ.get("MHDG_KRYLOV") == "host" else
+                               "device graph (solver.KrylovEngine)")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -680,7 +681,7 @@ def run_b200_partitioned(args, rank, local_rank, world):
                     "fgmres_inner": sum(r["inner_iters_total"] for r in rec),
                     "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
                     "dt": args.implicit_dt, "tableau": "DIRK(3,3)",
-                    "halvings": getattr(integ, "halvings", None)}
+                    "halvings": integ.halvings, "krylov": "host loop (distributed dots)"}
     peaks = load_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     nqf = t.fphi.shape[0]

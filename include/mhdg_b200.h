@@ -186,6 +186,14 @@ int mhdg_from_conservative(mhdg_ctx* ctx, int64_t n, const double* u, double* w,
  * entropy, thermo_entropy, kinetic_energy, mass, total_energy */
 int mhdg_integrals(mhdg_ctx* ctx, const double* w, double* out_host,
                    void* stream);
+/* Discretization.entropy_identity_defect (assembly.py:649-672, face term
+ * fluxes.py:245-255): out_host = {lhs, rhs, |lhs - rhs|} with
+ * lhs = sum v . r_w - sum v_hat . r_trace (r_* = residuals at stage None of
+ * the same fields) and rhs = -sum over side tiles and face points of
+ * face_w [(v(u_hat) - v(u)) . F^ - (psi_n(u_hat) - psi_n(u))]. */
+int mhdg_entropy_identity(mhdg_ctx* ctx, const double* w, const double* trace,
+                          const double* r_w, const double* r_trace, double* out_host,
+                          void* stream);
 /* Discretization.kinetic_energy_dissipation numerator (assembly.py:622-648):
  * out_host[0] = 2 mu_eff * integral of rho |curl V|^2 / 2 (divide by |Omega|) */
 int mhdg_dissipation(mhdg_ctx* ctx, const double* w, const double* q,

@@ -98,6 +98,8 @@ _SIGS = {
                                        C.c_void_p]),
     "mhdg_from_conservative": (C.c_int, [C.c_void_p, C.c_int64, dptr, dptr, C.c_void_p]),
     "mhdg_integrals": (C.c_int, [C.c_void_p, dptr, C.POINTER(C.c_double), C.c_void_p]),
+    "mhdg_entropy_identity": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, C.POINTER(C.c_double),
+                                        C.c_void_p]),
     "mhdg_dissipation": (C.c_int, [C.c_void_p, dptr, dptr, C.POINTER(C.c_double), C.c_void_p]),
     "mhdg_dot": (C.c_int, [C.c_void_p, C.c_int64, dptr, dptr, dptr, C.c_void_p]),
     "mhdg_mgs": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, dptr, dptr, dptr, C.c_void_p]),

@@ -421,6 +421,18 @@ class Discretization:
         N.raise_for(rc)
         return float(out[0]) / self.domain_volume
 
+    def entropy_identity_defect(self, fields):
+        """sum v . R_V - sum v^ . R_V^ against minus the summed face entropy
+        residuals (assembly.py:649-672); returns (lhs, rhs, |lhs - rhs|).
+        Zero up to round-off for the EC flux; the dissipative fluxes produce
+        entropy."""
+        w, tr = self._fields(fields)
+        res = self.residuals(FieldSet(w, tr, self._q(fields)), stage=None)
+        out = (C.c_double * 3)()
+        N.raise_for(self._lib.mhdg_entropy_identity(self._ctx, N.ptr(w), N.ptr(tr), N.ptr(res.r_w),
+                                                    N.ptr(res.r_trace), out, N.stream_handle()))
+        return float(out[0]), float(out[1]), float(out[2])
+
     def total_generalized_entropy(self, fields):
         v = self.integrals(fields)
         return v["entropy"], v["thermo_entropy"]

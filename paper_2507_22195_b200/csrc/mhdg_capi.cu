@@ -1012,6 +1012,39 @@ extern "C" int mhdg_dissipation(mhdg_ctx* c, const double* w, const double* q, d
   return MHDG_OK;
 }
 
+// Discretization.entropy_identity_defect (assembly.py:649-672): out_host =
+// {lhs, rhs, |lhs - rhs|} for the residual (stage None) r_w, r_trace of the
+// same fields; lhs = sum v . r_w - sum v_hat . r_trace, rhs = -sum face_w r.
+extern "C" int mhdg_entropy_identity(mhdg_ctx* c, const double* w, const double* trace, const double* r_w,
+                                     const double* r_trace, double* out_host, void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  double* part = c->d_partial;                       // 3 x RED_BLOCKS partials
+  double* res = c->d_partial + 2 * RED_BLOCKS * 5;   // 3 results
+  const int nb = std::min(RED_BLOCKS, std::max(1, c->E));
+  k_entropy_dot<<<RED_BLOCKS, 256, 0, s>>>((int64_t)c->E * c->nn, c->geo.form, c->geo.gamma, w, r_w, part);
+  k_entropy_dot<<<RED_BLOCKS, 256, 0, s>>>((int64_t)c->F * c->nfn, c->geo.form, c->geo.gamma, trace, r_trace,
+                                           part + RED_BLOCKS);
+  switch (c->p) {
+    case 1: k_entropy_faces<1, 64><<<nb, 64, 0, s>>>(c->geo, w, trace, part + 2 * RED_BLOCKS); break;
+    case 2: k_entropy_faces<2, 64><<<nb, 64, 0, s>>>(c->geo, w, trace, part + 2 * RED_BLOCKS); break;
+    case 3: k_entropy_faces<3, 64><<<nb, 64, 0, s>>>(c->geo, w, trace, part + 2 * RED_BLOCKS); break;
+    default: k_entropy_faces<4, 128><<<nb, 128, 0, s>>>(c->geo, w, trace, part + 2 * RED_BLOCKS); break;
+  }
+  k_reduce_rows<<<1, 32, 0, s>>>(RED_BLOCKS, 1, part, res);
+  k_reduce_rows<<<1, 32, 0, s>>>(RED_BLOCKS, 1, part + RED_BLOCKS, res + 1);
+  k_reduce_rows<<<1, 32, 0, s>>>(nb, 1, part + 2 * RED_BLOCKS, res + 2);
+  c->launches += 6;
+  CK(cudaGetLastError());
+  double h[3];
+  CK(cudaMemcpyAsync(h, res, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out_host[0] = h[0] - h[1];
+  out_host[1] = -h[2];
+  out_host[2] = fabs(out_host[0] - out_host[1]);
+  return MHDG_OK;
+}
+
 extern "C" int mhdg_integrals(mhdg_ctx* c, const double* w, double* out_host, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));

@@ -1889,4 +1889,88 @@ k_integrals(Geo g, const double* __restrict__ w, double* __restrict__ partial) {
   if (threadIdx.x < 5) partial[blockIdx.x * 5 + threadIdx.x] = red[threadIdx.x][0];
 }
 
+// entropy identity monitor, face part (assembly.py:649-672 with
+// fluxes.py:245-255): per side tile k and face point q of every macro
+//   r = (v(u_hat) - v(u)) . F^(u, u_hat; n) - (psi_n(u_hat) - psi_n(u)),
+//   psi_n(u) = rho V . n, summed with face_w = fw_q area_k; per-block
+// partials (the caller reduces them in a fixed order).
+template <int P, int NT>
+__global__ void __launch_bounds__(NT)
+k_entropy_faces(Geo g, const double* __restrict__ w, const double* __restrict__ tr,
+                double* __restrict__ partial) {
+  using D = Dims<P>;
+  __shared__ double red[NT];
+  const double gam = g.gamma;
+  double acc = 0.0;
+  for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
+    for (int t = threadIdx.x; t < 4 * D::NQF; t += NT) {
+      const int k = t / D::NQF, q = t % D::NQF;
+      double wq[5] = {0, 0, 0, 0, 0}, wh[5] = {0, 0, 0, 0, 0};
+      const int f = g.fid[e * 4 + k];
+      for (int i = 0; i < D::NFN; ++i) {
+        const double a = g.pf[(k * D::NQF + q) * D::NFN + i];
+        const double b = g.fphi[q * D::NFN + i];
+        const double* wi = w + ((size_t)e * D::NN + g.rows[k * D::NFN + i]) * 5;
+        const double* ti = tr + ((size_t)f * D::NFN + g.tidx[((size_t)e * 4 + k) * D::NFN + i]) * 5;
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          wq[s] += a * wi[s];
+          wh[s] += b * ti[s];
+        }
+      }
+      double u[5], uh[5], n[3];
+      to_conservative(wq, g.form, gam, u);
+      to_conservative(wh, g.form, gam, uh);
+      for (int a = 0; a < 3; ++a) n[a] = g.nrm[((size_t)e * 4 + k) * 3 + a];
+      double fh[5], v[5], vh[5];
+      numerical_flux(g.kind, u, uh, n, gam, fh);
+      entropy_vars(u, gam, v);
+      entropy_vars(uh, gam, vh);
+      double r = 0.0;
+#pragma unroll
+      for (int s = 0; s < 5; ++s) r += (vh[s] - v[s]) * fh[s];
+      const double psi = (u[1] * n[0] + u[2] * n[1]) + u[3] * n[2];
+      const double psih = (uh[1] * n[0] + uh[2] * n[1]) + uh[3] * n[2];
+      r -= psih - psi;
+      acc += (g.fw[q] * g.area[e * 4 + k]) * r;
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int sft = NT / 2; sft > 0; sft >>= 1) {
+    if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+// sum over nodes of v(state) . r, v = state (entropy formulation) or
+// entropy_vars(state) (conservative): the left side of the identity
+__global__ void k_entropy_dot(int64_t n, int form, double gam, const double* __restrict__ x,
+                              const double* __restrict__ r, double* __restrict__ partial) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v[5];
+    if (form == 1) {
+#pragma unroll
+      for (int s = 0; s < 5; ++s) v[s] = x[i * 5 + s];
+    } else {
+      double u[5];
+#pragma unroll
+      for (int s = 0; s < 5; ++s) u[s] = x[i * 5 + s];
+      entropy_vars(u, gam, v);
+    }
+#pragma unroll
+    for (int s = 0; s < 5; ++s) acc += v[s] * r[i * 5 + s];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int sft = 128; sft > 0; sft >>= 1) {
+    if (threadIdx.x < sft) red[threadIdx.x] += red[threadIdx.x + sft];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
 }  // namespace mhdg

@@ -257,7 +257,56 @@ def main_cfg2_step():
          integrals=np.array([[disc.integrals(f)[k] for k in keys] for f in (f0, f1)]))
 
 
+def main_entropy():
+    """entropy_identity_defect (assembly.py:649-672) on perturbed-uniform
+    states (n=(2,2,2)) for es / kepes / ec at p=2, kepes at p=3, and on the
+    projected Taylor-Green state (n=2, p=3, kepes)."""
+    box3 = np.array([[0.0, 1.0]] * 3)
+    out = {}
+    for p, flux in ((2, "es"), (2, "kepes"), (2, "ec"), (3, "kepes")):
+        disc = Discretization(build_box_macro_mesh(box3, (2, 2, 2), 1), p=p, gas=GAS,
+                              formulation="entropy", flux=DissipationSpec(flux))
+        f = perturbed_uniform(disc, 3000 + 10 * p)
+        lhs, rhs, dfc = disc.entropy_identity_defect(f)
+        out[f"k{p}_{flux}"] = (f.w, f.trace, lhs, rhs, dfc)
+    tg = TaylorGreen(mach=0.1, gas=GAS)
+    disc = Discretization(build_box_macro_mesh(tg.box, 2, 1), p=3, gas=GAS,
+                          formulation="entropy", flux=DissipationSpec("kepes"))
+    f = disc.project(tg.initial)
+    out["tgv_k3_kepes"] = (f.w, f.trace) + tuple(disc.entropy_identity_defect(f))
+    arrays = {}
+    for k, (w, tr, lhs, rhs, dfc) in out.items():
+        arrays.update({f"{k}_w": w, f"{k}_trace": tr, f"{k}_lhs": lhs, f"{k}_rhs": rhs,
+                       f"{k}_defect": dfc})
+    save("entropy_identity", **arrays)
+
+
+def main_hsweep():
+    """Config-2 h-refinement study, first level (driver.py:570-606 space axis
+    semantics on the [0,10]^3 vortex of config 2): n=8, k=3, ES, t_eval =
+    0.1 t_c = 1.0, dt0 = t_eval / 10; L2 error of rho against the exact
+    translated vortex (assembly.py:674-684) and the final state."""
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          angle=0.0, center=(5.0, 5.0), gas=GAS)
+    disc = Discretization(build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), 8, 1), p=3,
+                          gas=GAS, formulation="entropy", flux=DissipationSpec("es"))
+    f0 = disc.project(vx.initial)
+    t_eval = 0.1 * vx.convective_period
+    integ = DIRKIntegrator(disc)
+    f1, t = integ.run(f0, t_final=t_eval, dt=t_eval / 10.0)
+    err = disc.l2_error(f1, lambda x: vx.state(x, t_eval), component=0)
+    err0 = disc.l2_error(f0, vx.initial, component=0)
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"], r["fgmres_iters"],
+                        r["jacobian_builds"]] for r in integ.records])
+    save("cfg2_hsweep_n8", w1=f1.w, trace1=f1.trace, l2=err, l2_initial=err0, t_eval=t_eval,
+         dt=t_eval / 10.0, newton=newton)
+
+
 def main():
+    if "--only-hsweep" in sys.argv:
+        return main_hsweep()
+    if "--only-entropy" in sys.argv:
+        return main_entropy()
     if "--only-cfg3" in sys.argv:
         return main_cfg3()
     if "--only-cfg2-step" in sys.argv:
@@ -371,6 +420,7 @@ def main():
     main_viscous_steps()
     main_cfg3()
     main_cfg2_step()
+    main_entropy()
     print(f"done in {time.time() - t0:.1f} s")
 
 
