@@ -257,6 +257,11 @@ int mhdg_krylov_solve(mhdg_krylov* k, const mhdg_lin_buffers* lin, const double*
                       double* x, mhdg_krylov_stats* stats, int sync, void* stream);
 void mhdg_krylov_destroy(mhdg_krylov* k);
 
+/* Diagnostic of the last linearization's batched inversions: out[0] / out[1]
+ * = S blocks / face blocks that failed the diagonal-pivot ratio check and
+ * went through the partial-pivoting pass (synchronizes the stream). */
+int mhdg_gj_fallbacks(mhdg_ctx* ctx, int* out, void* stream);
+
 /* number of library kernels launched since creation (evidence counter) */
 int64_t mhdg_launch_count(const mhdg_ctx* ctx);
 /* FP64 FMA throughput probe (roofline denominator), returns GFLOP/s */

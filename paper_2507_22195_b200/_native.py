@@ -114,6 +114,7 @@ _SIGS = {
     "mhdg_krylov_solve": (C.c_int, [C.c_void_p, C.POINTER(LinBuffers), dptr, dptr, dptr, C.c_int,
                                     C.c_void_p]),
     "mhdg_krylov_destroy": (None, [C.c_void_p]),
+    "mhdg_gj_fallbacks": (C.c_int, [C.c_void_p, dptr, C.c_void_p]),
     "mhdg_launch_count": (C.c_int64, [C.c_void_p]),
     "mhdg_fp64_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_dmma_probe": (C.c_double, [C.c_int, C.c_void_p]),

@@ -249,6 +249,13 @@ class Discretization:
     def trace_idx(self):
         return self.tables.trace_idx
 
+    def gj_fallbacks(self):
+        """(S blocks, face blocks) of the last linearization that needed the
+        partial-pivoting pass of the batched Gauss-Jordan."""
+        out = (C.c_int * 2)()
+        N.raise_for(self._lib.mhdg_gj_fallbacks(self._ctx, C.cast(out, C.c_void_p), N.stream_handle()))
+        return int(out[0]), int(out[1])
+
     @property
     def launch_count(self):
         return int(self._lib.mhdg_launch_count(self._ctx))

@@ -37,6 +37,7 @@ struct mhdg_ctx {
   double* d_tmp_trace; // F*nt*5 workspace
   double* d_gbuf;      // E*nm local right-hand sides (condensed operator)
   double* d_zbuf;      // E*nm local solutions
+  int* d_fb;           // Gauss-Jordan pivoting fallback: counts [2] + list
   int64_t launches;
 };
 
@@ -275,6 +276,8 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   c->d_unsym = (int*)dalloc(c, sizeof(int) * 4, err);
   c->d_partial = (double*)dalloc(c, sizeof(double) * (2 * RED_BLOCKS * 5 + 64), err);
   c->d_tmp_trace = (double*)dalloc(c, sizeof(double) * F * NFN * 5, err);
+  c->d_fb = (int*)dalloc(c, sizeof(int) * (2 + (size_t)std::max(t->n_macros, t->n_faces)), err);
+  if (c->d_fb) cudaMemset(c->d_fb, 0, 2 * sizeof(int));
   c->d_gbuf = (double*)dalloc(c, sizeof(double) * E * NN * 5, err);
   c->d_zbuf = (double*)dalloc(c, sizeof(double) * E * NN * 5, err);
   if (*err != MHDG_OK) {
@@ -302,6 +305,16 @@ extern "C" void mhdg_lin_sizes(const mhdg_ctx* c, int64_t sizes[6]) {
   sizes[1] = sizes[2] = sizes[3] = (int64_t)c->E * 4 * c->nqf * 25;
   sizes[4] = (int64_t)c->F * nb * nb;
   sizes[5] = c->visc ? (int64_t)c->E * nm : 1;
+}
+
+// matrices of the last linearization that needed the partial-pivoting pass
+// (out[0]: S blocks, out[1]: face blocks); diagnostic, synchronizes
+extern "C" int mhdg_gj_fallbacks(mhdg_ctx* c, int* out, void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(out, c->d_fb, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return MHDG_OK;
 }
 
 extern "C" int64_t mhdg_launch_count(const mhdg_ctx* c) { return c->launches; }
@@ -537,14 +550,34 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 #ifndef MHDG_GJ_NWT_SMALL
 #define MHDG_GJ_NWT_SMALL 4
 #endif
+// Two passes (mhdg_gj_blocked.cuh GjPass): diagonal pivots with a ratio
+// check, then partial pivoting for the matrices that failed it (their S is
+// still in place).  fb = c->d_fb + slot: [0] count, list at c->d_fb + 2.
+#ifndef MHDG_GJ_NOPIV
+#define MHDG_GJ_NOPIV 1
+#endif
 template <int N>
-static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s) {
+static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s,
+                        int slot = 0) {
   constexpr int NWT = N >= 64 ? MHDG_GJ_NWT : MHDG_GJ_NWT_SMALL;
   constexpr int NPW = N >= 64 ? MHDG_GJ_NPW : MHDG_GJ_NPW_SMALL;
   using GL = GJLA2<N, NWT, NPW>;
-  if (set_smem(k_gj_la2<N, NWT, NPW>, GL::bytes)) return MHDG_CUDA_ERROR;
-  k_gj_la2<N, NWT, NPW><<<grid_for(c, nmat, occ(k_gj_la2<N, NWT, NPW>, GL::NT, GL::bytes)), GL::NT, GL::bytes,
-                          s>>>(nmat, mats, status);
+  if (set_smem(k_gj_la2<N, NWT, NPW, false>, GL::bytes)) return MHDG_CUDA_ERROR;
+  const int grid = grid_for(c, nmat, occ(k_gj_la2<N, NWT, NPW, false>, GL::NT, GL::bytes));
+  if (MHDG_GJ_NOPIV) {
+    if (set_smem(k_gj_la2<N, NWT, NPW, true>, GL::bytes)) return MHDG_CUDA_ERROR;
+    int* cnt = c->d_fb + slot;
+    int* list = c->d_fb + 2;
+    CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+    k_gj_la2<N, NWT, NPW, true><<<grid, GL::NT, GL::bytes, s>>>(nmat, mats, status,
+                                                               GjPass{nullptr, nullptr, cnt, list});
+    k_gj_la2<N, NWT, NPW, false><<<grid, GL::NT, GL::bytes, s>>>(0, mats, status,
+                                                                GjPass{list, cnt, nullptr, nullptr});
+    c->launches += 1;
+  } else {
+    k_gj_la2<N, NWT, NPW, false><<<grid, GL::NT, GL::bytes, s>>>(nmat, mats, status,
+                                                                GjPass{nullptr, nullptr, nullptr, nullptr});
+  }
   return MHDG_OK;
 }
 template <int P>
@@ -575,7 +608,7 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
     c->launches++;
   }
   constexpr int NM = Dims<P>::NM;
-  if (gj_lookahead<NM>(c, c->E, L->sinv, c->d_status, s)) return MHDG_CUDA_ERROR;
+  if (gj_lookahead<NM>(c, c->E, L->sinv, c->d_status, s, 0)) return MHDG_CUDA_ERROR;
   (void)ptc;
   c->launches++;
   CK(cudaGetLastError());
@@ -636,17 +669,32 @@ static int launch_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
     constexpr int NWT = NB >= 64 ? MHDG_GJ_NWT : MHDG_GJ_NWT_SMALL;
     constexpr int NPW = NB >= 64 ? MHDG_GJ_NPW : MHDG_GJ_NPW_SMALL;
     const size_t fsm = (GJLA2<NB, NWT, NPW>::bytes + 15) / 16 * 16 + FaceBlockSrc<P, 32 * NWT>::extra_bytes;
-    if (set_smem(k_precond_gj<P, NWT, NPW>, fsm)) return MHDG_CUDA_ERROR;
-    k_precond_gj<P, NWT, NPW><<<grid_for(c, c->n_owned, occ(k_precond_gj<P, NWT, NPW>, 32 * NWT, fsm)), 32 * NWT,
-                                fsm, s>>>(c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv,
-                                          c->d_status + 1, c->d_unsym);
-    c->launches++;
+    if (set_smem(k_precond_gj<P, NWT, NPW, false>, fsm)) return MHDG_CUDA_ERROR;
+    const int grid = grid_for(c, c->n_owned, occ(k_precond_gj<P, NWT, NPW, false>, 32 * NWT, fsm));
+    if (MHDG_GJ_NOPIV) {   // diagonal pivots, then partial pivoting for the rest
+      if (set_smem(k_precond_gj<P, NWT, NPW, true>, fsm)) return MHDG_CUDA_ERROR;
+      int* cnt = c->d_fb + 1;
+      int* list = c->d_fb + 2;
+      CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+      k_precond_gj<P, NWT, NPW, true><<<grid, 32 * NWT, fsm, s>>>(c->geo, c->n_owned, L->hh, hh_rem, tidx_rem,
+                                                                  area_rem, L->pinv, c->d_status + 1, c->d_unsym,
+                                                                  GjPass{nullptr, nullptr, cnt, list});
+      k_precond_gj<P, NWT, NPW, false><<<grid, 32 * NWT, fsm, s>>>(c->geo, 0, L->hh, hh_rem, tidx_rem, area_rem,
+                                                                   L->pinv, c->d_status + 1, nullptr,
+                                                                   GjPass{list, cnt, nullptr, nullptr});
+      c->launches += 2;
+    } else {
+      k_precond_gj<P, NWT, NPW, false><<<grid, 32 * NWT, fsm, s>>>(c->geo, c->n_owned, L->hh, hh_rem, tidx_rem,
+                                                                   area_rem, L->pinv, c->d_status + 1, c->d_unsym,
+                                                                   GjPass{nullptr, nullptr, nullptr, nullptr});
+      c->launches++;
+    }
   } else if constexpr (true) {   // assemble, then the blocked tensor-core Gauss-Jordan
     if (set_smem(k_precond_factor<P, NT, false>, smem)) return MHDG_CUDA_ERROR;
     int per_sm = occ(k_precond_factor<P, NT, false>, NT, smem);
     k_precond_factor<P, NT, false><<<grid_for(c, c->n_owned, per_sm), NT, smem, s>>>(
         c->geo, c->n_owned, L->hh, hh_rem, tidx_rem, area_rem, L->pinv, c->d_status + 1, c->d_unsym);
-    if (gj_lookahead<NB>(c, c->n_owned, L->pinv, c->d_status + 1, s)) return MHDG_CUDA_ERROR;
+    if (gj_lookahead<NB>(c, c->n_owned, L->pinv, c->d_status + 1, s, 1)) return MHDG_CUDA_ERROR;
     c->launches += 2;
   } else {
     if (set_smem(k_precond_factor<P, NT>, smem)) return MHDG_CUDA_ERROR;

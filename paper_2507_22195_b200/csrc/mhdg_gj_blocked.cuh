@@ -226,7 +226,7 @@ struct GJLA2 {
   static constexpr int RPL = (NP + 32 * NPW - 1) / (32 * NPW);
   static constexpr int NT = 32 * NWT;
   static constexpr int UF = T * 2 * 32;
-  static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 8 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
+  static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 16 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
 };
 
 #ifndef MHDG_GJ_TILE_STORE
@@ -260,16 +260,35 @@ struct GjGlobalSrc {   // the matrix is read from mats[m] and overwritten
   }
 };
 
-template <int N, int NWT, int NPW, class Src>
+// Matrix selection and the diagonal-pivot pass (GjPass): with nopiv the
+// pivots are taken on the diagonal (no search on the pivot chain: a pivot
+// step is broadcast -> reciprocal -> update); every panel warp checks, off
+// the chain, that the pivot is at least GJ_TAU times the largest remaining
+// entry of its rows in that column.  A matrix that fails the check (or meets
+// a zero / non-finite pivot) is left untouched in `mats` and appended to
+// fb_list; the partial-pivoting pass then runs over that list (list /
+// count_dev), so singular blocks are still detected and reported by the
+// pivoting elimination exactly as before.
+#ifndef MHDG_GJ_TAU
+#define MHDG_GJ_TAU 0.05
+#endif
+struct GjPass {
+  const int* list;       // matrices to process (nullptr: 0 .. nmat-1)
+  const int* count_dev;  // length of list (device), when list != nullptr
+  int* fb_count;         // nopiv pass: fallback list length
+  int* fb_list;          // nopiv pass: fallback matrix ids
+};
+
+template <int N, int NWT, int NPW, class Src, bool NOPIV = false>
 __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats, unsigned long long* status,
-                                            const Src& src) {
+                                            const Src& src, GjPass pass = GjPass{nullptr, nullptr, nullptr, nullptr}) {
   using L = GJLA2<N, NWT, NPW>;
   constexpr int NP = L::NP, S = L::S, T = L::T, NPAN = L::NPAN, RPL = L::RPL, NT = L::NT;
   extern __shared__ __align__(16) double smem[];
   double* A = smem;                        // NP x S
   double* Ub = A + NP * S;                 // 2 x UF
-  double* sProw = Ub + 2 * L::UF;          // 8: pivot row of the current step
-  unsigned* sCand = reinterpret_cast<unsigned*>(sProw + 8);   // [NPW][3]: hi, lo, row
+  double* sProw = Ub + 2 * L::UF;          // 2 x 8: pivot row of the current step
+  unsigned* sCand = reinterpret_cast<unsigned*>(sProw + 16);  // [NPW][3]: hi, lo, row
   int* q = (int*)(sCand + 4 * NPW);        // NP: pivot row of step k
   int* qi = q + NP;
   int* flag = qi + NP;
@@ -294,6 +313,65 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
       for (int j = 0; j < 8; ++j) a[i][j] = r < NP ? A[r * S + k0 + j] : 0.0;
     }
     int pt[8];
+    if constexpr (NOPIV) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        pt[t] = -1;
+        if (t < nbp) {
+          const int p = k0 + t;
+          // ratio check, off the pivot chain: largest |a_rt| over this warp's
+          // rows r > p (hi word of the bit pattern: a bound within 2^-20)
+          unsigned bhi = 0u;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int r = row_of(i);
+            const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(fabs(a[i][t])) >> 32);
+            if (r < N && r > p && hi > bhi) bhi = hi;
+          }
+          const unsigned mhi = __reduce_max_sync(0xffffffffu, bhi);
+          pt[t] = p;
+          if (pw == 0 && lane == 0) q[p] = p;
+          const int owner = p & 31, oslot = (p >> 5) / NPW, ow = (p >> 5) % NPW;
+          double prow[8];
+          if (NPW > 1) {
+            double* pr = sProw + (t & 1) * 8;   // double-buffered across pivots
+            if (pw == ow && lane == owner)
+#pragma unroll
+              for (int i = 0; i < RPL; ++i)
+                if (i == oslot)
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) pr[j] = a[i][j];
+            psync();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) prow[j] = pr[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              double v = a[0][j];
+#pragma unroll
+              for (int i = 1; i < RPL; ++i) v = oslot == i ? a[i][j] : v;
+              prow[j] = __shfl_sync(0xffffffffu, v, owner);
+            }
+          }
+          const double piv = prow[t];
+          const double cmax = __longlong_as_double((long long)((unsigned long long)mhi << 32));
+          if (!(fabs(piv) > 0.0) || !isfinite(piv) || fabs(piv) < MHDG_GJ_TAU * cmax) ok = false;
+          const double pinv = drcp(piv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) prow[j] = (j == t ? 1.0 : prow[j]) * pinv;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const bool isp = (pw == ow) && (lane == owner) && (oslot == i);
+            const double cr = a[i][t];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const double v = (j == t ? 0.0 : a[i][j]) - cr * prow[j];
+              a[i][j] = isp ? prow[j] : v;
+            }
+          }
+        }
+      }
+    } else {
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       pt[t] = -1;
@@ -378,6 +456,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
         }
       }
     }
+    }
     double* U = Ub + (pan & 1) * L::UF;
 #pragma unroll
     for (int i = 0; i < RPL; ++i) {
@@ -408,7 +487,9 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
 
   double* ex = smem + (L::bytes + 15) / 16 * 2;   // the source's scratch
   src.init(ex, tid, NT);
-  for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
+  if (pass.list) nmat = *pass.count_dev;
+  for (int mi = blockIdx.x; mi < nmat; mi += gridDim.x) {
+    const int m = pass.list ? pass.list[mi] : mi;
     double* M = mats + (size_t)m * N * N;
     __syncthreads();
     src.load(m, A, S, ex, Ub, tid, NT);   // Ub is free until the first panel
@@ -453,6 +534,12 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
     for (int k = tid; k < N; k += NT) qi[q[k]] = k;
     __syncthreads();
     int bad = *flag;
+    if constexpr (NOPIV) {
+      if (bad) {   // leave S in place for the pivoting pass
+        if (tid == 0) pass.fb_list[atomicAdd(pass.fb_count, 1)] = m;
+        continue;
+      }
+    }
 #if MHDG_GJ_TILE_STORE
     // column-major inverse in 4-row x 8-column tiles per warp: the gathered
     // rows q[r] / columns qi[c] spread over the banks (a column walk hits
@@ -491,10 +578,10 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
   }
 }
 
-template <int N, int NWT, int NPW>
+template <int N, int NWT, int NPW, bool NOPIV = false>
 __global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, (N < 64 ? MHDG_GJ_MINB_SMALL : 2))
-k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status) {
-  gj_la2_body<N, NWT, NPW>(nmat, mats, status, GjGlobalSrc<N>{mats});
+k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status, GjPass pass) {
+  gj_la2_body<N, NWT, NPW, GjGlobalSrc<N>, NOPIV>(nmat, mats, status, GjGlobalSrc<N>{mats}, pass);
 }
 
 // K4 face blocks assembled in place (assembly.py:994-1026): the face block
@@ -611,19 +698,19 @@ struct FaceBlockSrc {
         amax = fmax(amax, sRed[w]);
         dmax = fmax(dmax, sRed[NT / 32 + w]);
       }
-      if (!(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
+      if (n_unsym && !(dmax <= 1e-12 * fmax(1.0, amax))) atomicAdd(n_unsym, 1);
     }
   }
 };
 
-template <int P, int NWT, int NPW>
+template <int P, int NWT, int NPW, bool NOPIV = false>
 __global__ void __launch_bounds__(32 * NWT, (Dims<P>::NB < 64 ? MHDG_GJ_MINB_SMALL : 2))
 k_precond_gj(Geo g, int n_faces, const double* __restrict__ hh, const double* __restrict__ hh_rem,
              const int* __restrict__ tidx_rem, const double* __restrict__ area_rem, double* __restrict__ pinv,
-             unsigned long long* status, int* n_unsym) {
+             unsigned long long* status, int* n_unsym, GjPass pass) {
   static_assert(FaceBlockSrc<P, 32 * NWT>::tmp_doubles <= 2 * GJLA2<Dims<P>::NB, NWT, NPW>::UF, "staging");
-  gj_la2_body<Dims<P>::NB, NWT, NPW>(n_faces, pinv, status,
-                                     FaceBlockSrc<P, 32 * NWT>{g, hh, hh_rem, tidx_rem, area_rem, n_unsym});
+  gj_la2_body<Dims<P>::NB, NWT, NPW, FaceBlockSrc<P, 32 * NWT>, NOPIV>(
+      n_faces, pinv, status, FaceBlockSrc<P, 32 * NWT>{g, hh, hh_rem, tidx_rem, area_rem, n_unsym}, pass);
 }
 
 }  // namespace mhdg
