@@ -30,6 +30,13 @@
 // (0.521 ms: the early dependents hold SM slots), an L2 prefetch of the first
 // S^-1 columns before the wait was neutral.  Without the launch attribute the
 // wait is a no-op.
+// INVARIANT at every pdl_wait() call site (tests/test_gpu_pdl.py builds the
+// library with -DMHDG_PDL=0 and checks bit-identical operator outputs):
+// before the wait a kernel may only READ immutable context tables (basis /
+// facet tables, face ids, trace permutations, areas, rows, node-face maps)
+// and WRITE its own shared memory / registers; every CTA executes the wait
+// before touching any buffer a predecessor writes (x, z, gbuf, S^-1 inputs,
+// r_w, r_q, y, hh, hw, hhat) and no CTA exits before it.
 #ifndef MHDG_PDL
 #define MHDG_PDL 1
 #endif
@@ -1504,7 +1511,7 @@ k_local_solve(int E, const double* __restrict__ sinv, const double* __restrict__
   constexpr int MB = LocalSolveCfg<NM>::MB;
   __shared__ double sg[MB * NM];
   const int ml = threadIdx.x / NM, rr = threadIdx.x % NM;
-  pdl_wait();
+  pdl_wait();   // nothing precedes the wait but index arithmetic
   for (int e0 = blockIdx.x * MB; e0 < E; e0 += gridDim.x * MB) {
     const int nm = min(MB, E - e0);
     __syncthreads();
@@ -1657,6 +1664,8 @@ k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restri
       }
     }
   };
+  // before the wait: reference tables and face metadata (fid, tidx, area) into
+  // shared memory only; prefetch() (reads x / zin / hhat) runs after it
   pdl_wait();
   if (e00 < g.E) prefetch(e00, 0);
   int slot = 0;
@@ -1793,7 +1802,7 @@ k_precond_apply(int F, const double* __restrict__ pinv, const double* __restrict
                 double* __restrict__ z) {
   constexpr int NB = Dims<P>::NB;
   __shared__ double sR[NB];
-  pdl_wait();
+  pdl_wait();   // first instruction: r is the predecessor's output
   for (int f = blockIdx.x; f < F; f += gridDim.x) {
     __syncthreads();
     for (int i = threadIdx.x; i < NB; i += NT) sR[i] = r[(size_t)f * NB + i];

@@ -134,7 +134,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
   const bool use_x = mode != 1, use_r = mode != 0;
   const int nblk = (g.E + MB - 1) / MB;
   for (int i = NK * 5 + lt; i < V::NKP * 5; i += SP) sm[slot].Gk[i] = 0.0;
-  pdl_wait();
+  pdl_wait();   // before: shared-memory padding only (mhdg_kernels.cuh PDL invariant)
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int e = blk * MB + slot;
     const bool live = e < g.E;
@@ -264,7 +264,7 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
   const int slot = tid / NPF, lt = tid % NPF;
   const double gam = g.gamma;
   const int nblk = (g.E + MB - 1) / MB;
-  pdl_wait();
+  pdl_wait();   // before: index arithmetic only (mhdg_kernels.cuh PDL invariant)
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int e = blk * MB + slot;
     const bool live = slot < MB && e < g.E;
