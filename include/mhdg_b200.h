@@ -84,6 +84,21 @@ typedef struct {
   const double* pref;         /* (3, nn, nn) Mref^-1 Kref_k               */
   const double* kref;         /* (3, nn, nn) Kref_k[j][i]                 */
   const double* eref;         /* (n_st, nfn, nfn) Eref_k[i][j]            */
+  /* m > 1 macro subdivision (reference fem.py:550-724,
+   * assembly.py:155-324); ignored for m = 1.  nc / nt: macro C0 nodes and
+   * trace nodes per face; scatter: element node -> macro node per
+   * sub-element; per-(macro, sub-element) geometry; CSR lists giving, per
+   * trace entry (face * nt + node), the tile-contribution slots
+   * ((macro * n_st + tile) * nfn + facet node) in the reference's np.add.at
+   * order, and per face its tiles (macro * n_st + tile). */
+  int nc, nt;
+  const int64_t* scatter;        /* (n_sub, nn)          */
+  const double* sub_det_all;     /* (E, n_sub)           */
+  const double* sub_inv_jac_all; /* (E, n_sub, 3, 3)     */
+  const int64_t* trace_ptr;      /* (F * nt + 1)         */
+  const int64_t* trace_list;     /* (E * n_st * nfn)     */
+  const int64_t* face_ptr;       /* (F + 1)              */
+  const int64_t* face_list;      /* (E * n_st)           */
 } mhdg_tables;
 
 typedef struct mhdg_ctx mhdg_ctx;

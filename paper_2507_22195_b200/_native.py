@@ -50,6 +50,9 @@ class Tables(C.Structure):
         ("has_visc", C.c_int), ("reynolds", C.c_double), ("mach", C.c_double),
         ("prandtl", C.c_double), ("mu", C.c_double), ("minv_ref", dptr), ("pref", dptr),
         ("kref", dptr), ("eref", dptr),
+        ("nc", C.c_int), ("nt", C.c_int), ("scatter", dptr), ("sub_det_all", dptr),
+        ("sub_inv_jac_all", dptr), ("trace_ptr", dptr), ("trace_list", dptr),
+        ("face_ptr", dptr), ("face_list", dptr),
     ]
 
 

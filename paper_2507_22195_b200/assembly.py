@@ -108,6 +108,11 @@ def boundary_trace_operator(kind, state=None):
     raise InvalidConfig(f"unsupported boundary kind {kind!r}")
 
 
+# (m, p) with m > 1 on the device (mhdg_macro.cuh: the orders 5 nc of S and
+# 5 nt of the face blocks have batched Gauss-Jordan instantiations)
+MACRO_SUBDIVISIONS = {(2, 1), (2, 2), (2, 3), (3, 1)}
+
+
 class Discretization:
     """Spatial operator on a macro mesh at degree p, evaluated on the GPU.
 
@@ -126,8 +131,12 @@ class Discretization:
             raise InvalidConfig("SUPG streamline term is not on the B200 path")
         if tables is None and mesh.has_boundary and boundary is None:
             raise InvalidConfig("mesh has boundary faces, a boundary treatment is required")
-        if mesh.dim != 3 or mesh.m != 1:
-            raise InvalidConfig("the B200 operator is 3D with m = 1 macro subdivision")
+        if mesh.dim != 3:
+            raise InvalidConfig("the B200 operator is 3D")
+        if mesh.m > 1 and ((mesh.m, p) not in MACRO_SUBDIVISIONS or viscosity is not None
+                           or boundary is not None or tables is not None):
+            raise InvalidConfig(f"m > 1 on the B200 operator: (m, p) in {sorted(MACRO_SUBDIVISIONS)}, "
+                                "inviscid, periodic, single partition")
         if quad_degree not in (None, 2 * p + 1):
             raise InvalidConfig("the B200 operator uses the default quadrature degree 2p+1")
         if not 1 <= p <= 4:
@@ -183,9 +192,17 @@ class Discretization:
         tab.face_id_st = keep(t.face_id_st, np.int64)
         tab.trace_idx = keep(t.trace_idx, np.int64)
         tab.boundary_st = keep(t.boundary_st, np.uint8)
-        tab.face_sides = keep(t.face_sides, np.int64)
+        tab.face_sides = keep(t.face_sides, np.int64) if t.face_sides is not None else None
         tab.freestream = keep(boundary.state, np.float64) if boundary is not None else None
         tab.n_owned_faces = int(n_owned_faces)
+        tab.nc, tab.nt = t.layout.n_unique, t.n_trace
+        if mesh.m > 1:
+            tptr, tlist, fptr, flist = t.trace_csr()
+            tab.scatter = keep(t.layout.scatter, np.int64)
+            tab.sub_det_all = keep(t.sub_det, np.float64)
+            tab.sub_inv_jac_all = keep(t.sub_inv_jac, np.float64)
+            tab.trace_ptr, tab.trace_list = keep(tptr, np.int64), keep(tlist, np.int64)
+            tab.face_ptr, tab.face_list = keep(fptr, np.int64), keep(flist, np.int64)
         if viscosity is not None:
             if p > 3:
                 raise InvalidConfig("the viscous B200 operator supports p = 1..3")
@@ -338,7 +355,8 @@ class Discretization:
         torch = _torch()
         w = self._dev(fields.w)
         E = self.tables.mesh.n_macros
-        out = torch.empty((E, 1, self.phi.shape[0], 5), dtype=torch.float64, device=self.device)
+        out = torch.empty((E, self.layout.n_sub, self.phi.shape[0], 5), dtype=torch.float64,
+                          device=self.device)
         st = N.Status()
         rc = self._lib.mhdg_volume_quad_states(self._ctx, N.ptr(w), N.ptr(out), C.byref(st),
                                                N.stream_handle())
@@ -445,10 +463,16 @@ class Discretization:
         return v["entropy"], v["thermo_entropy"]
 
     def l2_error(self, fields, exact_fn, component=0):
+        """L2 norm of (component of u_h - exact) (assembly.py:674-684); the
+        device quadrature states, summed per sub-element in the reference's
+        order."""
         u_q = self.volume_quad_states(fields).cpu().numpy()
-        u_ex = exact_fn(self.quad_coords[:, 0])
-        diff = u_q[:, 0, :, component] - u_ex[..., component]
-        return math.sqrt(float(np.sum(self.vol_w[:, 0] * diff ** 2)))
+        total = 0.0
+        for s in range(self.layout.n_sub):
+            u_ex = exact_fn(self.quad_coords[:, s])
+            diff = u_q[:, s, :, component] - u_ex[..., component]
+            total += float(np.sum(self.vol_w[:, s] * diff ** 2))
+        return math.sqrt(total)
 
     def max_wavespeed(self, fields):
         u = self.volume_quad_states(fields).cpu().numpy()

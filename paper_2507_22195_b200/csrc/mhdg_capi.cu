@@ -17,6 +17,7 @@
 #include "mhdg_visc_fast.cuh"
 #include "mhdg_gj_blocked.cuh"
 #include "mhdg_host_mesh.cuh"
+#include "mhdg_macro.cuh"
 
 using namespace mhdg;
 
@@ -39,7 +40,24 @@ struct mhdg_ctx {
   double* d_zbuf;      // E*nm local solutions
   int* d_fb;           // Gauss-Jordan pivoting fallback: counts [2] + list
   int64_t launches;
+  int m;               // macro subdivision; m > 1 runs mhdg_macro.cuh
+  MGeo mg;             // m > 1 tables
+  double* d_cb;        // m > 1 tile-contribution buffer (E, n_st, nfn, 5)
 };
+
+// m > 1 operator (mhdg_macro_host.cuh, included at the end of this file)
+static mhdg_ctx* mm_create(const mhdg_tables* t, int device, int* err);
+static void mm_lin_sizes(const mhdg_ctx* c, int64_t sizes[6]);
+static int mm_residual_entry(mhdg_ctx* c, const double* w, const double* trace, int has_stage, double alpha,
+                             const double* offset, int check, double* r_w, double* r_trace, cudaStream_t s);
+static int mm_volume_states_entry(mhdg_ctx* c, const double* w, double* out, cudaStream_t s);
+static int mm_integrals_entry(mhdg_ctx* c, const double* w, double* out_host, cudaStream_t s);
+static int mm_linearize_entry(mhdg_ctx* c, const double* w, const double* trace, double alpha, double ptc,
+                              const mhdg_lin_buffers* L, mhdg_status* st, cudaStream_t s);
+static int mm_gemv_entry(mhdg_ctx* c, int nmat, int N, const double* A, const double* x, double* y,
+                         cudaStream_t s);
+static int mm_condensed(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, const double* x, const double* r_w,
+                        const double* r_trace, double* out, double* d_w, cudaStream_t s);
 
 static const int RED_BLOCKS = 1184;  // 148 SMs x 8, fixed for determinism
 static const int RED_THREADS = 256;
@@ -84,13 +102,14 @@ extern "C" double mhdg_match_points(int64_t n_faces, int nt, int dim, const doub
   return mhdg_host::match_points(n_faces, nt, dim, pts_nb, pts_own, match);
 }
 
-extern "C" const char* mhdg_version(void) { return "mhdg_b200 0.1 (sm_100a, fp64, m=1, P=1..4)"; }
+extern "C" const char* mhdg_version(void) { return "mhdg_b200 0.2 (sm_100a, fp64, m=1 P=1..4; m=2 P=1..3, m=3 P=1)"; }
 
 extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   int e0 = MHDG_OK;
   if (!err) err = &e0;
   *err = MHDG_OK;
-  if (t->dim != 3 || t->m != 1 || t->p < 1 || t->p > 4 || t->n_st != 4 || t->n_sub != 1) {
+  if (t->dim != 3 || t->m < 1 || t->p < 1 || t->p > 4 || t->n_st != 4 * t->m * t->m ||
+      t->n_sub != t->m * t->m * t->m) {
     *err = MHDG_INVALID_CONFIG;
     return nullptr;
   }
@@ -101,9 +120,15 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
     *err = MHDG_INVALID_CONFIG;  // non-default quadrature degree
     return nullptr;
   }
+  if (t->m > 1) return mm_create(t, device, err);
+  if (t->m != 1) {
+    *err = MHDG_INVALID_CONFIG;
+    return nullptr;
+  }
   if (cudaSetDevice(device) != cudaSuccess) { *err = MHDG_CUDA_ERROR; return nullptr; }
   mhdg_ctx* c = new mhdg_ctx();
   c->device = device;
+  c->m = 1;
   c->p = P; c->E = t->n_macros; c->F = t->n_faces;
   c->nn = NN; c->nq = NQ; c->nfn = NFN; c->nqf = NQF;
   c->n_owned = t->n_owned_faces > 0 ? t->n_owned_faces : t->n_faces;
@@ -300,6 +325,7 @@ extern "C" void mhdg_destroy(mhdg_ctx* c) {
 }
 
 extern "C" void mhdg_lin_sizes(const mhdg_ctx* c, int64_t sizes[6]) {
+  if (c->m > 1) return mm_lin_sizes(c, sizes);
   const int64_t nm = 5 * c->nn, nb = 5 * c->nfn;
   sizes[0] = (int64_t)c->E * nm * nm;
   sizes[1] = sizes[2] = sizes[3] = (int64_t)c->E * 4 * c->nqf * 25;
@@ -376,19 +402,21 @@ static int occ(K kernel, int threads, size_t smem, int cap = 32) {
   return std::min(n, cap);
 }
 
-static void decode_status(unsigned long long key, mhdg_status* st, bool admissibility) {
+// key = ((loc * 4 + sub) << 40) | macro; loc < nsub: volume sub-element loc,
+// else side tile loc - nsub (m = 1: nsub = 1)
+static void decode_status(unsigned long long key, mhdg_status* st, bool admissibility, int nsub = 1) {
   if (key == ~0ull) return;
   const int code = (int)(key >> 40);
   const int loc = code / 4, sub = code % 4;
   st->item = (int64_t)(key & ((1ull << 40) - 1));
   if (!admissibility) return;
   st->code = (sub == 0 || sub == 1) ? MHDG_NON_ADMISSIBLE_ENTROPY : MHDG_NON_ADMISSIBLE;
-  if (loc == 0) {
+  if (loc < nsub) {
     st->where_kind = 0;
-    st->where_index = 0;
+    st->where_index = loc;
   } else {
     st->where_kind = (sub == 0 || sub == 2) ? 1 : 2;
-    st->where_index = loc - 1;
+    st->where_index = loc - nsub;
   }
 }
 
@@ -431,7 +459,7 @@ extern "C" int mhdg_status_fetch(mhdg_ctx* c, mhdg_status* st, void* stream) {
   CK(cudaMemcpyAsync(&key, c->d_status, sizeof(key), cudaMemcpyDeviceToHost, S(stream)));
   CK(cudaStreamSynchronize(S(stream)));
   mhdg_status tmp = {0, 0, 0, -1, 0};
-  decode_status(key, &tmp, true);
+  decode_status(key, &tmp, true, c->m > 1 ? c->mg.nsub : 1);
   if (st) *st = tmp;
   return tmp.code;
 }
@@ -478,6 +506,7 @@ extern "C" int mhdg_residual_range(mhdg_ctx* c, const double* w, const double* t
                                    double* r_trace, double* r_q, int64_t e_begin, int64_t e_end, int zero,
                                    void* stream) {
   cudaStream_t s = S(stream);
+  if (c->m > 1) return MHDG_INVALID_CONFIG;   // partitioned runs: m = 1
   CK(cudaSetDevice(c->device));
   if (e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
   if (zero) {
@@ -507,6 +536,11 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
                              double* r_q, int sync, mhdg_status* st, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) {
+    const int rc = mm_residual_entry(c, w, trace, has_stage, alpha, offset, check, r_w, r_trace, s);
+    if (rc || !sync) return rc;
+    return mhdg_status_fetch(c, st, stream);
+  }
   CK(cudaMemsetAsync(c->d_status, 0xff, sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(r_trace, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   int rc;
@@ -754,6 +788,10 @@ static int precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* 
 extern "C" int mhdg_linearize(mhdg_ctx* c, const double* w, const double* trace, const double* q, double alpha,
                               double ptc, const mhdg_lin_buffers* L, mhdg_status* st, void* stream) {
   cudaStream_t s = S(stream);
+  if (c->m > 1) {
+    CK(cudaSetDevice(c->device));
+    return mm_linearize_entry(c, w, trace, alpha, ptc, L, st, s);
+  }
   if (c->visc && !q) return MHDG_INVALID_CONFIG;
   int rc = linearize_local(c, w, q, trace, alpha, ptc, L, s);
   if (rc) return rc;
@@ -766,6 +804,7 @@ extern "C" int mhdg_linearize_local(mhdg_ctx* c, const double* w, const double* 
                                     double alpha, double ptc, const mhdg_lin_buffers* L, mhdg_status* st,
                                     void* stream) {
   cudaStream_t s = S(stream);
+  if (c->m > 1) return MHDG_INVALID_CONFIG;
   if (c->visc && !q) return MHDG_INVALID_CONFIG;
   int rc = linearize_local(c, w, q, trace, alpha, ptc, L, s);
   if (rc) return rc;
@@ -777,6 +816,7 @@ extern "C" int mhdg_precond_factor(mhdg_ctx* c, const mhdg_lin_buffers* L, int n
                                    void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return MHDG_INVALID_CONFIG;
   CK(cudaMemsetAsync(c->d_status, 0xff, 2 * sizeof(unsigned long long), s));
   CK(cudaMemsetAsync(c->d_unsym, 0, sizeof(int), s));
   (void)n_remote;
@@ -887,6 +927,7 @@ extern "C" int mhdg_matvec_range(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
                                  int64_t e_begin, int64_t e_end, int stages, int zero, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return MHDG_INVALID_CONFIG;
   if (e_begin < 0 || e_end > c->E || e_begin > e_end) return MHDG_INVALID_CONFIG;
   if (zero) CK(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   const int e0 = (int)e_begin, e1 = (int)e_end;
@@ -909,6 +950,7 @@ extern "C" int mhdg_matvec_range(mhdg_ctx* c, const mhdg_lin_buffers* L, const d
 extern "C" int mhdg_matvec(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* x, double* y, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return mm_condensed(c, 0, L, x, nullptr, nullptr, y, nullptr, s);
   CK(cudaMemsetAsync(y, 0, sizeof(double) * (size_t)c->F * c->nfn * 5, s));
   return condensed(c, 0, L, x, nullptr, y, nullptr, s);
 }
@@ -923,6 +965,7 @@ extern "C" int mhdg_condensed_rhs(mhdg_ctx* c, const mhdg_lin_buffers* L, const 
                                   const double* r_trace, const double* r_q, double* b, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return mm_condensed(c, 1, L, nullptr, r_w, r_trace, b, nullptr, s);
   if (c->visc && !r_q) return MHDG_INVALID_CONFIG;
   const int64_t nt = (int64_t)c->F * c->nfn * 5;
   CK(cudaMemsetAsync(c->d_tmp_trace, 0, sizeof(double) * nt, s));
@@ -939,6 +982,7 @@ extern "C" int mhdg_recover(mhdg_ctx* c, const mhdg_lin_buffers* L, const double
                             const double* d_trace, double* d_w, double* d_q, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return mm_condensed(c, 2, L, d_trace, r_w, nullptr, nullptr, d_w, s);
   if (c->visc && (!r_q || !d_q)) return MHDG_INVALID_CONFIG;
   int rc = condensed(c, 2, L, d_trace, r_w, nullptr, d_w, s, r_q);
   if (rc || !c->visc) return rc;
@@ -955,6 +999,7 @@ extern "C" int mhdg_recover(mhdg_ctx* c, const mhdg_lin_buffers* L, const double
 extern "C" int mhdg_precond(mhdg_ctx* c, const mhdg_lin_buffers* L, const double* r, double* z, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return mm_gemv_entry(c, c->F, 5 * c->mg.nt, L->pinv, r, z, s);
   switch (c->p) {
     case 1: CK(launch_pdl(k_precond_apply<1, 32>, grid_for(c, c->n_owned, 32), 32, 0, s, c->n_owned, (const double*)L->pinv, r, z)); break;
     case 2: CK(launch_pdl(k_precond_apply<2, 32>, grid_for(c, c->n_owned, 32), 32, 0, s, c->n_owned, (const double*)L->pinv, r, z)); break;
@@ -972,6 +1017,10 @@ extern "C" int mhdg_precond(mhdg_ctx* c, const mhdg_lin_buffers* L, const double
 extern "C" int mhdg_volume_quad_states(mhdg_ctx* c, const double* w, double* out, mhdg_status* st, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) {
+    const int rc = mm_volume_states_entry(c, w, out, s);
+    return rc ? rc : mhdg_status_fetch(c, st, stream);
+  }
   CK(cudaMemsetAsync(c->d_status, 0xff, sizeof(unsigned long long), s));
   switch (c->p) {
     case 1: k_volume_states<1, 32><<<grid_for(c, c->E, 16), 32, 0, s>>>(c->geo, w, out, c->d_status); break;
@@ -1067,6 +1116,7 @@ extern "C" int mhdg_entropy_identity(mhdg_ctx* c, const double* w, const double*
                                      const double* r_trace, double* out_host, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return MHDG_INVALID_CONFIG;
   double* part = c->d_partial;                       // 3 x RED_BLOCKS partials
   double* res = c->d_partial + 2 * RED_BLOCKS * 5;   // 3 results
   const int nb = std::min(RED_BLOCKS, std::max(1, c->E));
@@ -1096,6 +1146,7 @@ extern "C" int mhdg_entropy_identity(mhdg_ctx* c, const double* w, const double*
 extern "C" int mhdg_integrals(mhdg_ctx* c, const double* w, double* out_host, void* stream) {
   cudaStream_t s = S(stream);
   CK(cudaSetDevice(c->device));
+  if (c->m > 1) return mm_integrals_entry(c, w, out_host, s);
   const int nblk = grid_for(c, c->E, 4);
   double* part = c->d_partial;
   double* res = c->d_partial + 2 * RED_BLOCKS * 5;
@@ -1453,4 +1504,5 @@ extern "C" double mhdg_fp64_probe(int device, void* stream) {
   return flops / (ms * 1e-3) / 1e9;
 }
 
+#include "mhdg_macro_host.cuh"
 #include "mhdg_krylov.cuh"

@@ -131,6 +131,32 @@ class HDGTables:
         # so the per-tile factor area*(d-1)! is stored and multiplied on use
         self.face_area = areas * math.factorial(d - 1)      # (E, n_st)
 
+    def trace_csr(self):
+        """Deterministic trace accumulation lists (m > 1 device path).
+
+        Returns (trace_ptr, trace_list, face_ptr, face_list): for each trace
+        entry (face * nt + node) the contribution slots (macro * n_st + tile)
+        * nfn + facet node in the reference's np.add.at order (tile, then
+        macro, then facet node: assembly.py:547), and for each face its side
+        tiles (macro * n_st + tile) in (tile, macro) order (assembly.py:
+        1012-1015)."""
+        E, nst = self.face_id_st.shape
+        nfn = self.trace_idx.shape[2]
+        e, k, j = np.meshgrid(np.arange(E), np.arange(nst), np.arange(nfn), indexing="ij")
+        ent = (self.face_id_st[:, :, None] * self.n_trace + self.trace_idx).ravel()
+        slot = ((e * nst + k) * nfn + j).ravel()
+        order = np.lexsort((j.ravel(), e.ravel(), k.ravel(), ent))
+        tlist = slot[order]
+        tptr = np.zeros(self.n_faces * self.n_trace + 1, dtype=np.int64)
+        np.cumsum(np.bincount(ent, minlength=self.n_faces * self.n_trace), out=tptr[1:])
+        e2, k2 = np.meshgrid(np.arange(E), np.arange(nst), indexing="ij")
+        fent = self.face_id_st.ravel()
+        forder = np.lexsort((e2.ravel(), k2.ravel(), fent))
+        flist = (e2 * nst + k2).ravel()[forder]
+        fptr = np.zeros(self.n_faces + 1, dtype=np.int64)
+        np.cumsum(np.bincount(fent, minlength=self.n_faces), out=fptr[1:])
+        return tptr, tlist, fptr, flist
+
     def viscous_reference(self):
         """Reference operators of the gradient equation (assembly.py:326-371)
         on the unit simplex: Mref^-1, Kref_k[j][i] = sum_q w dphi_k[q,j] phi[q,i],

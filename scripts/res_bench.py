@@ -16,26 +16,29 @@ if len(sys.argv) > 2 or (len(sys.argv) == 2 and sys.argv[1].endswith(".so") and 
 import torch  # noqa: E402
 
 sys.path.insert(0, ROOT)
-from bench import make_problem  # noqa: E402
+from bench import make_problem, stage_alpha  # noqa: E402
 from paper_2507_22195_b200.assembly import Discretization, StageContext  # noqa: E402
 from paper_2507_22195_b200.fluxes import DissipationSpec  # noqa: E402
 
-n, p, flux = 16, 3, os.environ.get("FLUX", "es")
-gas, mesh, vx, alpha = make_problem(n, p, flux)
+case = os.environ.get("CASE", "tgv")
+n, p = int(os.environ.get("NCELLS", 32)), int(os.environ.get("P", 3))
+flux = os.environ.get("FLUX", "kepes" if case == "tgv" else "es")
+gas, mesh, ic, _ = make_problem(case, n)
+alpha = stage_alpha(0.57 if case == "tgv" else 0.01)
 disc = Discretization(mesh, p=p, gas=gas, formulation="entropy", flux=DissipationSpec(flux),
                       device="cuda:0")
-fields = disc.project(vx.initial)
+fields = disc.project(ic.initial)
 stage = StageContext(alpha=alpha, offset=(-alpha * disc.volume_quad_states(fields)).contiguous())
 for _ in range(5):
     disc.residuals(fields, stage, sync=False)
 torch.cuda.synchronize()
-reps = 50
+reps = int(os.environ.get("REPS", 50))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(reps):
     r = disc.residuals(fields, stage, sync=False)
 e1.record()
 torch.cuda.synchronize()
-print(json.dumps({"lib": os.path.basename(os.environ.get("MHDG_LIB", "default")),
-                  "residual_ms": e0.elapsed_time(e1) / reps,
+print(json.dumps({"lib": os.path.basename(os.environ.get("MHDG_LIB", "default")), "case": case, "n": n,
+                  "flux": flux, "residual_ms": e0.elapsed_time(e1) / reps,
                   "checksum": float(r.r_w.abs().sum() + r.r_trace.abs().sum())}), flush=True)

@@ -302,7 +302,42 @@ def main_hsweep():
          dt=t_eval / 10.0, newton=newton)
 
 
+def main_macro():
+    """m > 1 macro subdivision: operator outputs on perturbed-
+    uniform states, 3D periodic unit box n=(2,1,1) (12 macros), for (m, p) =
+    (2,1), (2,2), (2,3), (3,1) with ES (and KEPES at (2,2)); one DIRK(3,3)
+    step of the config-1 vortex at m=2, p=2, n=2, dt=0.01."""
+    box3 = np.array([[0.0, 1.0]] * 3)
+    d00 = dirk33_tableau().d[0, 0]
+    for m, p, flux in ((2, 1, "es"), (2, 2, "es"), (2, 2, "kepes"), (2, 3, "es"), (3, 1, "es")):
+        mesh = build_box_macro_mesh(box3, (2, 1, 1), m)
+        disc = Discretization(mesh, p=p, gas=GAS, formulation="entropy", flux=DissipationSpec(flux))
+        seed = 5000 + 100 * m + 10 * p
+        fields = perturbed_uniform(disc, seed)
+        alpha = d00 / 0.01
+        offset = -alpha * disc.volume_quad_states(fields)
+        x = np.random.default_rng(seed + 1).standard_normal(fields.trace.shape)
+        out = operator_case(disc, fields, alpha, offset, 1.0, x)
+        sens = sensitivity(disc, fields, alpha, offset, 1.0, x, out)
+        save(f"macro_m{m}_k{p}_{flux}", w=fields.w, trace=fields.trace, offset=offset, alpha=alpha,
+             ptc=1.0, x=x, **out, **sens, **meta(disc, flux, "entropy", box3, (2, 1, 1), m, p))
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          angle=0.0, center=(5.0, 5.0), gas=GAS)
+    disc = Discretization(build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), 2, 2), p=2, gas=GAS,
+                          formulation="entropy", flux=DissipationSpec("es"))
+    f0 = disc.project(vx.initial)
+    integ = DIRKIntegrator(disc)
+    f1, _ = integ.run(f0, t_final=0.01, dt=0.01)
+    keys = ("entropy", "thermo_entropy", "kinetic_energy", "mass", "total_energy")
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"], r["fgmres_iters"],
+                        r["jacobian_builds"]] for r in integ.records])
+    save("macro_m2_step", w0=f0.w, trace0=f0.trace, w1=f1.w, trace1=f1.trace, newton=newton, dt=0.01,
+         integrals=np.array([[disc.integrals(f)[k] for k in keys] for f in (f0, f1)]))
+
+
 def main():
+    if "--only-macro" in sys.argv:
+        return main_macro()
     if "--only-hsweep" in sys.argv:
         return main_hsweep()
     if "--only-entropy" in sys.argv:
@@ -421,6 +456,8 @@ def main():
     main_cfg3()
     main_cfg2_step()
     main_entropy()
+    main_macro()
+    main_hsweep()
     print(f"done in {time.time() - t0:.1f} s")
 
 

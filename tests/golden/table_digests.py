@@ -28,6 +28,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "table_digests.json")
 CASES = [(n, p) for n in (4, 8, 16) for p in (1, 2, 3, 4)]
+# m > 1 macro subdivision: (n, m, p)
+MACRO_CASES = [(2, 2, 1), (2, 2, 2), (4, 2, 3), (2, 3, 1)]
 
 
 def digest(a):
@@ -57,11 +59,11 @@ def skeleton_arrays(mesh):
     return own, ownf, nb, nbf, shift, perm
 
 
-def collect(build_mesh, make_disc, n, p):
+def collect(build_mesh, make_disc, n, p, m=1):
     """build_mesh(box, n, m) -> mesh; make_disc(mesh, p) -> object exposing the
     reference's Discretization table attributes."""
     box = np.array([[0.0, 10.0]] * 3)
-    mesh = build_mesh(box, n, 1)
+    mesh = build_mesh(box, n, m)
     disc = make_disc(mesh, p)
     b, lay = disc.basis, disc.layout
     out = {}
@@ -123,9 +125,13 @@ def main():
         res[f"n{n}_p{p}"] = collect(build_box_macro_mesh,
                                     lambda mesh, p: Discretization(mesh, p), n, p)
         print("done", n, p, flush=True)
+    for n, m, p in MACRO_CASES:
+        res[f"n{n}_m{m}_p{p}"] = collect(build_box_macro_mesh,
+                                         lambda mesh, p: Discretization(mesh, p), n, p, m)
+        print("done", n, m, p, flush=True)
     with open(OUT, "w") as f:
         json.dump({"generator": "tests/golden/table_digests.py (reference macrohdg)",
-                   "box": "[[0,10]]^3 periodic, m=1", "cases": res}, f, indent=0, sort_keys=True)
+                   "box": "[[0,10]]^3 periodic", "cases": res}, f, indent=0, sort_keys=True)
 
 
 if __name__ == "__main__":

@@ -72,7 +72,7 @@ def test_unsupported_configurations_raise_invalid_config():
     box3 = np.array([[0.0, 1.0]] * 3)
     m1 = build_box_macro_mesh(box3, 1, 1)
     cases = [
-        (build_box_macro_mesh(box3, 1, 2), dict(p=2)),
+        (build_box_macro_mesh(box3, 1, 3), dict(p=2)),   # m = 3 only at p = 1
         (m1, dict(p=5)),
         (m1, dict(p=0)),
         (m1, dict(p=2, quad_degree=4)),

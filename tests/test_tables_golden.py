@@ -14,7 +14,7 @@ import os
 
 import pytest
 
-from golden.table_digests import CASES, OUT, collect
+from golden.table_digests import CASES, MACRO_CASES, OUT, collect
 
 with open(OUT) as f:
     GOLD = json.load(f)["cases"]
@@ -35,5 +35,17 @@ def test_tables_bit_exact(n, p):
     got = collect(build_box_macro_mesh, _ours, n, p)
     want = GOLD[f"n{n}_p{p}"]
     assert set(got) == set(want)
+    bad = {k: (got[k], want[k]) for k in want if got[k] != want[k]}
+    assert not bad, f"{len(bad)} tables differ from the reference: {sorted(bad)}"
+
+
+@pytest.mark.parametrize("n,m,p", MACRO_CASES)
+def test_macro_subdivision_tables_bit_exact(n, m, p):
+    """m > 1: Kuhn sub-elements, C0 macro nodes, side tiles and
+    the C0 trace space match the reference bit for bit."""
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+
+    got = collect(build_box_macro_mesh, _ours, n, p, m)
+    want = GOLD[f"n{n}_m{m}_p{p}"]
     bad = {k: (got[k], want[k]) for k in want if got[k] != want[k]}
     assert not bad, f"{len(bad)} tables differ from the reference: {sorted(bad)}"
