@@ -517,6 +517,20 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
       } else {
         const int uw = warp - NPW, nuw = NWT - NPW;
         const int pr0 = q[k0 + kq], pr1 = q[k0 + kq + 4];
+#ifndef MHDG_GJ_UREG
+#define MHDG_GJ_UREG 1
+#endif
+#if MHDG_GJ_UREG
+        // the panel's U fragments stay in registers across this warp's
+        // column tiles (they were re-read from shared memory per tile: the
+        // update loop is shared-memory-bandwidth bound)
+        double u0[T], u1[T];
+#pragma unroll
+        for (int rt = 0; rt < T; ++rt) {
+          u0[rt] = U[(rt * 2 + 0) * 32 + lane];
+          u1[rt] = U[(rt * 2 + 1) * 32 + lane];
+        }
+#endif
         int slot = 0;
         for (int ct = 0; ct < T; ++ct) {
           if (ct == pan || ct == nxt) continue;
@@ -525,7 +539,19 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
           const double r0 = pr0 >= 0 ? A[pr0 * S + c] : 0.0;
           const double r1 = pr1 >= 0 ? A[pr1 * S + c] : 0.0;
           __syncwarp();
+#if MHDG_GJ_UREG
+#pragma unroll
+          for (int rt = 0; rt < T; ++rt) {
+            double* cp = A + (rt * 8 + nr) * S + ct * 8 + kq * 2;
+            const double2 cv = *reinterpret_cast<const double2*>(cp);
+            double cc[2] = {cv.x, cv.y};
+            dmma_8x8x4(cc, u0[rt], r0);
+            dmma_8x8x4(cc, u1[rt], r1);
+            *reinterpret_cast<double2*>(cp) = make_double2(cc[0], cc[1]);
+          }
+#else
           update_tile(U, ct, r0, r1, 0, T, 1);
+#endif
         }
       }
       __syncthreads();

@@ -10,13 +10,16 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2507_22195_b200 import _native  # noqa: E402
-from bench import make_problem  # noqa: E402
+from bench import make_problem, stage_alpha  # noqa: E402
 from paper_2507_22195_b200.assembly import Discretization, StageContext  # noqa: E402
 from paper_2507_22195_b200.fluxes import DissipationSpec  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-gas, mesh, vx, alpha = make_problem(n, 3, "es")
-disc = Discretization(mesh, p=3, gas=gas, formulation="entropy", flux=DissipationSpec("es"),
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+case = sys.argv[2] if len(sys.argv) > 2 else "tgv"
+flux = "kepes" if case == "tgv" else "es"
+gas, mesh, vx, _ = make_problem(case, n)
+alpha = stage_alpha(0.57 if case == "tgv" else 0.01)
+disc = Discretization(mesh, p=3, gas=gas, formulation="entropy", flux=DissipationSpec(flux),
                       device="cuda:0")
 fields = disc.project(vx.initial)
 stage = StageContext(alpha=alpha, offset=(-alpha * disc.volume_quad_states(fields)).contiguous())
