@@ -1305,6 +1305,17 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     }
     __syncthreads();
     LIN_T(3);
+#ifndef MHDG_LIN2_FACE_FMA
+#define MHDG_LIN2_FACE_FMA 1
+#endif
+#if MHDG_LIN2_FACE_FMA
+    // face weights folded into the staged hw rows once (fw_q area_k hw_q),
+    // so each face-block term is one FMA with pf_i pf_j (was mul, mul, add)
+    for (int i = tid; i < 4 * NQF * 25; i += NT) {
+      const int k = i / (NQF * 25), q = (i / 25) % NQF;
+      sHW[i] *= sFW[q] * sGeo[22 + k];
+    }
+#endif
     for (int k = 0; k < 4; ++k) {
       __syncthreads();
       const double* sHWk = sHW + k * NQF * 25;
@@ -1317,9 +1328,16 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
 #pragma unroll 4
         for (int q = 0; q < NQF; ++q) {
           const double* pf = sPF + (k * NQF + q) * D::FS;
+#if MHDG_LIN2_FACE_FMA
+          const double pij = pf[i] * pf[j];
+#pragma unroll
+          for (int t = 0; t < 5; ++t) acc2[t] = fma(sHWk[q * 25 + s2 * 5 + t], pij, acc2[t]);
+          (void)ar;
+#else
           const double ci = (sFW[q] * ar) * pf[i], pj = pf[j];
 #pragma unroll
           for (int t = 0; t < 5; ++t) acc2[t] += (ci * sHWk[q * 25 + s2 * 5 + t]) * pj;
+#endif
         }
         const int r = sRows[k * NFN + i] * 5 + s2, c = sRows[k * NFN + j] * 5;
 #pragma unroll
