@@ -65,6 +65,7 @@ def parse(argv=None):
     ap.add_argument("--case", default="tgv", choices=sorted(CASES))
     ap.add_argument("--ncells", type=int, default=32, help="cells per axis (config 3: 32)")
     ap.add_argument("--p", type=int, default=3)
+    ap.add_argument("--m", type=int, default=1, help="macro subdivision (SURVEY f4: m = 2, 3)")
     ap.add_argument("--flux", default=None)
     ap.add_argument("--dt", type=float, default=None, help="operator linearization dt")
     ap.add_argument("--implicit-dt", type=float, default=None)
@@ -94,7 +95,7 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
-def make_problem(case, n):
+def make_problem(case, n, m=1):
     """Mesh, initial condition and viscous parameters of a BASELINE case
     (SURVEY 8d): repo objects, identical to the reference's definitions."""
     from paper_2507_22195_b200.cases import IsentropicVortex, TaylorGreen
@@ -112,7 +113,7 @@ def make_problem(case, n):
         ic = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
                               center=(5.0, 5.0), gas=gas)
         box = np.array([[0.0, 10.0]] * 3)
-    mesh = build_box_macro_mesh(box, n, 1)
+    mesh = build_box_macro_mesh(box, n, m)
     return gas, mesh, ic, visc
 
 
@@ -123,6 +124,8 @@ def stage_alpha(dt):
 
 
 def dof_units(E, F, nc, nt, viscous=False):
+    """DoF-applications per step; nc / nt are the macro C0 nodes and the
+    trace nodes per face (m > 1: the whole macro's C0 space)."""
     res = E * nc * 5 + F * nt * 5 + (E * nc * 15 if viscous else 0)
     return dict(residual=res, matvec=F * nt * 5, precond=F * nt * 5)
 
@@ -231,13 +234,13 @@ def cpu_baseline(args, steps=None, warmup=1):
     from oracle.ref_bench import time_reference
 
     return time_reference(case="vortex" if args.case == "vortex" else "tgv", n=args.cpu_sample_n,
-                          p=args.p, flux=args.flux, dt=args.dt, workers=cpu_workers(args),
+                          p=args.p, flux=args.flux, dt=args.dt, m=args.m, workers=cpu_workers(args),
                           warmup=warmup, steps=steps, budget_s=args.cpu_budget)
 
 
 def workload_name(args, E):
     return (f"{CASES[args.case][3]}, n={args.ncells} ({E} macros), k={args.p}, {args.flux}, "
-            "entropy variables, m=1; step = residual + condensed matvec + face-block precond")
+            f"entropy variables, m={args.m}; step = residual + condensed matvec + face-block precond")
 
 
 def run_reference(args, rank, world):
@@ -325,7 +328,7 @@ def run_b200(args, rank, local_rank, world):
         torch.distributed.init_process_group("nccl", device_id=dev)
 
     t_setup = time.perf_counter()
-    gas, mesh, ic, visc = make_problem(args.case, args.ncells)
+    gas, mesh, ic, visc = make_problem(args.case, args.ncells, args.m)
     disc = Discretization(mesh, p=args.p, gas=gas, formulation="entropy",
                           flux=DissipationSpec(args.flux), viscosity=visc, device=dev)
     t = disc.tables
@@ -492,7 +495,7 @@ def run_b200(args, rank, local_rank, world):
     for v in kern.values():
         v["frac"] = v["achieved"] / v["peak"]
     dom = max(kern, key=lambda k: kern[k]["ms"])
-    wl_key = f"{args.case}_n{args.ncells}_k{args.p}_{args.flux}"
+    wl_key = f"{args.case}_n{args.ncells}_k{args.p}_{args.flux}" + (f"_m{args.m}" if args.m > 1 else "")
     traffic, traffic_src = ncu_traffic(wl_key, dom)
     roofline = {"bound": kern[dom]["bound"], "achieved": kern[dom]["achieved"],
                 "peak": kern[dom]["peak"], "unit": kern[dom]["unit"], "frac": kern[dom]["frac"],

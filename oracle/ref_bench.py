@@ -48,7 +48,7 @@ def _import_ref():
     return macrohdg
 
 
-def build_sample(case, n, p, flux, dt):
+def build_sample(case, n, p, flux, dt, m=1):
     """Reference objects for the sample: (disc, fields, stage, lin, x, dofs)."""
     import numpy as np
 
@@ -63,11 +63,11 @@ def build_sample(case, n, p, flux, dt):
     gas = GasModel(1.4)
     if case == "tgv":
         ic = TaylorGreen(mach=0.1, gas=gas)
-        mesh = build_box_macro_mesh(ic.box, n, 1)
+        mesh = build_box_macro_mesh(ic.box, n, m)
     else:
         ic = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
                               center=(5.0, 5.0), gas=gas)
-        mesh = build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), n, 1)
+        mesh = build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), n, m)
     disc = Discretization(mesh, p=p, gas=gas, formulation="entropy",
                           flux=DissipationSpec(flux))
     fields = disc.project(ic.initial)
@@ -83,7 +83,7 @@ def build_sample(case, n, p, flux, dt):
 
 
 def _worker(args):
-    case, n, p, flux, dt, warmup, steps, budget_s, barrier = args
+    case, n, p, flux, dt, m, warmup, steps, budget_s, barrier = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
     try:
@@ -91,7 +91,7 @@ def _worker(args):
         limiter = threadpool_limits(1)
     except Exception:   # threadpoolctl absent: env vars above still apply to new pools
         limiter = None
-    disc, fields, stage, lin, x, dofs, E = build_sample(case, n, p, flux, dt)
+    disc, fields, stage, lin, x, dofs, E = build_sample(case, n, p, flux, dt, m)
 
     def step():
         disc.residuals(fields, stage)
@@ -116,19 +116,19 @@ def _worker(args):
 
 
 def time_reference(case="tgv", n=4, p=3, flux="kepes", dt=0.57, workers=1, warmup=1,
-                   steps=None, budget_s=10.0):
+                   steps=None, budget_s=10.0, m=1):
     """Run `workers` concurrent copies; returns the throughput summary."""
     if not ref_available():
         raise RuntimeError("oracle/_ref missing: run oracle/build_ref.sh in the build container")
     if workers <= 1:
-        r = _worker((case, n, p, flux, dt, warmup, steps, budget_s, None))
+        r = _worker((case, n, p, flux, dt, m, warmup, steps, budget_s, None))
         res = [r]
     else:
         ctx = mp.get_context("spawn")
         mgr = ctx.Manager()
         barrier = mgr.Barrier(workers)
         with ctx.Pool(workers) as pool:
-            res = pool.map(_worker, [(case, n, p, flux, dt, warmup, steps, budget_s, barrier)] *
+            res = pool.map(_worker, [(case, n, p, flux, dt, m, warmup, steps, budget_s, barrier)] *
                            workers)
     total = sum(r["dofs"] * r["steps"] for r in res)
     span = max(r["seconds"] for r in res)
@@ -137,7 +137,7 @@ def time_reference(case="tgv", n=4, p=3, flux="kepes", dt=0.57, workers=1, warmu
                 seconds_per_step=span / min(steps_each), steps=steps_each, span_s=span,
                 sample=(f"unmodified reference macrohdg (oracle/_ref) residual+matvec+precond, "
                         f"{'Taylor-Green M=0.1' if case == 'tgv' else 'isentropic vortex'} "
-                        f"n={n} sub-mesh ({res[0]['macros']} macros) k={p} {flux}, "
+                        f"n={n} sub-mesh ({res[0]['macros']} macros) k={p} m={m} {flux}, "
                         f"{workers} concurrent single-threaded copies, "
                         f"{sum(steps_each)} steps over {span:.1f} s"))
 
