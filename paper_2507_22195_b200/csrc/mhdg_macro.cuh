@@ -526,19 +526,29 @@ mm_face_out(MGeo g, const double* __restrict__ hh, const double* __restrict__ hw
   }
 }
 
-// y_m = A_m x_m for nmat column-major N x N matrices (S^-1, face-block inverses)
-__global__ void __launch_bounds__(128)
+// y_m = A_m x_m for nmat column-major N x N matrices (S^-1, face-block
+// inverses): one row per thread (blockDim >= N), four independent
+// accumulators over the columns so each thread keeps four streaming loads in
+// flight; the columns' loads are coalesced across the rows.
+__global__ void __launch_bounds__(512)
 mm_gemv(int nmat, int N, const double* __restrict__ A, const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(16) double sx[];
   for (int m = blockIdx.x; m < nmat; m += gridDim.x) {
     __syncthreads();
-    for (int i = threadIdx.x; i < N; i += 128) sx[i] = x[(size_t)m * N + i];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sx[i] = x[(size_t)m * N + i];
     __syncthreads();
     const double* Am = A + (size_t)m * N * N;
-    for (int r = threadIdx.x; r < N; r += 128) {
-      double acc = 0.0;
-      for (int c = 0; c < N; ++c) acc += Am[(size_t)c * N + r] * sx[c];
-      y[(size_t)m * N + r] = acc;
+    for (int r = threadIdx.x; r < N; r += blockDim.x) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int c = 0;
+      for (; c + 3 < N; c += 4) {
+        a0 += __ldcs(Am + (size_t)c * N + r) * sx[c];
+        a1 += __ldcs(Am + (size_t)(c + 1) * N + r) * sx[c + 1];
+        a2 += __ldcs(Am + (size_t)(c + 2) * N + r) * sx[c + 2];
+        a3 += __ldcs(Am + (size_t)(c + 3) * N + r) * sx[c + 3];
+      }
+      for (; c < N; ++c) a0 += __ldcs(Am + (size_t)c * N + r) * sx[c];
+      y[(size_t)m * N + r] = (a0 + a1) + (a2 + a3);
     }
   }
 }
