@@ -79,6 +79,9 @@ def parse(argv=None):
                     help="N>1: independent replicas instead of the partitioned operator")
     ap.add_argument("--partitioned", action="store_true",
                     help="use the partitioned operator also at N=1 (exchange-free)")
+    ap.add_argument("--orth", default="mgs", choices=["mgs", "cgs2"],
+                    help="partitioned runs: FGMRES orthogonalization (mgs = the reference's "
+                         "order; cgs2 = opt-in, 3 all-reduces per Arnoldi step)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="partitioned runs: gloo stages the halo through host memory "
                          "(several ranks may then share one GPU)")
@@ -600,7 +603,7 @@ def run_b200_partitioned(args, rank, local_rank, world):
     full = HDGTables(mesh, args.p)
     pdisc = PartitionedDiscretization(mesh, args.p, rank, world, device=dev, full_tables=full,
                                       gas=gas, formulation="entropy", viscosity=visc,
-                                      flux=DissipationSpec(args.flux))
+                                      flux=DissipationSpec(args.flux), orthogonalization=args.orth)
     disc = pdisc.local
     t = disc.tables
     part = pdisc.part
@@ -727,7 +730,8 @@ def run_b200_partitioned(args, rank, local_rank, world):
                     "fgmres_inner": sum(r["inner_iters_total"] for r in rec),
                     "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
                     "dt": args.implicit_dt, "tableau": "DIRK(3,3)",
-                    "halvings": integ.halvings, "krylov": "host loop (distributed dots)"}
+                    "halvings": integ.halvings,
+                    "krylov": f"host loop (distributed dots, {args.orth})"}
     peaks = load_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     nqf = t.fphi.shape[0]

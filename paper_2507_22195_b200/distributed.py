@@ -73,7 +73,10 @@ def collective(exchange, fn, rank=0):
 
 class PartitionedDiscretization:
     def __init__(self, mesh, p, rank, world, exchange=None, device=None, full_tables=None,
-                 **kw):
+                 orthogonalization="mgs", **kw):
+        if orthogonalization not in ("mgs", "cgs2"):
+            raise ValueError("orthogonalization must be 'mgs' (reference order) or 'cgs2'")
+        self.orthogonalization = orthogonalization
         full = full_tables if full_tables is not None else HDGTables(mesh, p)
         self.part = LocalPartition(full, rank, world)
         self.local = Discretization(mesh, p, device=device, tables=self.part.tables,
@@ -196,7 +199,7 @@ class PartitionedLinearizedSystem:
         self.pdisc = pdisc
         d = pdisc.local
         self.disc = d
-        self.vectors = DistVectors(pdisc)
+        self.vectors = DistVectors(pdisc, orth=getattr(pdisc, "orthogonalization", "mgs"))
         self.trace_shape = tuple(d._dev(fields.trace).shape)
         # local linearization without the preconditioner ...
         self.lin = LinearizedSystem.__new__(LinearizedSystem)
@@ -296,9 +299,16 @@ class DistVectors:
     """FGMRES vector operations for one rank: element-wise work on the whole
     local vector (ghost rows are carried along and never read), inner
     products on the owned rows only followed by an all-reduce.  MGS therefore
-    needs one all-reduce per basis vector (the reference's MGS order)."""
+    needs one all-reduce per basis vector (the reference's MGS order).
 
-    def __init__(self, pdisc, inner=None):
+    orth = "cgs2" (opt-in, reported separately; SURVEY 7 hard part 7):
+    classical Gram-Schmidt applied twice, h = V^T w as j+1 local dots and ONE
+    all-reduce per pass, w -= V h as one combine; 3 all-reduces per Arnoldi
+    step instead of j+2.  Same Krylov space, different rounding, so the
+    iteration counts may differ from the reference's MGS in the last
+    iteration near a tolerance."""
+
+    def __init__(self, pdisc, inner=None, orth="mgs"):
         from .solver import DeviceVectors
 
         self.inner = inner if inner is not None else DeviceVectors(pdisc.local)
@@ -307,6 +317,7 @@ class DistVectors:
         t = pdisc.local.tables
         self.n_owned = pdisc.part.n_owned * t.fphi.shape[1] * 5
         self.h = self.torch.zeros(66, dtype=self.torch.float64, device=pdisc.device)
+        self.orth = orth
         import torch.distributed as dist
 
         part = pdisc.part
@@ -330,7 +341,30 @@ class DistVectors:
     def combine(self, Z, k, y, x):
         self.inner.combine(Z, k, y, x)
 
+    def _cgs2(self, V, j, w):
+        torch = self.torch
+        k = j + 1
+        if self.h.numel() < 2 * (k + 1):
+            self.h = torch.zeros(2 * (k + 2), dtype=torch.float64, device=self.h.device)
+        tot = torch.zeros(k, dtype=torch.float64, device=self.h.device)
+        tmp = self.h[:k]
+        for _ in range(2):
+            for i in range(k):
+                self.inner.dot_into(V[i][: self.n_owned], w[: self.n_owned], tmp[i:i + 1])
+            self.exchange.allreduce_sum(tmp)
+            self.inner.combine_dev(V, k, -tmp, w)     # w -= V^T h
+            tot += tmp
+        hn = self.h[k:k + 1]
+        self._dot_dev(w, w, hn)
+        col = torch.cat([tot, hn]).cpu().numpy().copy()
+        col[j + 1] = math.sqrt(col[j + 1])
+        if col[j + 1] > 1e-300:
+            self.inner.div_into(w, col[j + 1], V[j + 1])
+        return col
+
     def mgs(self, V, j, w):
+        if self.orth == "cgs2":
+            return self._cgs2(V, j, w)
         if self.single:   # one rank, no ghost rows: the fused single-device MGS
             return self.inner.mgs(V, j, w)
         if self.h.numel() < j + 2:   # grown with the restart length (no fixed cap)

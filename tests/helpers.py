@@ -50,6 +50,9 @@ class CPUVectors:
     def axpy_dev(self, a, x, y):
         y.sub_(a[0] * x)
 
+    def combine_dev(self, Z, k, y, x):
+        x.add_(y[:k] @ Z[:k])
+
     def combine(self, Z, k, yv, x):
         x.add_(torch.from_numpy(np.ascontiguousarray(yv[:k])) @ Z[:k])
 

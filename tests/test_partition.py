@@ -144,6 +144,13 @@ def _worker(rank, world, port, flux, results):
                                    x.ravel(), rel_tol=1e-8, restart=15, max_iters=60)
         xd = res.x.view(shape).numpy()[: part.n_owned]
         err_x = float(np.abs(xd - xr.reshape(tr.shape)[own]).max() / np.abs(xr).max())
+        # opt-in CGS2 (3 all-reduces per Arnoldi step): same solution
+        vec2 = DistVectors(pdisc, inner=CPUVectors(), orth="cgs2")
+        res2 = solver.fgmres(dop, b, rel_tol=1e-8, restart=15, max_iters=60,
+                             raise_on_stagnation=False, vec=vec2)
+        xd2 = res2.x.view(shape).numpy()[: part.n_owned]
+        err_cgs2 = (abs(res2.iterations - it_ref),
+                    float(np.abs(xd2 - xr.reshape(tr.shape)[own]).max() / np.abs(xr).max()))
         # remote face sides for the face-block preconditioner: every rank
         # takes part, including one that owns no halo face
         nqf = t.fphi.shape[0]
@@ -152,7 +159,7 @@ def _worker(rank, world, port, flux, results):
         got = ex.gather_sides(hh_loc, nqf).numpy()
         ok_sides = np.array_equal(got, hh_glob[part.remote_side_ids])
         results[rank] = (ok_res and ok_sides, ok_fill, err_mv, res.iterations, it_ref, err_x,
-                         part.n_remote_sides)
+                         part.n_remote_sides, err_cgs2)
     finally:
         dist.destroy_process_group()
 
@@ -167,7 +174,8 @@ def test_gloo_world2_partitioned_operator_and_fgmres(flux):
                        join=True, start_method="spawn")
     assert min(results[r][6] for r in range(world)) == 0, "one rank should own no halo face"
     for rank in range(world):
-        ok_res, ok_fill, err_mv, it, it_ref, err_x, _ = results[rank]
+        ok_res, ok_fill, err_mv, it, it_ref, err_x, _, err_cgs2 = results[rank]
+        assert err_cgs2[0] <= 1 and err_cgs2[1] <= 1e-7, err_cgs2
         assert ok_res, "partitioned residual must be bit-identical"
         assert ok_fill
         assert err_mv <= 1e-14
