@@ -45,7 +45,7 @@ try:
 except (OSError, ValueError):
     pass
 HBM = float(peaks.get("hbm_gbs", 6650.0))
-FP64 = N.fp64_probe(0) / 1e3
+FP64 = max(N.fp64_probe(0), N.dmma_probe(0)) / 1e3   # the larger of the FMA and DMMA probes
 
 
 def perturbed_uniform(disc, seed):
@@ -96,6 +96,8 @@ for p in [int(x) for x in a.degrees.split(",")]:
     nq, nqf = (p + 1) ** 3, (p + 1) ** 2
     NM, NB = 5 * nc, 5 * nt
     r_ms = dev_time(lambda: disc.residuals(fields, stage, check=False, sync=False), a.reps)
+    lin = disc.jacobian(fields, stage, ptc_weight=1.0)   # warm (allocations)
+    del lin
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     lin = disc.jacobian(fields, stage, ptc_weight=1.0)
