@@ -614,6 +614,38 @@ static int gj_lookahead(mhdg_ctx* c, int nmat, double* mats, unsigned long long*
   }
   return MHDG_OK;
 }
+// the lookahead Gauss-Jordan with its working matrices in per-CTA global
+// slabs (L2-resident: 2 CTAs per SM x 259 KB at N = 175), same two passes
+#ifndef MHDG_GJ_GA
+#define MHDG_GJ_GA 1
+#endif
+template <int N>
+static int gj_lookahead_ga(mhdg_ctx* c, int nmat, double* mats, unsigned long long* status, cudaStream_t s,
+                           int slot) {
+  constexpr int NWT = MHDG_GJ_NWT, NPW = MHDG_GJ_NPW;
+  using GL = GJLA2<N, NWT, NPW>;
+  const size_t smem = GL::bytes_ga;
+  if (set_smem(k_gj_la2<N, NWT, NPW, false, true>, smem)) return MHDG_CUDA_ERROR;
+  if (set_smem(k_gj_la2<N, NWT, NPW, true, true>, smem)) return MHDG_CUDA_ERROR;
+  const int grid = grid_for(c, nmat, std::min(2, occ(k_gj_la2<N, NWT, NPW, true, true>, GL::NT, smem)));
+  const size_t need = (size_t)grid * GL::slab * sizeof(double);
+  if (need > c->scratch_bytes) {
+    if (c->d_scratch) cudaFree(c->d_scratch);
+    c->d_scratch = nullptr;
+    if (cudaMalloc(&c->d_scratch, need) != cudaSuccess) return MHDG_OUT_OF_MEMORY;
+    c->scratch_bytes = need;
+  }
+  int* cnt = c->d_fb + slot;
+  int* list = c->d_fb + 2;
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+  GjPass p1{nullptr, nullptr, cnt, list, c->d_scratch}, p2{list, cnt, nullptr, nullptr, c->d_scratch};
+  k_gj_la2<N, NWT, NPW, true, true><<<grid, GL::NT, smem, s>>>(nmat, mats, status, p1);
+  k_gj_la2<N, NWT, NPW, false, true><<<grid, GL::NT, smem, s>>>(0, mats, status, p2);
+  c->launches += 1;
+  CK(cudaGetLastError());
+  return MHDG_OK;
+}
+
 template <int P>
 static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, const double* tr, double weight,
                              double ptc, const mhdg_lin_buffers* L, cudaStream_t s) {
@@ -642,7 +674,28 @@ static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, cons
     c->launches++;
   }
   constexpr int NM = Dims<P>::NM;
-  if (gj_lookahead<NM>(c, c->E, L->sinv, c->d_status, s, 0)) return MHDG_CUDA_ERROR;
+  if constexpr (Lin2<P>::GS) {
+    if (MHDG_GJ_GA) {
+      c->launches++;
+      return gj_lookahead_ga<NM>(c, c->E, L->sinv, c->d_status, s, 0);
+    }
+    // k = 4: the blocked Gauss-Jordan with its working matrix in an
+    // L2-resident global slab per CTA (NM = 175 does not fit shared memory)
+    using GB = GJB<NM>;
+    const size_t gsm = GB::bytes_gm;
+    if (set_smem(k_gj_blocked<NM, true>, gsm)) return MHDG_CUDA_ERROR;
+    const int ggrid = grid_for(c, c->E, std::min(2, occ(k_gj_blocked<NM, true>, GB::NT, gsm)));
+    const size_t slabs = (size_t)ggrid * GB::slab * sizeof(double);
+    if (slabs > c->scratch_bytes) {
+      if (c->d_scratch) cudaFree(c->d_scratch);
+      c->d_scratch = nullptr;
+      if (cudaMalloc(&c->d_scratch, slabs) != cudaSuccess) return MHDG_OUT_OF_MEMORY;
+      c->scratch_bytes = slabs;
+    }
+    k_gj_blocked<NM, true><<<ggrid, GB::NT, gsm, s>>>(c->E, L->sinv, c->d_status, c->d_scratch);
+  } else if (gj_lookahead<NM>(c, c->E, L->sinv, c->d_status, s, 0)) {
+    return MHDG_CUDA_ERROR;
+  }
   (void)ptc;
   c->launches++;
   CK(cudaGetLastError());
@@ -771,6 +824,10 @@ static int linearize_local(mhdg_ctx* c, const double* w, const double* q, const 
     case 3: return launch_linearize2<3>(c, w, q, trace, weight, ptc, L, s);
     default:
       if (c->visc) return MHDG_INVALID_CONFIG;   // viscous k = 4 not on the device yet
+#ifndef MHDG_LIN_K4_V2
+#define MHDG_LIN_K4_V2 1
+#endif
+      if (MHDG_LIN_K4_V2) return launch_linearize2<4>(c, w, q, trace, weight, ptc, L, s);
       return launch_linearize<4, 512>(c, w, trace, weight, ptc, L, s);
   }
 }

@@ -227,6 +227,8 @@ struct GJLA2 {
   static constexpr int NT = 32 * NWT;
   static constexpr int UF = T * 2 * 32;
   static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 16 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
+  static constexpr size_t bytes_ga = (size_t)(2 * UF + 16 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
+  static constexpr size_t slab = (size_t)NP * S;   // doubles per CTA (GA)
 };
 
 #ifndef MHDG_GJ_TILE_STORE
@@ -277,16 +279,22 @@ struct GjPass {
   const int* count_dev;  // length of list (device), when list != nullptr
   int* fb_count;         // nopiv pass: fallback list length
   int* fb_list;          // nopiv pass: fallback matrix ids
+  double* slab = nullptr;   // GA: per-CTA global working matrices (NP x S each)
 };
 
-template <int N, int NWT, int NPW, class Src, bool NOPIV = false>
+// GA: the working matrix lives in a per-CTA global slab (L2-resident) instead
+// of shared memory, for orders whose matrix does not fit (k = 4: N = 175,
+// 259 KB); the U panels, pivot data and everything else stay in shared
+// memory.  Within one SM the global accesses of the CTA's warps are coherent
+// through L1 after the CTA barriers.
+template <int N, int NWT, int NPW, class Src, bool NOPIV = false, bool GA = false>
 __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats, unsigned long long* status,
                                             const Src& src, GjPass pass = GjPass{nullptr, nullptr, nullptr, nullptr}) {
   using L = GJLA2<N, NWT, NPW>;
   constexpr int NP = L::NP, S = L::S, T = L::T, NPAN = L::NPAN, RPL = L::RPL, NT = L::NT;
   extern __shared__ __align__(16) double smem[];
-  double* A = smem;                        // NP x S
-  double* Ub = A + NP * S;                 // 2 x UF
+  double* A = GA ? pass.slab + (size_t)blockIdx.x * NP * S : smem;   // NP x S
+  double* Ub = GA ? smem : A + NP * S;     // 2 x UF
   double* sProw = Ub + 2 * L::UF;          // 2 x 8: pivot row of the current step
   unsigned* sCand = reinterpret_cast<unsigned*>(sProw + 16);  // [NPW][3]: hi, lo, row
   int* q = (int*)(sCand + 4 * NPW);        // NP: pivot row of step k
@@ -485,7 +493,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
     }
   };
 
-  double* ex = smem + (L::bytes + 15) / 16 * 2;   // the source's scratch
+  double* ex = smem + ((GA ? L::bytes_ga : L::bytes) + 15) / 16 * 2;   // the source's scratch
   src.init(ex, tid, NT);
   if (pass.list) nmat = *pass.count_dev;
   for (int mi = blockIdx.x; mi < nmat; mi += gridDim.x) {
@@ -604,10 +612,10 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
   }
 }
 
-template <int N, int NWT, int NPW, bool NOPIV = false>
+template <int N, int NWT, int NPW, bool NOPIV = false, bool GA = false>
 __global__ void __launch_bounds__(GJLA2<N, NWT, NPW>::NT, (N < 64 ? MHDG_GJ_MINB_SMALL : 2))
 k_gj_la2(int nmat, double* __restrict__ mats, unsigned long long* status, GjPass pass) {
-  gj_la2_body<N, NWT, NPW, GjGlobalSrc<N>, NOPIV>(nmat, mats, status, GjGlobalSrc<N>{mats}, pass);
+  gj_la2_body<N, NWT, NPW, GjGlobalSrc<N>, NOPIV, GA>(nmat, mats, status, GjGlobalSrc<N>{mats}, pass);
 }
 
 // K4 face blocks assembled in place (assembly.py:994-1026): the face block

@@ -997,31 +997,40 @@ __device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, doub
 #endif
 // C row kk rotated by 4 kk columns: a half-warp's stage-1 B-fragment loads
 // (four kk rows x four columns) then hit 16 distinct bank pairs
-#define LIN2_CI(kk, col) ((kk) * CS + (MHDG_LIN2_PAD ? (((col) + 4 * (kk)) & 31) : (col)))
+#define LIN2_CI(kk, col) ((kk) * CS + (L::ROT ? (((col) + 4 * (kk)) & 31) : (col)))
 #ifndef MHDG_LIN2_NW
 #define MHDG_LIN2_NW 8   // 10 warps (whole dual passes) measured slower: 168-register cap spills
 #endif
+// k = 4 (NM = 175): S (245 KB) does not fit shared memory; it is assembled
+// in place in the S^-1 buffer (GS: L2-resident per CTA, the blocked
+// Gauss-Jordan inverts it there), C rows are unpadded (CS = 25, the
+// st >= 25 fragment lanes read 0) and the (st, i-tile) pairs run in two
+// passes so that the stage-2 accumulators fit the register file.
 template <int P>
 struct Lin2 {
   using D = Dims<P>;
+  static constexpr bool GS = (size_t)D::NM * D::NM * 8 > 100 * 1024;   // S in global memory
+  static constexpr bool ROT = MHDG_LIN2_PAD && !GS;    // rotated C rows (needs CS = 32)
   static constexpr int NW = MHDG_LIN2_NW, NT = 32 * NW;
   static constexpr int NNP = (D::NN + 7) / 8 * 8;      // padded nodes
   static constexpr int IT = NNP / 8;                    // node tiles
   static constexpr int QC = 8;                          // q chunk (2 k-steps)
   static constexpr int NCH = (D::NQ + QC - 1) / QC;
-  static constexpr int CS = 32;                          // C row (st padded)
+  static constexpr int CS = GS ? 25 : 32;                // C row (st padded)
   // D row stride (doubles): NNP + 4, so the stage-1 stores of the four
   // (lane & 3) st columns and the stage-2 loads of the four q rows fall on
   // distinct bank pairs (NNP = 0 mod 8 put all four on one)
   static constexpr int DS = MHDG_LIN2_PAD ? NNP + 4 : NNP;
   static constexpr int NPAIR = 25 * IT;                  // (st, i-tile) pairs
-  static constexpr int PPW = (NPAIR + NW - 1) / NW;      // pairs per warp
+  static constexpr int NPASS = GS ? 2 : 1;               // passes over the pairs
+  static constexpr int PPW = ((NPAIR + NW - 1) / NW + NPASS - 1) / NPASS;   // pairs per warp and pass
   // shared memory (doubles)
-  static constexpr int S_ = D::NM * D::NM;
+  static constexpr int S_ = GS ? 0 : D::NM * D::NM;
   static constexpr int C_ = D::NQ * 4 * CS;
   static constexpr int DD_ = QC * 25 * DS;
   static constexpr int doubles = S_ + C_ + DD_ + D::NN * 5 + 4 * D::NFN * 5 + 4 * D::NQF * D::FS +
-                                 D::NQF * D::FS + D::NQ + D::NQF + 4 * D::NQF * 25 + 4 * D::NM + 32;
+                                 D::NQF * D::FS + D::NQ + D::NQF + 4 * D::NQF * 25 +
+                                 (GS ? 0 : 4 * D::NM) + 32;
   static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + 2 * D::NM + 4;
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4 + 16 + D::NN * 15 * 8;
 };
@@ -1037,8 +1046,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
   constexpr int NN = D::NN, NQ = D::NQ, NM = D::NM, NFN = D::NFN, NQF = D::NQF;
   constexpr int NT = L::NT, QC = L::QC, CS = L::CS, IT = L::IT;
   extern __shared__ __align__(16) double smem[];
-  double* S = smem;                          // NM*NM
-  double* sC = S + L::S_;                    // NQ*4*CS
+  double* const sS = smem;                   // NM*NM (GS: none)
+  double* sC = sS + L::S_;                   // NQ*4*CS
   double* sD = sC + L::C_;                   // QC*25*DS   [qq][st][i]
   double* sW = sD + L::DD_;                  // NN*5
   double* sTR = sW + NN * 5;                 // 4*NFN*5
@@ -1047,9 +1056,9 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
   double* sQW = sFP + NQF * D::FS;           // NQ
   double* sFW = sQW + NQ;                    // NQF
   double* sHW = sFW + NQF;                   // 4*NQF*25 (all tiles)
-  double* sCol = sHW + 4 * NQF * 25;         // 2*NM
-  double* sRow = sCol + 2 * NM;              // 2*NM
-  double* sGeo = sRow + 2 * NM;              // 32
+  double* sCol = sHW + 4 * NQF * 25;         // 2*NM (GS: none)
+  double* sRow = sCol + (L::GS ? 0 : 2 * NM);
+  double* sGeo = sRow + (L::GS ? 0 : 2 * NM);   // 32
   int* sRows = (int*)(sGeo + 32);
   int* sFid = sRows + 4 * NFN;
   int* sTid = sFid + 4;
@@ -1076,7 +1085,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
 #define LIN_T(k) do { } while (0)
 #endif
   for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
-    if (tid == 0) bulk_wait_read();   // previous macro's S left shared memory
+    double* const S = L::GS ? sinv + (size_t)e * NM * NM : sS;
+    if (!L::GS && tid == 0) bulk_wait_read();   // previous macro's S left shared memory
     __syncthreads();
     for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
     if (VISC)
@@ -1145,6 +1155,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     __syncthreads();
     LIN_T(1);
     // ---- S volume blocks on the tensor cores
+    for (int pass = 0; pass < L::NPASS; ++pass) {
     double acc[L::PPW][IT][2];
 #pragma unroll
     for (int c = 0; c < L::PPW; ++c)
@@ -1162,7 +1173,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           const double a = (q < NQ && i < NN) ? __ldg(Bt + ((size_t)q * 4 + kk) * NN + i) : 0.0;
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) {
-            const double b = q < NQ ? sC[(size_t)q * 4 * CS + LIN2_CI(kk, nt * 8 + r8)] : 0.0;
+            const double b = (q < NQ && (!L::GS || nt * 8 + r8 < 25))
+                                 ? sC[(size_t)q * 4 * CS + LIN2_CI(kk, nt * 8 + r8)] : 0.0;
             double c2[2] = {0.0, 0.0};
             dmma_8x8x4(c2, a, b);
             const int ii = itl * 8 + r8, st0 = nt * 8 + (lane & 3) * 2;
@@ -1185,7 +1197,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         }
 #pragma unroll
         for (int c = 0; c < L::PPW; ++c) {
-          const int pr = warp + L::NW * c;
+          const int pr = warp + L::NW * (pass * L::PPW + c);
           if (pr < L::NPAIR) {
             const int st = pr / IT, itl = pr % IT;
             const double a = sD[((size_t)qq * 25 + st) * L::DS + itl * 8 + (lane >> 2)];
@@ -1199,7 +1211,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     // scatter the accumulators into S[(i,s)][(j,t)]
 #pragma unroll
     for (int c = 0; c < L::PPW; ++c) {
-      const int pr = warp + L::NW * c;
+      const int pr = warp + L::NW * (pass * L::PPW + c);
       if (pr < L::NPAIR) {
         const int st = pr / IT, itl = pr % IT, s2 = st / 5, t = st % 5;
         const int i = itl * 8 + (lane >> 2);
@@ -1212,6 +1224,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           }
       }
     }
+    }   // pass
     // ---- face tiles: hw, hhat, hh tensors of all four tiles in one pass,
     //      then the S face blocks tile by tile (fixed accumulation order)
     __syncthreads();
@@ -1345,13 +1358,15 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
       }
     }
     // ---- S (row-major) to the S^-1 buffer with one TMA bulk store (80 KB at
-    //      k = 3); k_gj_blocked inverts it in place
-    fence_proxy_async();
-    __syncthreads();
-    LIN_T(4);
-    if (tid == 0) bulk_s2g(sinv + (size_t)e * NM * NM, S, (uint32_t)(NM * NM * sizeof(double)));
+    //      k = 3); the Gauss-Jordan inverts it in place (GS: already there)
+    if (!L::GS) {
+      fence_proxy_async();
+      __syncthreads();
+      LIN_T(4);
+      if (tid == 0) bulk_s2g(sinv + (size_t)e * NM * NM, S, (uint32_t)(NM * NM * sizeof(double)));
+    }
   }
-  if (tid == 0) bulk_wait_all();
+  if (!L::GS && tid == 0) bulk_wait_all();
 }
 
 // ===========================================================================
