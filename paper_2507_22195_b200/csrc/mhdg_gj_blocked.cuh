@@ -653,11 +653,7 @@ struct FaceBlockSrc {
     double* sArea = sRed + 2 * (NT / 32);
     int* sT = reinterpret_cast<int*>(sArea + 2);
     const int lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < NB * NB; i += nt) A[(i / NB) * S + i % NB] = 0.0;
-    // both sides staged at once; every entry of the block receives exactly
-    // one term per side (tidx is a bijection per side), so the two sides'
-    // shared-memory atomics add x + y onto a zero in either order and the
-    // block is bit-identical to the side-by-side accumulation
+    // both sides staged at once
     for (int side = 0; side < 2; ++side) {
       const int st = g.fsides[f * 2 + side];
       double* hs = sHH + side * NQF * 25;
@@ -675,41 +671,55 @@ struct FaceBlockSrc {
       }
     }
     __syncthreads();
-    // a warp owns whole (side, M tile) tasks: the A fragment (a table entry)
-    // of each K step feeds the four N tiles' independent accumulator chains
-    for (int task = warp; task < 2 * WMT; task += NT / 32) {
-      const int side = task & 1, mt = task >> 1;
+    // the sides one after the other, a warp per M tile: every entry of the
+    // block receives exactly one term per side (tidx is a bijection per
+    // side), so the first present side stores and the second adds: the
+    // block is (term0) + term1, bit-identical to the former shared-memory
+    // atomics onto zero (whose two orders give the same IEEE sum) without
+    // their serialisation, and no zero fill is needed (padding rows and
+    // columns of A stay zero from the kernel start)
+    const bool has0 = g.fsides[f * 2] != -1;
+#pragma unroll 1
+    for (int side = 0; side < 2; ++side) {
       if (g.fsides[f * 2 + side] == -1) continue;
+      const bool first = side == 0 || !has0;
       const double* hs = sHH + side * NQF * 25;
       const int* ts = sT + side * NFN;
       const double area = sArea[side];
-      const int ija = mt * 8 + (lane >> 2);
-      const bool rowok = ija < NFN * NFN;
-      const int ia = rowok ? ija / NFN : 0, ja = rowok ? ija % NFN : 0;
-      double c[WNT][2];
+      for (int mt = warp; mt < WMT; mt += NT / 32) {
+        const int ija = mt * 8 + (lane >> 2);
+        const bool rowok = ija < NFN * NFN;
+        const int ia = rowok ? ija / NFN : 0, ja = rowok ? ija % NFN : 0;
+        double c[WNT][2];
 #pragma unroll
-      for (int ntl = 0; ntl < WNT; ++ntl) c[ntl][0] = c[ntl][1] = 0.0;
+        for (int ntl = 0; ntl < WNT; ++ntl) c[ntl][0] = c[ntl][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < WKS; ++ks) {
-        const int qa = ks * 4 + (lane & 3);
-        const double a = (rowok && qa < NQF) ? (sFw[qa] * sFP[qa * NFN + ia]) * sFP[qa * NFN + ja] : 0.0;
+        for (int ks = 0; ks < WKS; ++ks) {
+          const int qa = ks * 4 + (lane & 3);
+          const double a = (rowok && qa < NQF) ? (sFw[qa] * sFP[qa * NFN + ia]) * sFP[qa * NFN + ja] : 0.0;
 #pragma unroll
-        for (int ntl = 0; ntl < WNT; ++ntl) {
-          const int n = ntl * 8 + (lane >> 2);
-          const double b = (qa < NQF && n < 25) ? hs[qa * 25 + n] : 0.0;
-          dmma_8x8x4(c[ntl], a, b);
+          for (int ntl = 0; ntl < WNT; ++ntl) {
+            const int n = ntl * 8 + (lane >> 2);
+            const double b = (qa < NQF && n < 25) ? hs[qa * 25 + n] : 0.0;
+            dmma_8x8x4(c[ntl], a, b);
+          }
+        }
+        if (rowok) {
+          const int rb = ts[ia] * 5, cb = ts[ja] * 5;
+#pragma unroll
+          for (int ntl = 0; ntl < WNT; ++ntl)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int st2 = ntl * 8 + (lane & 3) * 2 + h2;
+              if (st2 < 25) {
+                double* dst = &A[(rb + st2 / 5) * S + cb + st2 % 5];
+                const double v = area * c[ntl][h2];
+                *dst = first ? v : *dst + v;
+              }
+            }
         }
       }
-      if (rowok) {
-        const int rb = ts[ia] * 5, cb = ts[ja] * 5;
-#pragma unroll
-        for (int ntl = 0; ntl < WNT; ++ntl)
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int st2 = ntl * 8 + (lane & 3) * 2 + h2;
-            if (st2 < 25) atomicAdd(&A[(rb + st2 / 5) * S + cb + st2 % 5], area * c[ntl][h2]);
-          }
-      }
+      __syncthreads();
     }
     __syncthreads();
     double amax = 0.0, dmax = 0.0;
