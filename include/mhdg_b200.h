@@ -300,6 +300,22 @@ int mhdg_math_eval(int fn, int64_t n, const double* x, double* y, void* stream);
 int64_t mhdg_pair_sides(int64_t n_sides, int key_width, const int64_t* keys, int64_t* partner);
 double mhdg_match_points(int64_t n_faces, int nt, int dim, const double* pts_nb,
                          const double* pts_own, int64_t* match);
+/* mhdg_side_keys: canonical quantised side keys (wrap on periodic max
+ * planes, round(x / quantum), rows sorted) of n_sides sides (d x d vertex
+ * coordinates each) -> keys (n_sides, d * d); mhdg_face_shift_perm: periodic
+ * shift and owner -> neighbour vertex permutation of paired faces (va, vb:
+ * (nf, d, d) vertices), returns the largest matched distance or -1 (both:
+ * reference mesh.py:226-299, host-only). */
+/* mhdg_match_faces: mhdg_match_points with the neighbour points built from
+ * the macro maps (origin + J fun[nfl] - shift; fun: (d+1, nt, d) face-unique
+ * reference nodes, ne / nfl: neighbour macro and local face per face). */
+double mhdg_match_faces(int64_t nf, int nt, int d, const double* fun, const int64_t* ne,
+                        const int64_t* nfl, const double* origins, const double* jac,
+                        const double* shift, const double* po, int64_t* match);
+void mhdg_side_keys(int64_t n_sides, int d, const double* sv, const double* box_hi,
+                    const double* extent, const int* periodic, double quantum, int64_t* keys);
+double mhdg_face_shift_perm(int64_t nf, int d, const double* va, const double* vb,
+                            const double* extent, double* shift, int64_t* perm);
 const char* mhdg_version(void);
 
 #ifdef __cplusplus

@@ -124,6 +124,10 @@ _SIGS = {
     "mhdg_math_eval": (C.c_int, [C.c_int, C.c_int64, dptr, dptr, C.c_void_p]),
     "mhdg_pair_sides": (C.c_int64, [C.c_int64, C.c_int, dptr, dptr]),
     "mhdg_match_points": (C.c_double, [C.c_int64, C.c_int, C.c_int, dptr, dptr, dptr]),
+    "mhdg_match_faces": (C.c_double, [C.c_int64, C.c_int, C.c_int, dptr, dptr, dptr, dptr, dptr, dptr,
+                                      dptr, dptr]),
+    "mhdg_side_keys": (None, [C.c_int64, C.c_int, dptr, dptr, dptr, dptr, C.c_double, dptr]),
+    "mhdg_face_shift_perm": (C.c_double, [C.c_int64, C.c_int, dptr, dptr, dptr, dptr, dptr]),
     "mhdg_version": (C.c_char_p, []),
 }
 

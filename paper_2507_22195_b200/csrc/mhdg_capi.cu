@@ -102,6 +102,22 @@ extern "C" double mhdg_match_points(int64_t n_faces, int nt, int dim, const doub
   return mhdg_host::match_points(n_faces, nt, dim, pts_nb, pts_own, match);
 }
 
+extern "C" double mhdg_match_faces(int64_t nf, int nt, int d, const double* fun, const int64_t* ne,
+                                   const int64_t* nfl, const double* origins, const double* jac,
+                                   const double* shift, const double* po, int64_t* match) {
+  return mhdg_host::match_faces(nf, nt, d, fun, ne, nfl, origins, jac, shift, po, match);
+}
+
+extern "C" void mhdg_side_keys(int64_t n_sides, int d, const double* sv, const double* box_hi,
+                               const double* extent, const int* periodic, double quantum, int64_t* keys) {
+  mhdg_host::side_keys(n_sides, d, sv, box_hi, extent, periodic, quantum, keys);
+}
+
+extern "C" double mhdg_face_shift_perm(int64_t nf, int d, const double* va, const double* vb,
+                                       const double* extent, double* shift, int64_t* perm) {
+  return mhdg_host::face_shift_perm(nf, d, va, vb, extent, shift, perm);
+}
+
 extern "C" const char* mhdg_version(void) { return "mhdg_b200 0.2 (sm_100a, fp64, m=1 P=1..4; m=2 P=1..3, m=3 P=1)"; }
 
 extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {

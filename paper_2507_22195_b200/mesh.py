@@ -239,6 +239,17 @@ def skeleton_arrays(mesh):
     E = mesh.n_macros
     fids = np.array([[k for k in range(d + 1) if k != f] for f in range(d + 1)])
     sv = mesh.macro_vertices[:, fids, :].reshape(E * (d + 1), d, d)
+    lib = _host_lib()
+    if lib is not None:   # native keys (csrc/mhdg_host_mesh.cuh), same integers
+        svc = np.ascontiguousarray(sv)
+        kk = np.empty((len(svc), d, d), dtype=np.int64)
+        hi = np.ascontiguousarray(mesh.box[:, 1], dtype=np.float64)
+        ext = np.ascontiguousarray(extent, dtype=np.float64)
+        per = np.ascontiguousarray([1 if x else 0 for x in mesh.periodic], dtype=np.int32)
+        lib.mhdg_side_keys(len(svc), d, svc.ctypes.data_as(_c_void_p), hi.ctypes.data_as(_c_void_p),
+                           ext.ctypes.data_as(_c_void_p), per.ctypes.data_as(_c_void_p), quantum,
+                           kk.ctypes.data_as(_c_void_p))
+        return _pair_and_shift(mesh, sv, kk, extent, quantum, lib)
     wrapped = sv.copy()
     for a in range(d):
         if mesh.periodic[a]:
@@ -261,8 +272,13 @@ def skeleton_arrays(mesh):
                 decided |= gt | lt
             kk[swap, j - 1], kk[swap, j] = cur[swap], prev[swap]
             j -= 1
+    return _pair_and_shift(mesh, sv, kk, extent, quantum, lib)
+
+
+def _pair_and_shift(mesh, sv, kk, extent, quantum, lib):
+    """Pair sides with equal canonical keys; shift and vertex permutation."""
+    d = mesh.dim
     flat = np.ascontiguousarray(kk.reshape(len(kk), d * d))
-    lib = _host_lib()
     if lib is not None:
         # native pairing (csrc/mhdg_host_mesh.cuh): sort by key, pair equal
         # neighbours; faces in increasing owner-side order as below
@@ -299,7 +315,22 @@ def skeleton_arrays(mesh):
     F = len(first)
     shift = np.zeros((F, d))
     perm = np.full((F, d), -1, dtype=np.int64)
-    if has_nb.any():
+    if has_nb.any() and lib is not None:   # native shift / permutation, same floats
+        va = np.ascontiguousarray(sv[first[has_nb]])
+        vb = np.ascontiguousarray(sv[second[has_nb]])
+        sh = np.empty((len(va), d))
+        pm = np.empty((len(va), d), dtype=np.int64)
+        ext = np.ascontiguousarray(extent, dtype=np.float64)
+        worst = lib.mhdg_face_shift_perm(len(va), d, va.ctypes.data_as(_c_void_p),
+                                         vb.ctypes.data_as(_c_void_p), ext.ctypes.data_as(_c_void_p),
+                                         sh.ctypes.data_as(_c_void_p), pm.ctypes.data_as(_c_void_p))
+        if worst < 0:
+            raise TopologyError("degenerate vertex matching")
+        if worst > quantum:
+            raise TopologyError("face vertices do not match after shift")
+        shift[has_nb] = sh
+        perm[has_nb] = pm
+    elif has_nb.any():
         va = sv[first[has_nb]]
         vb = sv[second[has_nb]]
         delta = vb.mean(axis=1) - va.mean(axis=1)

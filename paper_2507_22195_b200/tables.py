@@ -206,6 +206,22 @@ class HDGTables:
         from .mesh import _host_lib
 
         lib = _host_lib()
+        if lib is not None and len(nbf):   # native: points built and matched per face
+            ne, nf = skel.neighbor[nbf], skel.neighbor_face[nbf]
+            match = np.empty((len(nbf), nt), dtype=np.int64)
+            c = np.ascontiguousarray
+            fun_c, ne_c, nf_c = c(fun, dtype=np.float64), c(ne, dtype=np.int64), c(nf, dtype=np.int64)
+            org, jac = c(mesh.macro_origins, dtype=np.float64), c(mesh.macro_jacobians, dtype=np.float64)
+            shf, owp = c(skel.shift[nbf], dtype=np.float64), c(own_pts[nbf])
+            worst = lib.mhdg_match_faces(len(nbf), nt, d, *(a.ctypes.data_as(_c_void_p) for a in
+                                                            (fun_c, ne_c, nf_c, org, jac, shf, owp,
+                                                             match)))
+            if worst < 0 or worst > tol:
+                raise InvalidConfig("trace nodes of a skeleton face do not match")
+            face_id[ne, nf] = nbf
+            side_of[ne, nf] = 1
+            trace_perm[ne, nf] = match
+            nbf = nbf[:0]
         chunk = max(1, 4_000_000 // max(1, nt * nt)) if lib is None else max(1, len(nbf))
         for c0 in range(0, len(nbf), chunk):
             fs = nbf[c0:c0 + chunk]
@@ -239,10 +255,8 @@ class HDGTables:
         self.boundary_side = boundary
         self.side_of = side_of
         st = self.st_face
-        self.trace_idx = np.take_along_axis(
-            trace_perm[:, st, :],
-            np.broadcast_to(self.st_face_scatter[None], (E,) + self.st_face_scatter.shape),
-            axis=2)                                         # (E, n_st, nfn)
+        # trace_idx[e, k, j] = trace_perm[e, st[k], st_face_scatter[k, j]]
+        self.trace_idx = trace_perm[:, st[:, None], self.st_face_scatter]   # (E, n_st, nfn)
         self.face_id_st = face_id[:, st]                    # (E, n_st)
         self.boundary_st = boundary[:, st]
         self.side_st = side_of[:, st]
