@@ -136,3 +136,35 @@ def test_cfg2_step_n8(cuda_ok):
     want = z["integrals"]
     assert np.all(np.abs(ints - want) <= 1e-12 * np.maximum(1.0, np.abs(want)))
     assert np.sign(ints[1, 0] - ints[0, 0]) == np.sign(want[1, 0] - want[0, 0])
+
+
+@pytest.mark.gpu
+def test_cfg2_hsweep_first_level(cuda_ok):
+    """Config-2 h-refinement study, first level (reference driver.py:570-606
+    semantics): n = 8, k = 3, ES, 10 steps of dt = 0.1 to t = 0.1 t_c; the
+    L2 error of rho against the exact translated vortex (assembly.py:674-684)
+    and the state match the reference; Newton counts identical."""
+    import math
+
+    from paper_2507_22195_b200 import Discretization, DissipationSpec, GasModel
+    from paper_2507_22195_b200.cases import IsentropicVortex
+    from paper_2507_22195_b200.mesh import build_box_macro_mesh
+    from paper_2507_22195_b200.time_march import DIRKIntegrator
+
+    z = load_golden("cfg2_hsweep_n8")
+    gas = GasModel(1.4)
+    vx = IsentropicVortex(dim=3, mach=1 / math.sqrt(1.4), strength=5.0, v_inf=1.0,
+                          center=(5.0, 5.0), gas=gas)
+    disc = Discretization(build_box_macro_mesh(np.array([[0.0, 10.0]] * 3), 8, 1), p=3,
+                          gas=gas, formulation="entropy", flux=DissipationSpec("es"),
+                          device="cuda:0")
+    f0 = disc.project(vx.initial)
+    t_eval = float(z["t_eval"])
+    assert abs(disc.l2_error(f0, vx.initial) - float(z["l2_initial"])) <= 1e-12 * float(z["l2_initial"])
+    integ = DIRKIntegrator(disc)
+    f1, t = integ.run(f0, t_final=t_eval, dt=float(z["dt"]))
+    newton = np.array([[r["step"], r["stage"], r["newton_iters"]] for r in integ.records])
+    assert np.array_equal(newton, z["newton"][:, :3])
+    assert rel(f1.w, z["w1"]) <= 1e-10 and rel(f1.trace, z["trace1"]) <= 1e-10
+    err = disc.l2_error(f1, lambda x: vx.state(x, t_eval), component=0)
+    assert abs(err - float(z["l2"])) <= 1e-9 * float(z["l2"])
