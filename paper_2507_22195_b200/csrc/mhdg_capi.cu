@@ -589,7 +589,7 @@ extern "C" int mhdg_residual(mhdg_ctx* c, const double* w, const double* trace, 
 // batched in-place inverse (row-major in, column-major out): lookahead
 // Gauss-Jordan, 8 warps for the condensed blocks S (N >= 64), 4 otherwise
 #ifndef MHDG_GJ_NPW
-#define MHDG_GJ_NPW 4        // panel warps for the condensed blocks S (N >= 64)
+#define MHDG_GJ_NPW 2        // panel warps for the condensed blocks S (N >= 64): warps 0 and 4
 #endif
 #ifndef MHDG_GJ_NPW_SMALL
 #define MHDG_GJ_NPW_SMALL 1  // panel warps for the face blocks (N < 64)
@@ -1491,9 +1491,9 @@ extern "C" double mhdg_dmma_probe(int device, void* stream) {
 // experiment builds: residual phase clocks, DFMA dependent-chain latency
 extern "C" void mhdg_debug_res_clk(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, g_res_clk, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_res_clk, sizeof(unsigned long long) * 32);
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     cudaMemcpyToSymbol(g_res_clk, z, sizeof(z));
   }
 }
@@ -1531,7 +1531,148 @@ __global__ void k_dmma_lat(int n, double* out, long long* cyc, int indep) {
   out[1] = c[0][0] + c[1][1] + c[2][0] + c[3][1];
   cyc[0] = t1 - t0;
 }
+__global__ void k_misc_lat(int n, double* out, long long* cyc, int which) {
+  double a = out[0] + 1.5;
+  const int lane = threadIdx.x & 31;
+  const long long t0 = clock64();
+  if (which == 10) {
+    for (int i = 0; i < n; ++i) a = __shfl_sync(0xffffffffu, a, (lane + 5) & 31) + 1.0;
+  } else if (which == 11) {
+    for (int i = 0; i < n; ++i) a = drcp(a) + 1.5;
+  } else if (which == 12) {
+    for (int i = 0; i < n; ++i) {
+      const unsigned hi = (unsigned)((unsigned long long)__double_as_longlong(a) >> 32);
+      a += (double)(__reduce_max_sync(0xffffffffu, hi) & 1u);
+    }
+  } else {
+    for (int i = 0; i < n; ++i) { asm volatile("bar.sync 1, 128;" ::: "memory"); a += 1.0; }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) { out[1] = a; cyc[0] = t1 - t0; }
+}
+// warp 0: a dependent chain (mode 0: DFMA, 1: SHFL + DADD, 2: FSEL-like
+// integer chain); warp `other`: an endless stream of independent DMMAs (or
+// DFMAs when dm = 0) until warp 0 is done.  other = 4 shares warp 0's
+// scheduler (warp id % 4), other = 1 does not.
+__global__ void k_contend(int n, double* out, long long* cyc, int mode, int other, int dm) {
+  __shared__ volatile int done;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
+  if (warp == 0) {
+    double a = out[0] + 1.5;
+    int ia = lane;
+    const long long t0 = clock64();
+    if (mode == 0) for (int i = 0; i < n; ++i) a = fma(a, 1.0000001, 1e-9);
+    else if (mode == 1) for (int i = 0; i < n; ++i) a = __shfl_sync(0xffffffffu, a, (lane + 5) & 31) + 1.0;
+    else for (int i = 0; i < n; ++i) ia = (ia * 3 + 1) ^ (ia >> 3);
+    const long long t1 = clock64();
+    if (lane == 0) { out[1] = a + ia; cyc[0] = t1 - t0; }
+    __syncwarp();
+    done = 1;
+  } else if (warp == other) {
+    double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    const double a = out[0] + 1.0, b = 0.5;
+    long long cnt = 0;
+    while (!done) {
+      if (dm) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          dmma_8x8x4(c[0], a, b); dmma_8x8x4(c[1], a, b); dmma_8x8x4(c[2], a, b); dmma_8x8x4(c[3], a, b);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          c[0][0] = fma(c[0][0], a, b); c[1][0] = fma(c[1][0], a, b); c[2][0] = fma(c[2][0], a, b); c[3][0] = fma(c[3][0], a, b);
+          c[0][1] = fma(c[0][1], a, b); c[1][1] = fma(c[1][1], a, b); c[2][1] = fma(c[2][1], a, b); c[3][1] = fma(c[3][1], a, b);
+        }
+      }
+      cnt += 32;
+    }
+    if (lane == 0) { out[2] = c[0][0] + c[1][1] + c[2][0] + c[3][1]; cyc[1] = cnt; }
+  }
+}
+__global__ void __launch_bounds__(256, 2) k_warpid(int* out) {
+  extern __shared__ double sm_[];
+  unsigned smid, wid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+  if ((threadIdx.x & 31) == 0) {
+    int* o = out + (blockIdx.x * 8 + (threadIdx.x >> 5)) * 2;
+    o[0] = (int)smid;
+    o[1] = (int)wid;
+  }
+  sm_[threadIdx.x] = 1.0;
+  // keep the CTA resident long enough for the whole grid to be placed
+  const long long t0 = clock64();
+  while (clock64() - t0 < 2000000) { }
+}
+extern "C" void mhdg_debug_warpid(int* host_out, int nblocks) {
+  int* d;
+  cudaMalloc(&d, sizeof(int) * nblocks * 16);
+  cudaFuncSetAttribute(k_warpid, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  k_warpid<<<nblocks, 256, 100 * 1024>>>(d);
+  cudaMemcpy(host_out, d, sizeof(int) * nblocks * 16, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+}
+// the 8 x 8 cooperative Gauss-Jordan of block_panel, alone on an SM
+__global__ void k_gj8_lat(int n, double* out, long long* cyc, int variant) {
+  const int lane = threadIdx.x & 31, kq = lane & 3, nr = lane >> 2;
+  double d0 = (nr == 2 * kq ? 4.0 : 0.1 * (lane + 1)) + out[0], d1 = (nr == 2 * kq + 1 ? 4.0 : 0.01 * (lane + 3));
+  int nbad = 0;
+  const long long t0 = clock64();
+  for (int it = 0; it < n; ++it) {
+#pragma unroll 1
+    for (int t = 0; t < 8; ++t) {
+      const double dsel = (t & 1) ? d1 : d0;
+      const double p0 = __shfl_sync(0xffffffffu, d0, t * 4 + kq);
+      const double p1 = __shfl_sync(0xffffffffu, d1, t * 4 + kq);
+      const double cr = __shfl_sync(0xffffffffu, dsel, (lane & ~3) | (t >> 1));
+      const double piv = __shfl_sync(0xffffffffu, dsel, t * 4 + (t >> 1));
+      const double apiv = fabs(piv);
+      if (variant == 0)
+        nbad |= (int)!(apiv > 0.0) | (int)!(apiv < 1.7976931348623157e308) |
+                ((int)(nr > t) & (int)(apiv < 0.05 * fabs(cr)));
+      const double pinv = variant == 2 ? 1.0 / piv : drcp(piv);
+      const bool c0t = 2 * kq == t, c1t = 2 * kq + 1 == t;
+      const double s0 = (c0t ? 1.0 : p0) * pinv, s1 = (c1t ? 1.0 : p1) * pinv;
+      const double v0 = (c0t ? 0.0 : d0) - cr * s0, v1 = (c1t ? 0.0 : d1) - cr * s1;
+      d0 = nr == t ? s0 : v0;
+      d1 = nr == t ? s1 : v1;
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) { out[1] = d0 + d1 + nbad; cyc[0] = t1 - t0; }
+}
+extern "C" double mhdg_debug_gj8(int variant) {
+  double* d; long long* cy; long long h = 0;
+  cudaMalloc(&d, 16); cudaMalloc(&cy, 8); cudaMemset(d, 0, 16);
+  const int n = 512;
+  k_gj8_lat<<<1, 32>>>(n, d, cy, variant);
+  cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost);
+  cudaFree(d); cudaFree(cy);
+  return (double)h / (n * 8);
+}
+extern "C" double mhdg_debug_contend(int mode, int other, int dm, double* other_ops) {
+  double* d; long long* cy; long long h[2] = {0, 0};
+  cudaMalloc(&d, 32); cudaMalloc(&cy, 16); cudaMemset(d, 0, 32); cudaMemset(cy, 0, 16);
+  const int n = 4096;
+  k_contend<<<1, 256>>>(n, d, cy, mode, other, dm);
+  cudaMemcpy(h, cy, 16, cudaMemcpyDeviceToHost);
+  cudaFree(d); cudaFree(cy);
+  if (other_ops) *other_ops = h[0] > 0 ? (double)h[1] / (double)h[0] : 0.0;   // other warp's ops per clock
+  return (double)h[0] / n;
+}
 extern "C" double mhdg_debug_latency(int which) {
+  if (which >= 10) {
+    double* d; long long* cy; long long h = 0;
+    cudaMalloc(&d, 16); cudaMalloc(&cy, 8); cudaMemset(d, 0, 16);
+    const int n = 4096;
+    k_misc_lat<<<1, which == 13 ? 128 : 32>>>(n, d, cy, which);
+    cudaMemcpy(&h, cy, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d); cudaFree(cy);
+    return (double)h / n;
+  }
   if (which >= 3) {
     double* d; long long* cy; long long h = 0;
     cudaMalloc(&d, 16); cudaMalloc(&cy, 8); cudaMemset(d, 0, 16);

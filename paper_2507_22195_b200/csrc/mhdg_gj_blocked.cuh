@@ -226,8 +226,9 @@ struct GJLA2 {
   static constexpr int RPL = (NP + 32 * NPW - 1) / (32 * NPW);
   static constexpr int NT = 32 * NWT;
   static constexpr int UF = T * 2 * 32;
-  static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + 16 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
-  static constexpr size_t bytes_ga = (size_t)(2 * UF + 16 + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
+  static constexpr int XD = NPW > 1 ? 64 : 16;   // pivot-row / diagonal-block exchange (doubles)
+  static constexpr size_t bytes = (size_t)(NP * S + 2 * UF + XD + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
+  static constexpr size_t bytes_ga = (size_t)(2 * UF + XD + 2 * NPW) * 8 + (size_t)(2 * NP + 4 + 2 * NPW) * 4;
   static constexpr size_t slab = (size_t)NP * S;   // doubles per CTA (GA)
 };
 
@@ -274,6 +275,12 @@ struct GjGlobalSrc {   // the matrix is read from mats[m] and overwritten
 #ifndef MHDG_GJ_TAU
 #define MHDG_GJ_TAU 0.05
 #endif
+#ifndef MHDG_GJ_SCHED_ROLES
+#define MHDG_GJ_SCHED_ROLES 0   // panel warps = the warps on hardware scheduler 0
+#endif
+#ifndef MHDG_GJ_BLOCKPANEL
+#define MHDG_GJ_BLOCKPANEL 1   // diagonal-pivot pass: panels through the 8 x 8 block inverse
+#endif
 struct GjPass {
   const int* list;       // matrices to process (nullptr: 0 .. nmat-1)
   const int* count_dev;  // length of list (device), when list != nullptr
@@ -295,15 +302,46 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
   extern __shared__ __align__(16) double smem[];
   double* A = GA ? pass.slab + (size_t)blockIdx.x * NP * S : smem;   // NP x S
   double* Ub = GA ? smem : A + NP * S;     // 2 x UF
-  double* sProw = Ub + 2 * L::UF;          // 2 x 8: pivot row of the current step
-  unsigned* sCand = reinterpret_cast<unsigned*>(sProw + 16);  // [NPW][3]: hi, lo, row
+  double* sProw = Ub + 2 * L::UF;          // 2 x 8: pivot row of the current step (block panels: 8 x 8 diagonal block)
+  unsigned* sCand = reinterpret_cast<unsigned*>(sProw + L::XD);  // [NPW][3]: hi, lo, row
   int* q = (int*)(sCand + 4 * NPW);        // NP: pivot row of step k
   int* qi = q + NP;
   int* flag = qi + NP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kq = lane & 3, nr = lane >> 2;
-  const bool panel = warp < NPW;
-  const int pw = warp;
+  // Warp roles by hardware scheduler.  A warp issues on scheduler
+  // %warpid % 4 (measured: a dependent DFMA chain sharing a scheduler with
+  // a DMMA stream slows from 8.8 to 47.5 cycles per operation, a chain on
+  // another scheduler is unaffected; the second co-resident CTA's warps sit
+  // one scheduler further, so the warp index alone does not tell).  When
+  // the CTA has NPW warps on hardware scheduler 0 they become the panel
+  // warps, so the serial panel chains of all co-resident CTAs share one
+  // scheduler and the update warps' DMMA streams run on the other three;
+  // otherwise the first NPW warps are the panel warps.
+  bool panel = warp < NPW;
+  int pw = warp, n_panel_below = min(NPW, warp);
+  if constexpr (4 * NPW <= NWT && MHDG_GJ_SCHED_ROLES) {
+    unsigned hw;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(hw));
+    if (lane == 0) q[warp] = (int)(hw & 3u);
+    __syncthreads();
+    int cnt0 = 0, mine = 0, below = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NWT; ++w2) {
+      const bool p2 = q[w2] == 0 && cnt0 < NPW;
+      if (w2 == warp) { mine = p2 ? cnt0 : -1; }
+      if (p2) {
+        ++cnt0;
+        if (w2 < warp) ++below;
+      }
+    }
+    if (cnt0 == NPW) {
+      panel = mine >= 0;
+      pw = mine >= 0 ? mine : 0;
+      n_panel_below = below;
+    }
+    __syncthreads();
+  }
   auto psync = [&]() {
     if (NPW > 1) asm volatile("bar.sync 1, %0;" ::"r"(32 * NPW) : "memory");
     else __syncwarp();
@@ -482,6 +520,120 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
       for (int t = nbp; t < 8; ++t) q[k0 + t] = -1;
   };
 
+  // Diagonal-pivot pass, block form (MHDG_GJ_BLOCKPANEL).  The eight Gauss-
+  // Jordan steps of panel p with pivots on its own diagonal block D_p compose
+  // to  panel <- [ G_p = D_p^-1 on the block rows ; -P G_p elsewhere ],  and
+  // D_{p+1} needs, of panel p's whole update, one tile:
+  //   D_{p+1} = A[p+1][p+1] + U_p[p+1] R_p[p+1],  U_p = panel_p - E.
+  // So the serial chain is  one tile update -> 8 x 8 inverse  per panel, on
+  // ONE warp (the chain warp), and everything else is throughput work:
+  //   phase 1 (all warps)   : panel p's columns <- -P G_p, U_p fragments;
+  //                           the R tile the chain needs next is copied aside
+  //   phase 2 (chain warp)  : D_{p+1}, G_{p+1} = D_{p+1}^-1 (cooperative in
+  //                           the C-fragment layout: row lane / 4, columns
+  //                           2 (lane % 4), +1; shuffles only, and the next
+  //                           pivot's reciprocal is started one step ahead)
+  //           (update warps): A[:, c] += U_p R_p[c] for every column tile
+  //                           c != p (tile (p+1, p+1) excepted: the chain's)
+  // Checks, lane-local and branch-free: every in-block pivot is at least
+  // GJ_TAU times the entries below it in D, and no composite multiplier
+  // (-P G below the block) exceeds 1 / GJ_TAU; a matrix failing either goes
+  // to the partial-pivoting pass.
+  double* sG = Ub + L::UF;   // G row-major 8 x 8 (the second U buffer is free in this pass)
+  double* sR = sG + 64;      // R_p on panel p+1's columns, row-major 8 x 8
+  static_assert(!(NOPIV && MHDG_GJ_BLOCKPANEL) || L::UF >= 128, "block-panel scratch");
+#ifdef MHDG_RES_TIMING
+  long long tp = 0;
+#define BP_T0() tp = clock64()
+#define BP_T(k, cond) do { const long long t_ = clock64(); if (cond) atomicAdd(&g_res_clk[(N == 100 ? 16 : 21) + (k)], (unsigned long long)(t_ - tp)); tp = t_; } while (0)
+#else
+#define BP_T0() do { } while (0)
+#define BP_T(k, cond) do { } while (0)
+#endif
+  // phase 1: the panel transform of panel pn, all warps
+  auto panel_transform = [&](int pn, bool& ok) {
+    const int k0n = pn * 8, nbp = min(8, N - k0n);
+    const double b0 = sG[kq * 8 + nr], b1 = sG[(kq + 4) * 8 + nr];
+    const double2 gd = *reinterpret_cast<const double2*>(sG + nr * 8 + 2 * kq);
+    int nbad = 0;
+#pragma unroll 2
+    for (int rt = warp; rt < T; rt += NWT) {
+      const double* ap = A + (rt * 8 + nr) * S + k0n + kq;
+      double c[2] = {0.0, 0.0};
+      dmma_8x8x4(c, ap[0], b0);
+      dmma_8x8x4(c, ap[4], b1);
+      __syncwarp();   // the tile's A fragments are read before its columns are rewritten
+      double n0 = -c[0], n1 = -c[1];
+      nbad |= (int)(rt > pn) & ((int)!(fabs(n0) <= 1.0 / MHDG_GJ_TAU) | (int)!(fabs(n1) <= 1.0 / MHDG_GJ_TAU));
+      double u0 = n0, u1 = n1;
+      if (rt == pn) {
+        n0 = gd.x;
+        n1 = gd.y;
+        u0 = gd.x - ((nr == 2 * kq && nr < nbp) ? 1.0 : 0.0);
+        u1 = gd.y - ((nr == 2 * kq + 1 && nr < nbp) ? 1.0 : 0.0);
+      }
+      *reinterpret_cast<double2*>(A + (rt * 8 + nr) * S + k0n + kq * 2) = make_double2(n0, n1);
+      *reinterpret_cast<double2*>(Ub + (rt * 2 + (kq >> 1)) * 32 + nr * 4 + 2 * (kq & 1)) = make_double2(u0, u1);
+    }
+    // the R tile of the next panel's columns, for the chain warp (the owner
+    // of that column tile rewrites it during phase 2)
+    if (warp == NWT - 1 && pn + 1 < T)
+      *reinterpret_cast<double2*>(sR + nr * 8 + 2 * kq) =
+          *reinterpret_cast<const double2*>(A + (k0n + nr) * S + k0n + 8 + 2 * kq);
+    if (__any_sync(0xffffffffu, nbad) && lane == 0) *flag = 1;
+  };
+  // phase 2, chain warp: D_pn (with panel pn-1's update when Up) and G_pn
+  auto chain_block = [&](int pn, bool with_update, bool& ok) {
+    const int k0n = pn * 8, nbp = min(8, N - k0n);
+    BP_T0();
+    double d0, d1;
+    {
+      const double2 dd = *reinterpret_cast<const double2*>(A + (k0n + nr) * S + k0n + kq * 2);
+      double c[2] = {dd.x, dd.y};
+      if (with_update) {
+        dmma_8x8x4(c, Ub[(pn * 2 + 0) * 32 + lane], sR[kq * 8 + nr]);
+        dmma_8x8x4(c, Ub[(pn * 2 + 1) * 32 + lane], sR[(kq + 4) * 8 + nr]);
+      }
+      d0 = c[0];
+      d1 = c[1];
+    }
+    BP_T(0, lane == 0);
+    int nbad = 0;
+    double piv = __shfl_sync(0xffffffffu, d0, 0);
+    double pinv = drcp(piv);
+#pragma unroll 1
+    for (int t = 0; t < nbp; ++t) {
+      const double dt = (t & 1) ? d1 : d0, dn = (t & 1) ? d0 : d1;   // column t / t + 1 slots
+      const double p0 = __shfl_sync(0xffffffffu, d0, t * 4 + kq);
+      const double p1 = __shfl_sync(0xffffffffu, d1, t * 4 + kq);
+      const double cr = __shfl_sync(0xffffffffu, dt, (lane & ~3) | (t >> 1));
+      // next pivot one step ahead: D[t+1][t+1] - D[t+1][t] (D[t][t+1] pinv),
+      // the same operations its owner lane performs below
+      const int t1 = (t + 1) & 7;
+      const double la = __shfl_sync(0xffffffffu, dn, t1 * 4 + (t1 >> 1));
+      const double lb = __shfl_sync(0xffffffffu, dt, t1 * 4 + (t >> 1));
+      const double lc = __shfl_sync(0xffffffffu, dn, t * 4 + (t1 >> 1));
+      const double apiv = fabs(piv);
+      nbad |= (int)!(apiv > 0.0) | (int)!(apiv < 1.7976931348623157e308) |
+              ((int)(nr > t) & (int)(apiv < MHDG_GJ_TAU * fabs(cr)));
+      const double pnext = la - lb * (lc * pinv);
+      const double pinv_next = drcp(pnext);
+      const bool c0t = 2 * kq == t, c1t = 2 * kq + 1 == t;
+      const double s0 = (c0t ? 1.0 : p0) * pinv, s1 = (c1t ? 1.0 : p1) * pinv;
+      const double v0 = (c0t ? 0.0 : d0) - cr * s0, v1 = (c1t ? 0.0 : d1) - cr * s1;
+      d0 = nr == t ? s0 : v0;
+      d1 = nr == t ? s1 : v1;
+      piv = pnext;
+      pinv = pinv_next;
+    }
+    BP_T(1, lane == 0);
+    if (lane < 8) q[k0n + lane] = lane < nbp ? k0n + lane : -1;
+    *reinterpret_cast<double2*>(sG + nr * 8 + 2 * kq) = make_double2(d0, d1);
+    if (__any_sync(0xffffffffu, nbad) && lane == 0) *flag = 1;
+    (void)ok;
+    BP_T(2, lane == 0);
+  };
+
   auto update_tile = [&](const double* U, int ct, double r0, double r1, int rt0, int rt1, int rts) {
     for (int rt = rt0; rt < rt1; rt += rts) {
       double* cp = A + (rt * 8 + nr) * S + ct * 8 + kq * 2;
@@ -500,18 +652,45 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
     const int m = pass.list ? pass.list[mi] : mi;
     double* M = mats + (size_t)m * N * N;
     __syncthreads();
+#ifdef MHDG_RES_TIMING
+    // experiment builds: [b] load, [b+1] panel-warp busy, [b+2] update-warp
+    // busy, [b+3] interval total, [b+4] store (b = 5: order 100, 10: others)
+    constexpr int TB = (N == 100) ? 5 : 10;
+    long long tg = clock64();
+#define GJ_T(k, cond) do { const long long t_ = clock64(); if (cond) atomicAdd(&g_res_clk[TB + (k)], (unsigned long long)(t_ - tg)); } while (0)
+#define GJ_T0() tg = clock64()
+#else
+#define GJ_T(k, cond) do { } while (0)
+#define GJ_T0() do { } while (0)
+#endif
     src.load(m, A, S, ex, Ub, tid, NT);   // Ub is free until the first panel
     if (tid == 0) *flag = 0;
     __syncthreads();
+    GJ_T(0, tid == 0);
     unsigned used = 0u;
     bool ok = true;
     for (int pan = -1; pan < NPAN; ++pan) {
+      GJ_T0();
       const double* U = Ub + (pan & 1) * L::UF;
       const int k0 = pan * 8, nxt = pan + 1;
-      if (pan < 0) {
-        if (panel) factor_panel(0, used, ok);
+      constexpr bool BP = NOPIV && MHDG_GJ_BLOCKPANEL;
+      if constexpr (BP) {
+        U = Ub;
+        if (pan >= 0) {
+          panel_transform(pan, ok);
+          __syncthreads();
+          GJ_T(1, tid == 0);   // timing builds: phase 1 in the "panel busy" slot
+          GJ_T0();
+        }
+      }
+      if (BP && panel) {
+        if constexpr (BP)
+          if (pw == 0 && nxt < NPAN) chain_block(nxt, pan >= 0, ok);
+      } else if (pan < 0) {
+        if constexpr (!BP)
+          if (panel) factor_panel(0, used, ok);
       } else if (panel) {
-        if (nxt < NPAN) {
+        if (!BP && nxt < NPAN) {
           // R_p on panel p+1's columns (read by all panel warps before any
           // of them updates those columns), update them, factor panel p+1
           const int c = nxt * 8 + nr;
@@ -523,7 +702,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
           factor_panel(nxt, used, ok);
         }
       } else {
-        const int uw = warp - NPW, nuw = NWT - NPW;
+        const int uw = warp - n_panel_below, nuw = NWT - NPW;
         const int pr0 = q[k0 + kq], pr1 = q[k0 + kq + 4];
 #ifndef MHDG_GJ_UREG
 #define MHDG_GJ_UREG 1
@@ -541,7 +720,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
 #endif
         int slot = 0;
         for (int ct = 0; ct < T; ++ct) {
-          if (ct == pan || ct == nxt) continue;
+          if (ct == pan || (!BP && ct == nxt)) continue;
           if ((slot++ % nuw) != uw) continue;
           const int c = ct * 8 + nr;
           const double r0 = pr0 >= 0 ? A[pr0 * S + c] : 0.0;
@@ -550,6 +729,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
 #if MHDG_GJ_UREG
 #pragma unroll
           for (int rt = 0; rt < T; ++rt) {
+            if (BP && ct == nxt && rt == nxt) continue;   // the chain warp's tile
             double* cp = A + (rt * 8 + nr) * S + ct * 8 + kq * 2;
             const double2 cv = *reinterpret_cast<const double2*>(cp);
             double cc[2] = {cv.x, cv.y};
@@ -562,9 +742,13 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
 #endif
         }
       }
+      if (!BP) GJ_T(1, panel && pw == 0 && lane == 0);
+      GJ_T(2, !panel && warp - n_panel_below == 0 && lane == 0);
       __syncthreads();
+      GJ_T(3, tid == 0);
     }
-    if (panel && !ok && lane == 0) *flag = 1;
+    GJ_T0();
+    if (panel && __any_sync(0xffffffffu, !ok) && lane == 0) *flag = 1;
     for (int k = tid; k < N; k += NT) qi[q[k]] = k;
     __syncthreads();
     int bad = *flag;
@@ -608,6 +792,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
       }
     }
 #endif
+    GJ_T(4, tid == 0);
     if (__syncthreads_or(bad) && tid == 0) report(status, 0, 0, m);
   }
 }

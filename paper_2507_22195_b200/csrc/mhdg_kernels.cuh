@@ -154,7 +154,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 
 #ifdef MHDG_RES_TIMING
 // phase clocks of the residual (experiment builds only): per group leader
-__device__ unsigned long long g_res_clk[16];
+__device__ unsigned long long g_res_clk[32];
 #define RES_T(k)                                                   \
   do {                                                             \
     const long long t_ = clock64();                                \
