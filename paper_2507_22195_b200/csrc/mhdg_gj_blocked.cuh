@@ -249,6 +249,11 @@ struct GjGlobalSrc {   // the matrix is read from mats[m] and overwritten
   static constexpr size_t extra_bytes = 0;
   const double* mats;
   __device__ __forceinline__ void init(double*, int, int) const {}
+  // the next matrix towards L2 while this one is inverted
+  __device__ __forceinline__ void prefetch(int m, int tid, int NT) const {
+    const char* M = reinterpret_cast<const char*>(mats + (size_t)m * N * N);
+    for (int i = tid * 128; i < N * N * 8; i += NT * 128) prefetch_l2(M + i);
+  }
   __device__ __forceinline__ void load(int m, double* A, int S, double*, double*, int tid, int NT) const {
     const double* M = mats + (size_t)m * N * N;
     if constexpr (N % 2 == 0) {
@@ -274,6 +279,9 @@ struct GjGlobalSrc {   // the matrix is read from mats[m] and overwritten
 // pivoting elimination exactly as before.
 #ifndef MHDG_GJ_TAU
 #define MHDG_GJ_TAU 0.05
+#endif
+#ifndef MHDG_GJ_PREFETCH
+#define MHDG_GJ_PREFETCH 1   // L2 prefetch of the next matrix / face rows
 #endif
 #ifndef MHDG_GJ_SCHED_ROLES
 #define MHDG_GJ_SCHED_ROLES 0   // panel warps = the warps on hardware scheduler 0
@@ -664,6 +672,7 @@ __device__ __forceinline__ void gj_la2_body(int nmat, double* __restrict__ mats,
 #define GJ_T0() do { } while (0)
 #endif
     src.load(m, A, S, ex, Ub, tid, NT);   // Ub is free until the first panel
+    if (MHDG_GJ_PREFETCH && mi + (int)gridDim.x < nmat) src.prefetch(pass.list ? pass.list[mi + gridDim.x] : mi + (int)gridDim.x, tid, NT);
     if (tid == 0) *flag = 0;
     __syncthreads();
     GJ_T(0, tid == 0);
@@ -829,6 +838,14 @@ struct FaceBlockSrc {
     double* sFw = sFP + NQF * NFN;
     for (int i = tid; i < NQF * NFN; i += nt) sFP[i] = g.fphi[i];
     for (int i = tid; i < NQF; i += nt) sFw[i] = g.fw[i];
+  }
+  // the next face's hh rows (both sides) towards L2
+  __device__ __forceinline__ void prefetch(int f, int tid, int nt) const {
+    constexpr int LN = (NQF * 25 * 8 + 127) / 128;
+    for (int i = tid; i < 2 * LN; i += nt) {
+      const int st = g.fsides[f * 2 + i / LN];
+      if (st >= 0) prefetch_l2(reinterpret_cast<const char*>(hh + (size_t)st * NQF * 25) + (i % LN) * 128);
+    }
   }
   __device__ __forceinline__ void load(int f, double* A, int S, double* ex, double* tmp, int tid, int nt) const {
     const double* sFP = ex;

@@ -152,6 +152,8 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 #ifdef MHDG_RES_TIMING
 // phase clocks of the residual (experiment builds only): per group leader
 __device__ unsigned long long g_res_clk[32];
@@ -998,6 +1000,12 @@ __device__ bool gj_store_colmajor(const double* Y, const int* q, int* qinv, doub
 // C row kk rotated by 4 kk columns: a half-warp's stage-1 B-fragment loads
 // (four kk rows x four columns) then hit 16 distinct bank pairs
 #define LIN2_CI(kk, col) ((kk) * CS + (L::ROT ? (((col) + 4 * (kk)) & 31) : (col)))
+#ifndef MHDG_LIN2_PREFETCH
+#define MHDG_LIN2_PREFETCH 0   // L2 prefetch of the next macro's inputs (measured: 115.0 vs 114.3 ms, off)
+#endif
+#ifndef MHDG_LIN2_FB_PAIR
+#define MHDG_LIN2_FB_PAIR 1   // face-block units per warp pass (1 or 2: measured equal)
+#endif
 #ifndef MHDG_LIN2_NW
 #define MHDG_LIN2_NW 8   // 10 warps (whole dual passes) measured slower: 168-register cap spills
 #endif
@@ -1034,6 +1042,172 @@ struct Lin2 {
   static constexpr int ints = 4 * D::NFN + 4 + 4 * D::NFN + 4 + 2 * D::NM + 4;
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4 + 16 + D::NN * 15 * 8;
 };
+
+// One volume quadrature point and dual direction t (it = 5 q + t) of the
+// linearization: the C rows  -vol_w J^-1 dF/dw_t  (kk = 0..2) and
+// weight vol_w du/dw_t  (kk = 3) of point q, written into the macro's C block
+// (shared memory in the fused kernel, the macro's S^-1 storage in the split
+// pointwise kernel).  PADZ: also zero this item's share of the st >= 25
+// padding columns (the split kernel fills a fresh block).
+template <int P, bool VISC, bool PADZ>
+__device__ __forceinline__ void lin2_volume_item(const Geo& g, const ViscGeo& vg, int it, const double* __restrict__ sW,
+                                                 const double* __restrict__ sQn, const double* __restrict__ sQW,
+                                                 const double* __restrict__ sGeo, double weight, double* sC) {
+  using D = Dims<P>;
+  using L = Lin2<P>;
+  constexpr int NN = D::NN, CS = L::CS;
+  const double* __restrict__ Bt = g.B;
+  const double gam = g.gamma;
+  const int q = it / 5, t = it % 5;
+  const double* ph = Bt + ((size_t)q * 4 + 3) * NN;
+  double wq[5] = {0, 0, 0, 0, 0};
+  for (int i = 0; i < NN; ++i) {
+    const double a = __ldg(ph + i);
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) wq[s2] += a * sW[i * 5 + s2];
+  }
+  Dual wd[5], ud[5];
+#pragma unroll
+  for (int s2 = 0; s2 < 5; ++s2) wd[s2] = mk(wq[s2], s2 == t ? 1.0 : 0.0);
+  to_conservative(wd, g.form, gam, ud);
+  Dual F[5][3];
+  flux(ud, gam, F);
+  if (VISC) {
+    double qq[5][3];
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
+    for (int i = 0; i < NN; ++i) {
+      const double a = __ldg(ph + i);
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQn[i * 15 + s2 * 3 + b];
+    }
+    Dual Gv[5][3];
+    visc_G(vg, g.form, wd, ud, qq, gam, Gv);
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) F[s2][a] = F[s2][a] + Gv[s2][a];
+  }
+  const double vw = sQW[q] * sGeo[0];
+  double* C = sC + (size_t)q * 4 * CS;
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk) {
+    const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2)
+      C[LIN2_CI(kk, s2 * 5 + t)] = -(vw * ((j0 * F[s2][0].d + j1 * F[s2][1].d) + j2 * F[s2][2].d));
+  }
+#pragma unroll
+  for (int s2 = 0; s2 < 5; ++s2) C[LIN2_CI(3, s2 * 5 + t)] = weight * (vw * ud[s2].d);
+  if (PADZ && CS > 25) {
+    for (int col = 25 + t; col < CS; col += 5)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) C[LIN2_CI(kk, col)] = 0.0;
+  }
+}
+
+// One face quadrature point, dual direction t and side (it4 = ((k NQF + q) 2
+// + which) 5 + t): the hw / hhat / hh tensor entries of tile k at point q
+// (assembly.py:846-940); sHW (optional) stages the hw rows for the S face
+// blocks of the fused kernel.
+template <int P, bool VISC, int FK>
+__device__ __forceinline__ void lin2_face_item(const Geo& g, const ViscGeo& vg, int e, int it4,
+                                               const double* __restrict__ sW, const double* __restrict__ sTR,
+                                               const double* __restrict__ sQn, const double* __restrict__ sPF,
+                                               const double* __restrict__ sFP, const int* __restrict__ sRows,
+                                               const double* __restrict__ sGeo, const int* __restrict__ sBnd,
+                                               double ptc, double* __restrict__ hw_out,
+                                               double* __restrict__ hhat_out, double* __restrict__ hh_out,
+                                               double* sHW) {
+  using D = Dims<P>;
+  constexpr int NFN = D::NFN, NQF = D::NQF;
+  const double gam = g.gamma;
+  const int k = it4 / (NQF * 10), it = it4 % (NQF * 10);
+  const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
+  double* sHWk = sHW ? sHW + k * NQF * 25 : nullptr;
+  const int q = it / 10, t = (it % 10) % 5, which = (it % 10) / 5;
+  const double* pf = sPF + (k * NQF + q) * D::FS;
+  const double* fp = sFP + q * D::FS;
+  double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
+  for (int j = 0; j < NFN; ++j) {
+    const double a = pf[j], b = fp[j];
+    const int row = sRows[k * NFN + j];
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) {
+      wq[s2] += a * sW[row * 5 + s2];
+      whq[s2] += b * sTR[(k * NFN + j) * 5 + s2];
+    }
+  }
+  Dual wd[5], whd[5], ud[5], uhd[5], fd[5];
+#pragma unroll
+  for (int s2 = 0; s2 < 5; ++s2) {
+    wd[s2] = mk(wq[s2], (which == 0 && s2 == t) ? 1.0 : 0.0);
+    whd[s2] = mk(whq[s2], (which == 1 && s2 == t) ? 1.0 : 0.0);
+  }
+  to_conservative(wd, g.form, gam, ud);
+  to_conservative(whd, g.form, gam, uhd);
+  numerical_flux(FK >= 0 ? FK : g.kind, ud, uhd, n, gam, fd, g.form == FORM_ENTROPY ? wd : nullptr,
+                 g.form == FORM_ENTROPY ? whd : nullptr);
+  if (VISC) {
+    double qq[5][3];
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
+    for (int j = 0; j < NFN; ++j) {
+      const double a = pf[j];
+      const int row = sRows[k * NFN + j];
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQn[row * 15 + s2 * 3 + b];
+    }
+    Dual Gv[5][3];
+    visc_G(vg, g.form, wd, ud, qq, gam, Gv);
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) {
+      const Dual gn = (Gv[s2][0] * n[0] + Gv[s2][1] * n[1]) + Gv[s2][2] * n[2];
+      fd[s2] = fd[s2] + (gn - (0.5 * vg.pdiag[s2]) * (whd[s2] - wd[s2]));
+    }
+  }
+  const size_t base = ((size_t)e * 4 + k) * 25 * NQF + q;   // ten layout (E,4,25,NQF)
+  if (which == 0) {
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) {
+      hw_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
+      if (sHWk) sHWk[q * 25 + s2 * 5 + t] = fd[s2].d;
+    }
+  } else {
+    double hv[5];
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) {
+      hhat_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
+      hv[s2] = fd[s2].d;
+    }
+    if (sBnd[k] && g.has_uinf) {
+      Dual ui[5], gd[5];
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) ui[s2] = mk(g.uinf[s2], 0.0);
+      const double mn[3] = {-n[0], -n[1], -n[2]};
+      numerical_flux(FK >= 0 ? FK : g.kind, ui, uhd, mn, gam, gd);
+      if (VISC) {
+        double winf[5];
+        if (g.form == FORM_ENTROPY) entropy_vars(g.uinf, gam, winf);
+        else for (int s2 = 0; s2 < 5; ++s2) winf[s2] = g.uinf[s2];
+#pragma unroll
+        for (int s2 = 0; s2 < 5; ++s2) gd[s2] = gd[s2] + (0.0 - (0.5 * vg.pdiag[s2]) * (whd[s2] - winf[s2]));
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + gd[s2].d;
+    }
+    if (ptc != 0.0) {
+#pragma unroll
+      for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + (-ptc * uhd[s2].d);
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < 5; ++s2) hh_out[base + (s2 * 5 + t) * NQF] = hv[s2];
+  }
+}
 
 template <int P, bool VISC, int FK = -1>   // FK: flux kind fixed at compile time (-1: run time)
 __global__ void __launch_bounds__(32 * MHDG_LIN2_NW, 1)
@@ -1088,9 +1262,21 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     double* const S = L::GS ? sinv + (size_t)e * NM * NM : sS;
     if (!L::GS && tid == 0) bulk_wait_read();   // previous macro's S left shared memory
     __syncthreads();
+    const int en = e + gridDim.x;
     for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
     if (VISC)
       for (int i = tid; i < NN * 15; i += NT) sQn[i] = qn[(size_t)e * NN * 15 + i];
+    // the next macro's inputs towards L2 (its load phase was HBM-latency bound)
+    if (MHDG_LIN2_PREFETCH && en < g.E) {
+      if (tid < (NN * 5 * 8 + 127) / 128) prefetch_l2(reinterpret_cast<const char*>(w + (size_t)en * NN * 5) + tid * 128);
+      if (tid == 32) prefetch_l2(g.fid + en * 4);
+      if (tid == 33) prefetch_l2(g.det + en);
+      if (tid == 34) prefetch_l2(g.invj + (size_t)en * 9);
+      if (tid == 35) prefetch_l2(g.nrm + (size_t)en * 12);
+      if (tid == 36) prefetch_l2(g.area + (size_t)en * 4);
+      if (tid >= 64 && tid < 64 + (4 * NFN * 4 + 127) / 128)
+        prefetch_l2(reinterpret_cast<const char*>(g.tidx + (size_t)en * 4 * NFN) + (tid - 64) * 128);
+    }
     if (tid < 4) {
       sFid[tid] = g.fid[e * 4 + tid];
       sBnd[tid] = g.bnd ? g.bnd[e * 4 + tid] : 0;
@@ -1107,51 +1293,8 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     }
     LIN_T(0);
     // ---- pointwise duals for all volume quadrature points
-    for (int it = tid; it < NQ * 5; it += NT) {
-      const int q = it / 5, t = it % 5;
-      const double* ph = Bt + ((size_t)q * 4 + 3) * NN;
-      double wq[5] = {0, 0, 0, 0, 0};
-      for (int i = 0; i < NN; ++i) {
-        const double a = __ldg(ph + i);
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) wq[s2] += a * sW[i * 5 + s2];
-      }
-      Dual wd[5], ud[5];
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) wd[s2] = mk(wq[s2], s2 == t ? 1.0 : 0.0);
-      to_conservative(wd, g.form, gam, ud);
-      Dual F[5][3];
-      flux(ud, gam, F);
-      if (VISC) {
-        double qq[5][3];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
-        for (int i = 0; i < NN; ++i) {
-          const double a = __ldg(ph + i);
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQn[i * 15 + s2 * 3 + b];
-        }
-        Dual Gv[5][3];
-        visc_G(vg, g.form, wd, ud, qq, gam, Gv);
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) F[s2][a] = F[s2][a] + Gv[s2][a];
-      }
-      const double vw = sQW[q] * sGeo[0];
-      double* C = sC + (size_t)q * 4 * CS;
-#pragma unroll
-      for (int kk = 0; kk < 3; ++kk) {
-        const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2)
-          C[LIN2_CI(kk, s2 * 5 + t)] = -(vw * ((j0 * F[s2][0].d + j1 * F[s2][1].d) + j2 * F[s2][2].d));
-      }
-#pragma unroll
-      for (int s2 = 0; s2 < 5; ++s2) C[LIN2_CI(3, s2 * 5 + t)] = weight * (vw * ud[s2].d);
-    }
+    for (int it = tid; it < NQ * 5; it += NT)
+      lin2_volume_item<P, VISC, false>(g, vg, it, sW, sQn, sQW, sGeo, weight, sC);
     __syncthreads();
     LIN_T(1);
     // ---- S volume blocks on the tensor cores
@@ -1229,92 +1372,20 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
     //      then the S face blocks tile by tile (fixed accumulation order)
     __syncthreads();
     LIN_T(2);
+    if (MHDG_LIN2_PREFETCH && en < g.E && tid >= NT - 4 * NFN) {   // the next macro's trace rows towards L2 (last warps: they run fewer face items)
+      const int i = tid - (NT - 4 * NFN), k = i / NFN;
+      const int f = g.fid[en * 4 + k], t2 = g.tidx[(size_t)en * 4 * NFN + i];
+      prefetch_l2(trace + ((size_t)f * NFN + t2) * 5);
+    }
     for (int it4 = tid; it4 < 4 * NQF * 10; it4 += NT) {
-      {
-        const int k = it4 / (NQF * 10), it = it4 % (NQF * 10);
-        const double n[3] = {sGeo[10 + k * 3], sGeo[11 + k * 3], sGeo[12 + k * 3]};
-        double* sHWk = sHW + k * NQF * 25;
-        const int q = it / 10, t = (it % 10) % 5, which = (it % 10) / 5;
-        const double* pf = sPF + (k * NQF + q) * D::FS;
-        const double* fp = sFP + q * D::FS;
-        double wq[5] = {0, 0, 0, 0, 0}, whq[5] = {0, 0, 0, 0, 0};
-        for (int j = 0; j < NFN; ++j) {
-          const double a = pf[j], b = fp[j];
-          const int row = sRows[k * NFN + j];
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) {
-            wq[s2] += a * sW[row * 5 + s2];
-            whq[s2] += b * sTR[(k * NFN + j) * 5 + s2];
-          }
-        }
-        Dual wd[5], whd[5], ud[5], uhd[5], fd[5];
-#pragma unroll
-        for (int s2 = 0; s2 < 5; ++s2) {
-          wd[s2] = mk(wq[s2], (which == 0 && s2 == t) ? 1.0 : 0.0);
-          whd[s2] = mk(whq[s2], (which == 1 && s2 == t) ? 1.0 : 0.0);
-        }
-        to_conservative(wd, g.form, gam, ud);
-        to_conservative(whd, g.form, gam, uhd);
-        numerical_flux(FK >= 0 ? FK : g.kind, ud, uhd, n, gam, fd, g.form == FORM_ENTROPY ? wd : nullptr,
-                       g.form == FORM_ENTROPY ? whd : nullptr);
-        if (VISC) {
-          double qq[5][3];
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) qq[s2][0] = qq[s2][1] = qq[s2][2] = 0.0;
-          for (int j = 0; j < NFN; ++j) {
-            const double a = pf[j];
-            const int row = sRows[k * NFN + j];
-#pragma unroll
-            for (int s2 = 0; s2 < 5; ++s2)
-#pragma unroll
-              for (int b = 0; b < 3; ++b) qq[s2][b] += a * sQn[row * 15 + s2 * 3 + b];
-          }
-          Dual Gv[5][3];
-          visc_G(vg, g.form, wd, ud, qq, gam, Gv);
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) {
-            const Dual gn = (Gv[s2][0] * n[0] + Gv[s2][1] * n[1]) + Gv[s2][2] * n[2];
-            fd[s2] = fd[s2] + (gn - (0.5 * vg.pdiag[s2]) * (whd[s2] - wd[s2]));
-          }
-        }
-        const size_t base = ((size_t)e * 4 + k) * 25 * NQF + q;   // ten layout (E,4,25,NQF)
-        if (which == 0) {
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) {
-            hw_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
-            sHWk[q * 25 + s2 * 5 + t] = fd[s2].d;
-          }
-        } else {
-          double hv[5];
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) {
-            hhat_out[base + (s2 * 5 + t) * NQF] = fd[s2].d;
-            hv[s2] = fd[s2].d;
-          }
-          if (sBnd[k] && g.has_uinf) {
-            Dual ui[5], gd[5];
-#pragma unroll
-            for (int s2 = 0; s2 < 5; ++s2) ui[s2] = mk(g.uinf[s2], 0.0);
-            const double mn[3] = {-n[0], -n[1], -n[2]};
-            numerical_flux(FK >= 0 ? FK : g.kind, ui, uhd, mn, gam, gd);
-            if (VISC) {
-              double winf[5];
-              if (g.form == FORM_ENTROPY) entropy_vars(g.uinf, gam, winf);
-              else for (int s2 = 0; s2 < 5; ++s2) winf[s2] = g.uinf[s2];
-#pragma unroll
-              for (int s2 = 0; s2 < 5; ++s2) gd[s2] = gd[s2] + (0.0 - (0.5 * vg.pdiag[s2]) * (whd[s2] - winf[s2]));
-            }
-#pragma unroll
-            for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + gd[s2].d;
-          }
-          if (ptc != 0.0) {
-#pragma unroll
-            for (int s2 = 0; s2 < 5; ++s2) hv[s2] = hv[s2] + (-ptc * uhd[s2].d);
-          }
-#pragma unroll
-          for (int s2 = 0; s2 < 5; ++s2) hh_out[base + (s2 * 5 + t) * NQF] = hv[s2];
-        }
-      }
+#ifdef MHDG_RES_TIMING
+      const long long tr0 = clock64();
+#endif
+      lin2_face_item<P, VISC, FK>(g, vg, e, it4, sW, sTR, sQn, sPF, sFP, sRows, sGeo, sBnd, ptc, hw_out, hhat_out,
+                                  hh_out, sHW);
+#ifdef MHDG_RES_TIMING
+      if (tid == 0) atomicAdd(&g_res_clk[26 + min(it4 / NT, 2)], (unsigned long long)(clock64() - tr0));
+#endif
     }
     __syncthreads();
     LIN_T(3);
@@ -1329,6 +1400,74 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
       sHW[i] *= sFW[q] * sGeo[22 + k];
     }
 #endif
+#ifndef MHDG_LIN2_FACE_DMMA
+#define MHDG_LIN2_FACE_DMMA 1
+#endif
+#if MHDG_LIN2_FACE_DMMA && MHDG_LIN2_FACE_FMA
+    // S face blocks on the tensor cores: rows = the face's node pairs (i, j),
+    // K = face points, N = (s, t); A = pf_i pf_j formed on the fly, B = the
+    // staged weighted hw rows.  A warp takes (pair tile, half of the N tiles)
+    // units; every S entry of a face gets exactly one term, so the adds of a
+    // face do not collide (the former thread-per-(pair, s) FMA loop was
+    // bound by its shared-memory loads: 18k of the kernel's 98k cycles per
+    // macro at k = 3).
+    for (int k = 0; k < 4; ++k) {
+      __syncthreads();
+      const double* sHWk = sHW + k * NQF * 25;
+      constexpr int WMT = (NFN * NFN + 7) / 8, WKS = (NQF + 3) / 4;
+      const int kq = lane & 3, nr = lane >> 2;
+      // two units per pass: four independent DMMA chains per warp
+      for (int u0 = warp; u0 < 2 * WMT; u0 += MHDG_LIN2_FB_PAIR * L::NW) {
+        int ia[2], ja[2], nh[2];
+        bool rowok[2];
+        double c[2][2][2];
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+          const int u = u0 + uu * L::NW;
+          const int ija = (u >> 1) * 8 + nr;
+          nh[uu] = u & 1;
+          rowok[uu] = uu < MHDG_LIN2_FB_PAIR && u < 2 * WMT && ija < NFN * NFN;
+          ia[uu] = rowok[uu] ? ija / NFN : 0;
+          ja[uu] = rowok[uu] ? ija % NFN : 0;
+          c[uu][0][0] = c[uu][0][1] = c[uu][1][0] = c[uu][1][1] = 0.0;
+        }
+        const bool two = MHDG_LIN2_FB_PAIR > 1 && u0 + L::NW < 2 * WMT;   // warp-uniform
+#pragma unroll
+        for (int ks = 0; ks < WKS; ++ks) {
+          const int qa = ks * 4 + kq;
+          const double* pf = sPF + (k * NQF + (qa < NQF ? qa : 0)) * D::FS;
+          double av[2], bv[2][2];
+#pragma unroll
+          for (int uu = 0; uu < 2; ++uu) {
+            av[uu] = (rowok[uu] && qa < NQF) ? pf[ia[uu]] * pf[ja[uu]] : 0.0;
+#pragma unroll
+            for (int ntl = 0; ntl < 2; ++ntl) {
+              const int n = (nh[uu] * 2 + ntl) * 8 + nr;
+              bv[uu][ntl] = (qa < NQF && n < 25) ? sHWk[qa * 25 + n] : 0.0;
+            }
+          }
+          dmma_8x8x4(c[0][0], av[0], bv[0][0]);
+          dmma_8x8x4(c[0][1], av[0], bv[0][1]);
+          if (two) {
+            dmma_8x8x4(c[1][0], av[1], bv[1][0]);
+            dmma_8x8x4(c[1][1], av[1], bv[1][1]);
+          }
+        }
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu)
+          if (rowok[uu]) {
+            const int rb = sRows[k * NFN + ia[uu]] * 5, cb = sRows[k * NFN + ja[uu]] * 5;
+#pragma unroll
+            for (int ntl = 0; ntl < 2; ++ntl)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int st = (nh[uu] * 2 + ntl) * 8 + kq * 2 + h;
+                if (st < 25) S[(rb + st / 5) * NM + cb + st % 5] += c[uu][ntl][h];
+              }
+          }
+      }
+    }
+#else
     for (int k = 0; k < 4; ++k) {
       __syncthreads();
       const double* sHWk = sHW + k * NQF * 25;
@@ -1357,6 +1496,7 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
         for (int t = 0; t < 5; ++t) S[r * NM + c + t] += acc2[t];
       }
     }
+#endif
     // ---- S (row-major) to the S^-1 buffer with one TMA bulk store (80 KB at
     //      k = 3); the Gauss-Jordan inverts it in place (GS: already there)
     if (!L::GS) {

@@ -39,4 +39,5 @@ out.update({"gj50_" + nm: buf[10 + i] / F for i, nm in enumerate(gn)})
 pn = ["chain_D", "chain_gj8x8", "chain_publish", "unused"]
 out.update({"gj100_bp_" + nm: buf[16 + i] / E for i, nm in enumerate(pn)})
 out.update({"gj50_bp_" + nm: buf[21 + i] / F for i, nm in enumerate(pn)})
+out.update({f"lin_face_round{i}": buf[26 + i] / E for i in range(3)})
 print(json.dumps(out, indent=1))
