@@ -277,6 +277,16 @@ void mhdg_krylov_destroy(mhdg_krylov* k);
  * went through the partial-pivoting pass (synchronizes the stream). */
 int mhdg_gj_fallbacks(mhdg_ctx* ctx, int* out, void* stream);
 
+/* Batched in-place inverse of nmat row-major matrices of order n (20, 50 or
+ * 100), column-major result: the device replacement of the reference's
+ * per-macro lu_factor / lu_solve (assembly.py:718-733) and per-face block
+ * factorization (assembly.py:736-752), exposed for direct testing.  Diagonal-
+ * pivot pass first, partial pivoting for the matrices that fail its checks
+ * (*fallbacks = their number); MHDG_SINGULAR_LOCAL with *item = the first
+ * singular matrix.  nmat <= max(macros, faces) of the context.  Synchronizes. */
+int mhdg_batched_inverse(mhdg_ctx* ctx, int n, int nmat, double* mats, int* fallbacks,
+                         int64_t* item, void* stream);
+
 /* number of library kernels launched since creation (evidence counter) */
 int64_t mhdg_launch_count(const mhdg_ctx* ctx);
 /* FP64 FMA throughput probe (roofline denominator), returns GFLOP/s */

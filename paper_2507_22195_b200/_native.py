@@ -118,6 +118,7 @@ _SIGS = {
                                     C.c_void_p]),
     "mhdg_krylov_destroy": (None, [C.c_void_p]),
     "mhdg_gj_fallbacks": (C.c_int, [C.c_void_p, dptr, C.c_void_p]),
+    "mhdg_batched_inverse": (C.c_int, [C.c_void_p, C.c_int, C.c_int, dptr, C.c_void_p, C.c_void_p, C.c_void_p]),
     "mhdg_launch_count": (C.c_int64, [C.c_void_p]),
     "mhdg_fp64_probe": (C.c_double, [C.c_int, C.c_void_p]),
     "mhdg_dmma_probe": (C.c_double, [C.c_int, C.c_void_p]),

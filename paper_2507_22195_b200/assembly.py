@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .errors import InvalidConfig
+from .errors import InvalidConfig, SingularLocalMatrix
 from .fluxes import DissipationSpec
 from .gas import GasModel
 from .tables import HDGTables
@@ -272,6 +272,28 @@ class Discretization:
         out = (C.c_int * 2)()
         N.raise_for(self._lib.mhdg_gj_fallbacks(self._ctx, C.cast(out, C.c_void_p), N.stream_handle()))
         return int(out[0]), int(out[1])
+
+    def batched_inverse(self, mats):
+        """Inverses of a batch of square matrices (order 20, 50 or 100) by
+        the device Gauss-Jordan that replaces the reference's per-macro
+        lu_factor / lu_solve (assembly.py:718-733).  mats: (n_mat, n, n)
+        float64 on the device; returns (inverses, fallbacks) where fallbacks
+        counts the matrices that needed the partial-pivoting pass.  Raises
+        SingularLocalMatrix(macro = index in the batch) like the reference."""
+        torch = _torch()
+        a = self._dev(mats).to(torch.float64)
+        if a.dim() != 3 or a.shape[1] != a.shape[2]:
+            raise InvalidConfig("batched_inverse expects (n_mat, n, n)")
+        work = a.contiguous().clone()
+        fb, item = C.c_int(0), C.c_int64(-1)
+        rc = self._lib.mhdg_batched_inverse(self._ctx, int(a.shape[1]), int(a.shape[0]), N.ptr(work),
+                                            C.cast(C.byref(fb), C.c_void_p), C.cast(C.byref(item), C.c_void_p),
+                                            N.stream_handle())
+        if rc == 3:
+            raise SingularLocalMatrix(f"singular condensed block on macro {item.value}", macro=int(item.value))
+        N.raise_for(rc, None, "(batched_inverse)")
+        # the kernel writes the inverse column-major
+        return work.transpose(1, 2), int(fb.value)
 
     @property
     def launch_count(self):

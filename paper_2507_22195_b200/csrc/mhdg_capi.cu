@@ -662,6 +662,38 @@ static int gj_lookahead_ga(mhdg_ctx* c, int nmat, double* mats, unsigned long lo
   return MHDG_OK;
 }
 
+// Batched in-place inverse of `nmat` row-major matrices of order n (20, 50 or
+// 100: the condensed / face block orders of k = 1..3), column-major result,
+// through the same two-pass Gauss-Jordan the linearization uses.  On return
+// fallbacks (host) holds the number of matrices that took the partial-
+// pivoting pass; a singular matrix reports MHDG_SINGULAR_LOCAL with its index.
+extern "C" int mhdg_batched_inverse(mhdg_ctx* c, int n, int nmat, double* mats, int* fallbacks, int64_t* item,
+                                    void* stream) {
+  cudaStream_t s = S(stream);
+  CK(cudaSetDevice(c->device));
+  const unsigned long long none = ~0ULL;
+  if (nmat < 0 || nmat > std::max(c->E, c->geo.F)) return MHDG_INVALID_CONFIG;   // fallback list capacity
+  CK(cudaMemsetAsync(c->d_status, 0xff, sizeof(unsigned long long), s));
+  int rc = MHDG_INVALID_CONFIG;
+  if (n == 20) rc = gj_lookahead<20>(c, nmat, mats, c->d_status, s, 0);
+  else if (n == 50) rc = gj_lookahead<50>(c, nmat, mats, c->d_status, s, 0);
+  else if (n == 100) rc = gj_lookahead<100>(c, nmat, mats, c->d_status, s, 0);
+  if (rc) return rc;
+  c->launches++;
+  unsigned long long st = none;
+  int fb = 0;
+  CK(cudaMemcpyAsync(&st, c->d_status, sizeof(st), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&fb, c->d_fb, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  if (fallbacks) *fallbacks = fb;
+  if (st != none) {
+    if (item) *item = (int64_t)(st & ((1ULL << 40) - 1));
+    return MHDG_SINGULAR_LOCAL;
+  }
+  return MHDG_OK;
+}
+
 template <int P>
 static int launch_linearize2(mhdg_ctx* c, const double* w, const double* q, const double* tr, double weight,
                              double ptc, const mhdg_lin_buffers* L, cudaStream_t s) {

@@ -255,7 +255,17 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   int* sNF = sRows + 4 * NFN;                      // 3*NN
   int* iball = sNF + 3 * NN;                       // NG * 2 * EB * per_macro_int
   const int tid = threadIdx.x, lane = tid & 31;
-  const int grp = tid / GT, gtid = tid % GT, gwarp = gtid >> 5;
+  // Optional: group g = the warps with warp id % NG == g: a warp issues on scheduler
+  // warp id % 4, so with four groups each group owns one scheduler and its
+  // warps move through the pointwise and the DMMA phases together (a
+  // dependent DFMA chain sharing a scheduler with another group's DMMA
+  // stream runs 5x slower: 8.8 -> 47.5 cycles per operation, measured).
+#ifndef MHDG_RES_SCHED_GROUPS
+#define MHDG_RES_SCHED_GROUPS 0   // measured: KEPES config 3 2.94 vs 2.85 ms (worse), ES config 2 0.383 vs 0.406 ms (better)
+#endif
+  const int grp = MHDG_RES_SCHED_GROUPS ? (tid >> 5) % R::NG : tid / GT;
+  const int gwarp = MHDG_RES_SCHED_GROUPS ? (tid >> 5) / R::NG : (tid % GT) >> 5;
+  const int gtid = gwarp * 32 + lane;
   for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
   for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
   for (int i = tid; i < NQ; i += NT) sQW[i] = g.qw[i];
