@@ -152,6 +152,12 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS) and its completion wait
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 #ifdef MHDG_RES_TIMING
@@ -215,15 +221,16 @@ struct ResCfg {
   // w / trace (phase 1) and the face / volume partial rows (phases 2-3)
   // share one region; the far-field flux rows HG exist only with a
   // free-stream boundary (has_uinf)
-  static constexpr int AREG = (W_ + TR_ > FR_ + VOL_) ? W_ + TR_ : FR_ + VOL_;
-  static constexpr int per_macro_base = AREG + G_ + H_ + GEO_;
+  // w / trace / geometry of a batch arrive by cp.async in a staging region of
+  // their own (STG_ per macro), read in place by phase 1; the face / volume
+  // partial rows (phases 2-3) have theirs
+  static constexpr int AREG = FR_ + VOL_;
+  static constexpr int STG_ = W_ + TR_ + GEO_;
+  static constexpr int per_macro_base = AREG + G_ + H_ + STG_;
   static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF + AF_ +
                                 (SB ? D::NQ * 4 * RS + D::NN * D::NQ : 0);
   static constexpr int per_macro_int = 4 + 4 * D::NFN + 4;   // x 2 slots (double-buffered)
   static constexpr int META = 4 + 4 * D::NFN + 4;
-  static constexpr int WPT = (EB * D::NN * 5 + GT - 1) / GT;       // prefetch registers per thread
-  static constexpr int TPT = (EB * 4 * D::NFN * 5 + GT - 1) / GT;
-  static constexpr int GPT = (EB * 26 + GT - 1) / GT;
   static constexpr int table_int = 4 * D::NFN + 3 * D::NN;
   __host__ __device__ static constexpr int per_macro(int has_uinf) { return per_macro_base + (has_uinf ? H_ : 0); }
   __host__ __device__ static constexpr size_t bytes(int has_uinf) {
@@ -298,13 +305,13 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   const int bar_id = 1 + grp;
   auto gsync = [&]() { group_sync(bar_id, GT); };
 
-  auto W = [&](int m) { return mb + m * PM; };
-  auto TR = [&](int m) { return W(m) + R::W_; };
-  auto FR = [&](int m) { return W(m); };                 // aliases W / TR (phases 2-3)
-  auto VOL = [&](int m) { return W(m) + R::FR_; };
-  auto G = [&](int m) { return W(m) + R::AREG; };
+  auto FR = [&](int m) { return mb + m * PM; };          // face partial rows (phases 2-3)
+  auto VOL = [&](int m) { return FR(m) + R::FR_; };
+  auto G = [&](int m) { return FR(m) + R::AREG; };
   auto H = [&](int m) { return G(m) + R::G_; };
-  auto GEO = [&](int m) { return H(m) + R::H_; };
+  auto W = [&](int m) { return H(m) + R::H_; };          // staging: w, trace, geometry (cp.async)
+  auto TR = [&](int m) { return W(m) + R::W_; };
+  auto GEO = [&](int m) { return TR(m) + R::TR_; };
   auto HG = [&](int m) { return GEO(m) + R::GEO_; };     // only with has_uinf
   // meta (face ids, trace permutations, boundary flags) is double-buffered:
   // slot `cur` serves the batch being computed, slot `cur ^ 1` receives the
@@ -318,34 +325,26 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   auto meta_ld = [&](int e0n, int i, int& v) {     // i over EB*META (packed per-macro meta)
     if (e0n + i / R::META < g.E) v = g.meta[(size_t)e0n * R::META + i];
   };
-  auto geo_ld = [&](int e0n, int i) -> double {     // i over EB*26 (packed per-macro geometry)
-    return e0n + i / 26 < g.E ? g.geo26[(size_t)e0n * 26 + i] : 0.0;
-  };
-  double pW[R::WPT], pT[R::TPT], pG[R::GPT];
+  // The next batch's w / geometry / trace values go straight from global to
+  // the staging region with cp.async (no registers: as register prefetches
+  // they were spilled at the 128-register cap, and the spill store waited for
+  // each load, 14% of the kernel's stall samples).  Issued after the barrier
+  // that ends phase 1 (the staging region is read only by phase 1), waited
+  // for at the top of the next batch.
   auto prefetch_wg = [&](int e0n) {                 // w and geometry
     const int nmn = min(EB, g.E - e0n);
-#pragma unroll
-    for (int c = 0; c < R::WPT; ++c) {
-      const int i = gtid + c * GT;
-      if (i < nmn * NN * 5) pW[c] = w[(size_t)e0n * NN * 5 + i];
-    }
-#pragma unroll
-    for (int c = 0; c < R::GPT; ++c) {
-      const int i = gtid + c * GT;
-      if (i < EB * 26) pG[c] = geo_ld(e0n, i);
-    }
+    for (int i = gtid; i < nmn * (NN * 5 / 1); i += GT)
+      cp_async8(W(i / (NN * 5)) + i % (NN * 5), w + (size_t)e0n * NN * 5 + i);
+    for (int i = gtid; i < nmn * 26; i += GT)
+      cp_async8(GEO(i / 26) + i % 26, g.geo26 + (size_t)e0n * 26 + i);
   };
   auto prefetch_tr = [&](int e0n, int slot) {       // trace values through slot's meta
     const int nmn = min(EB, g.E - e0n);
-#pragma unroll
-    for (int c = 0; c < R::TPT; ++c) {
-      const int i = gtid + c * GT;
-      if (i < nmn * 4 * NFN * 5) {
-        const int m = i / (4 * NFN * 5), r = i % (4 * NFN * 5);
-        const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
-        const int* mt = ib + (slot * EB + m) * R::per_macro_int;
-        pT[c] = trace[((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s];
-      }
+    for (int i = gtid; i < nmn * 4 * NFN * 5; i += GT) {
+      const int m = i / (4 * NFN * 5), r = i % (4 * NFN * 5);
+      const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
+      const int* mt = ib + (slot * EB + m) * R::per_macro_int;
+      cp_async8(TR(m) + r, trace + ((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s);
     }
   };
   const int gidx = blockIdx.x * R::NG + grp, gstride = gridDim.x * R::NG;
@@ -369,24 +368,9 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   for (int e0 = gidx * EB; e0 < g.E; e0 += gstride * EB) {
     const int nm = min(EB, g.E - e0);
     const int e1 = e0 + gstride * EB;
+    cp_async_wait_all();
     gsync();
     RES_T(0);
-#pragma unroll
-    for (int c = 0; c < R::WPT; ++c) {
-      const int i = gtid + c * GT;
-      if (i < nm * NN * 5) W(i / (NN * 5))[i % (NN * 5)] = pW[c];
-    }
-#pragma unroll
-    for (int c = 0; c < R::TPT; ++c) {
-      const int i = gtid + c * GT;
-      if (i < nm * 4 * NFN * 5) TR(i / (4 * NFN * 5))[i % (4 * NFN * 5)] = pT[c];
-    }
-#pragma unroll
-    for (int c = 0; c < R::GPT; ++c) {
-      const int i = gtid + c * GT;
-      if (i < EB * 26) GEO(i / 26)[i % 26] = pG[c];
-    }
-    gsync();
     RES_T(1);
 
     // ---- 1a. face quadrature points: two-point flux, weighted
@@ -473,11 +457,14 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         meta_ld(e1, i, v);
         ib[((cur ^ 1) * EB + i / R::META) * R::per_macro_int + i % R::META] = v;
       }
-      prefetch_wg(e1);
     }
     RES_T(3);
     gsync();
     RES_T(4);
+    if (e1 < g.E) {   // phase 1 is over for the whole group: the staging region is free
+      prefetch_wg(e1);
+      prefetch_tr(e1, cur ^ 1);
+    }
 
     // ---- 2. contraction on the FP64 tensor cores, all WPM warps of a macro
     // alike: warp r takes the volume-test K range q in [r NQ/WPM, (r+1)
@@ -570,7 +557,6 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     RES_T(5);
     gsync();
     RES_T(6);
-    if (e1 < g.E) prefetch_tr(e1, cur ^ 1);
     // ---- 3. r_w = volume part + face parts (tile order)
     for (int o = gtid; o < nm * NN * 5; o += GT) {
       const int m = o / (NN * 5), is = o % (NN * 5), i = is / 5, s = is % 5;
