@@ -70,6 +70,25 @@ static const int RED_THREADS = 256;
 
 static cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
+// Tangent frame of a unit normal on the host (fluxes.py:60-78, the same steps
+// as the device tangents() in mhdg_math.cuh): e = the axis of the smallest
+// |n_k|, t1 = normalize(e - (e.n) n), t2 = n x t1.
+static void host_tangents(const double* n, double* t1, double* t2) {
+  const double an[3] = {std::fabs(n[0]), std::fabs(n[1]), std::fabs(n[2])};
+  int k = 0;
+  if (an[1] < an[k]) k = 1;
+  if (an[2] < an[k]) k = 2;
+  double e[3] = {0.0, 0.0, 0.0};
+  e[k] = 1.0;
+  const double en = (e[0] * n[0] + e[1] * n[1]) + e[2] * n[2];
+  for (int a = 0; a < 3; ++a) t1[a] = e[a] - en * n[a];
+  const double nrm = std::sqrt((t1[0] * t1[0] + t1[1] * t1[1]) + t1[2] * t1[2]);
+  for (int a = 0; a < 3; ++a) t1[a] = t1[a] / nrm;
+  t2[0] = n[1] * t1[2] - n[2] * t1[1];
+  t2[1] = n[2] * t1[0] - n[0] * t1[2];
+  t2[2] = n[0] * t1[1] - n[1] * t1[0];
+}
+
 template <class T>
 static T* upload(mhdg_ctx* c, const T* host, size_t n, int* err) {
   if (!host || n == 0) return nullptr;
@@ -195,14 +214,15 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   g.bnd = t->boundary_st ? upload(c, t->boundary_st, E * 4, err) : nullptr;
   g.fsides = upload_i64(c, t->face_sides, (size_t)c->n_owned * 2, err);
   {   // packed per-macro geometry and meta for the residual's coalesced prefetch
-    std::vector<double> geo26(E * 26);
+    std::vector<double> geo26(E * 50);
     std::vector<int> meta(E * (8 + 4 * NFN));
     for (size_t e = 0; e < E; ++e) {
-      double* gp = &geo26[e * 26];
+      double* gp = &geo26[e * 50];
       gp[0] = t->sub_det[e];
       for (int i = 0; i < 9; ++i) gp[1 + i] = t->sub_inv_jac[e * 9 + i];
       for (int i = 0; i < 12; ++i) gp[10 + i] = t->face_normals[e * 12 + i];
       for (int i = 0; i < 4; ++i) gp[22 + i] = t->face_area[e * 4 + i];
+      for (int k = 0; k < 4; ++k) host_tangents(gp + 10 + 3 * k, gp + 26 + 6 * k, gp + 29 + 6 * k);
       int* mp = &meta[e * (8 + 4 * NFN)];
       for (int i = 0; i < 4; ++i) mp[i] = (int)t->face_id_st[e * 4 + i];
       for (int i = 0; i < 4 * NFN; ++i) mp[4 + i] = (int)t->trace_idx[e * 4 * NFN + i];
@@ -384,7 +404,7 @@ static Geo geo_range(const Geo& g0, int e0, int e1, int nfn) {
   g.fid += (size_t)e0 * 4;
   g.tidx += (size_t)e0 * 4 * nfn;
   if (g.bnd) g.bnd += (size_t)e0 * 4;
-  g.geo26 += (size_t)e0 * 26;
+  g.geo26 += (size_t)e0 * 50;
   g.meta += (size_t)e0 * (8 + 4 * nfn);
   return g;
 }

@@ -84,7 +84,7 @@ struct Geo {
   const int* tidx;     // (E, 4, NFN)
   const unsigned char* bnd;  // (E, 4)
   const int* fsides;   // (F, 2)
-  const double* geo26; // (E, 26): det, J^-1 (9), normals (12), areas (4)
+  const double* geo26; // (E, 50): det, J^-1 (9), normals (12), areas (4), tangent frames t1, t2 of the normals (24)
   const int* meta;     // (E, 8 + 4 NFN): face ids (4), trace permutations (4 NFN), boundary flags (4)
   int e_base;          // global index of macro 0 of this (sub-range) view, for error reports
   int has_uinf;
@@ -217,7 +217,7 @@ struct ResCfg {
   static constexpr int RS = D::NN + ((4 - D::NN) % 16 + 16) % 16;
   static constexpr int GS = 21;                    // G row stride (odd)
   static constexpr int W_ = D::NN * 5, TR_ = 4 * D::NFN * 5, G_ = D::NQ * GS, H_ = 4 * D::NQF * 5,
-                       FR_ = 4 * D::NFN * 5, VOL_ = WPM * D::NN * 5, GEO_ = 26;
+                       FR_ = 4 * D::NFN * 5, VOL_ = WPM * D::NN * 5, GEO_ = 50;
   // w / trace (phase 1) and the face / volume partial rows (phases 2-3)
   // share one region; the far-field flux rows HG exist only with a
   // free-stream boundary (has_uinf)
@@ -335,8 +335,8 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     const int nmn = min(EB, g.E - e0n);
     for (int i = gtid; i < nmn * (NN * 5 / 1); i += GT)
       cp_async8(W(i / (NN * 5)) + i % (NN * 5), w + (size_t)e0n * NN * 5 + i);
-    for (int i = gtid; i < nmn * 26; i += GT)
-      cp_async8(GEO(i / 26) + i % 26, g.geo26 + (size_t)e0n * 26 + i);
+    for (int i = gtid; i < nmn * R::GEO_; i += GT)
+      cp_async8(GEO(i / R::GEO_) + i % R::GEO_, g.geo26 + (size_t)e0n * R::GEO_ + i);
   };
   auto prefetch_tr = [&](int e0n, int slot) {       // trace values through slot's meta
     const int nmn = min(EB, g.E - e0n);
@@ -400,7 +400,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       const double n[3] = {geo[10 + k * 3], geo[11 + k * 3], geo[12 + k * 3]};
       double fh[5];
       numerical_flux(FK >= 0 ? FK : g.kind, u, uh, n, gam, fh, g.form == FORM_ENTROPY ? wq : nullptr,
-                     g.form == FORM_ENTROPY ? whq : nullptr);
+                     g.form == FORM_ENTROPY ? whq : nullptr, geo + 26 + 6 * k);
       const double fwq = sFW[q] * geo[22 + k];
       double* h = H(m) + kq * 5;
 #pragma unroll
@@ -418,6 +418,13 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     for (int it = gtid; it < nm * NQ; it += GT) {
       const int m = it / NQ, q = it % NQ, e = e0 + m;
       const double* sw = W(m);
+      // the stage offset of this point first: its global-load latency runs
+      // under the interpolation and the flux evaluation
+      double off[5] = {0, 0, 0, 0, 0};
+      if (has_stage && offset) {
+#pragma unroll
+        for (int s = 0; s < 5; ++s) off[s] = __ldcs(offset + ((size_t)e * NQ + q) * 5 + s);
+      }
       double wq[5] = {0, 0, 0, 0, 0};
 #pragma unroll 4
       for (int i = 0; i < NN; ++i) {
@@ -444,7 +451,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         double tmp = 0.0;
         if (has_stage) {
           tmp = alpha * u[s];
-          if (offset) tmp = tmp + offset[((size_t)e * NQ + q) * 5 + s];
+          if (offset) tmp = tmp + off[s];
           tmp = vw * tmp;
         }
         gr[15 + s] = tmp;
@@ -464,6 +471,10 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     if (e1 < g.E) {   // phase 1 is over for the whole group: the staging region is free
       prefetch_wg(e1);
       prefetch_tr(e1, cur ^ 1);
+      if (has_stage && offset) {   // the next batch's stage offsets towards L2
+        const int nmn = min(EB, g.E - e1);
+        for (int i = gtid * 16; i < nmn * NQ * 5; i += GT * 16) prefetch_l2(offset + (size_t)e1 * NQ * 5 + i);
+      }
     }
 
     // ---- 2. contraction on the FP64 tensor cores, all WPM warps of a macro
