@@ -157,6 +157,10 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async4(int* dst, const int* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
@@ -371,6 +375,14 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
     cp_async_wait_all();
     gsync();
     RES_T(0);
+    // next batch's meta into the other slot (free since the barrier above),
+    // asynchronously under phase 1
+    if (e1 < g.E) {
+      const int nmn = min(EB, g.E - e1);
+      for (int i = gtid; i < nmn * R::META; i += GT)
+        cp_async4(ib + ((cur ^ 1) * EB + i / R::META) * R::per_macro_int + i % R::META,
+                  g.meta + (size_t)e1 * R::META + i);
+    }
     RES_T(1);
 
     // ---- 1a. face quadrature points: two-point flux, weighted
@@ -457,14 +469,8 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
         gr[15 + s] = tmp;
       }
     }
-    // next batch: meta straight into the other slot, w / geometry into registers
-    if (e1 < g.E) {
-      for (int i = gtid; i < EB * R::META; i += GT) {
-        int v = 0;
-        meta_ld(e1, i, v);
-        ib[((cur ^ 1) * EB + i / R::META) * R::per_macro_int + i % R::META] = v;
-      }
-    }
+    // the next batch's meta (issued at the top of this batch) has landed
+    cp_async_wait_all();
     RES_T(3);
     gsync();
     RES_T(4);
