@@ -254,6 +254,14 @@ typedef struct {
   double inner_rtol;
   int inner_iters;
   int inner_precond;
+  /* 1: the inner sweep forms its true residual b - A x after the cycle, as
+   * solver.py:62-72 does literally (one more matvec per sweep).  0: when the
+   * cycle ended on the iteration cap the sweep returns x whatever that
+   * residual is (solver.py:68-69: exact), and when it ended on the Arnoldi
+   * residual test |g_k| / |b| <= inner_rtol that estimate stands in for the
+   * true residual (equal in exact arithmetic); breakdown exits still form
+   * the true residual.  The outer level always forms it. */
+  int inner_true_residual;
 } mhdg_krylov_params;
 
 typedef struct {

@@ -28,6 +28,7 @@ struct mhdg_ctx {
   int visc;
   ViscGeo vg;
   int n_sms;
+  size_t smem_optin;   // opt-in dynamic shared memory per CTA
   Geo geo;
   std::vector<void*> allocs;
   unsigned long long* d_status;
@@ -172,6 +173,11 @@ extern "C" mhdg_ctx* mhdg_create(const mhdg_tables* t, int device, int* err) {
   c->d_scratch = nullptr;
   c->scratch_bytes = 0;
   cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    c->smem_optin = optin > 0 ? (size_t)optin : 48 * 1024;
+  }
   const size_t E = t->n_macros, F = t->n_faces;
   // B table (NQ, 4, NN): dphi_x, dphi_y, dphi_z, phi
   std::vector<double> B((size_t)NQ * 4 * NN);
@@ -468,16 +474,21 @@ static int launch_residual(mhdg_ctx* c, const double* w, const double* tr, int h
   w += e0 * NMe;
   rw += e0 * NMe;
   if (off) off += e0 * NQe;
-  size_t smem = RC::bytes(c->geo.has_uinf);
+  // groups per CTA: all NG unless the far-field rows of a free-stream
+  // boundary push the CTA over the shared-memory limit
+  int ng = RC::NG;
+  while (ng > 1 && RC::bytes(c->geo.has_uinf, ng) > c->smem_optin) --ng;
+  size_t smem = RC::bytes(c->geo.has_uinf, ng);
   // the ES flux gets its own instantiation (40 B of spills instead of 244 B
   // with the run-time switch over all four kinds; a KEPES-only variant
   // allocates worse than the switch, so KEPES / EC / LF share it)
   auto go = [&](auto kern) -> int {
     if (set_smem(kern, smem)) return MHDG_CUDA_ERROR;
-    int per_sm = occ(kern, RC::NT, smem);
+    const int nt = ng * RC::GT;
+    int per_sm = occ(kern, nt, smem);
     const int batches = (gv.E + RC::EB - 1) / RC::EB;
-    int blocks = std::min((batches + RC::NG - 1) / RC::NG, c->n_sms * per_sm);
-    kern<<<std::max(1, blocks), RC::NT, smem, s>>>(gv, w, tr, has_stage, alpha, off, check, rw, rt,
+    int blocks = std::min((batches + ng - 1) / ng, c->n_sms * per_sm);
+    kern<<<std::max(1, blocks), nt, smem, s>>>(gv, w, tr, has_stage, alpha, off, check, rw, rt,
                                                    c->d_status);
     return MHDG_OK;
   };

@@ -211,7 +211,14 @@ struct ResCfg {
   static constexpr bool SB = P <= 3;               // basis tables in shared memory
   static constexpr int NT = NG * GT;
   static constexpr int MINB = (P >= 4) ? 2 : 1;    // resident CTAs per SM (register cap)
-  static constexpr int WPM = NW / EB > 0 ? NW / EB : 1;   // warps per macro in the contraction
+  // warps per macro in the contraction.  P = 2 has EB = 3 macros for 4 warps:
+  // one job per macro left a warp idle (barrier stalls 19% of the samples), so
+  // each macro is split four ways (K quarters of the volume test, one face each)
+  static constexpr int WPM = (P == 2) ? 4 : (NW / EB > 0 ? NW / EB : 1);
+  // P = 1: the tiles are too small for the tensor cores (NN = 4 of 8 columns,
+  // one DMMA per face followed by a scattered epilogue: the contraction was
+  // 42% of the kernel); one thread per output entry on the FP64 pipe instead
+  static constexpr bool POINTWISE_TEST = (P == 1);
   static constexpr int NTILE = (D::NN + 7) / 8;    // DMMA N tiles over nodes (volume test)
   static constexpr int FMT = (2 * D::NFN + 7) / 8; // face test: M tiles over phi_face + fphi rows
   static constexpr int FKS = (D::NQF + 3) / 4;     // face test: K steps over face points
@@ -237,9 +244,11 @@ struct ResCfg {
   static constexpr int META = 4 + 4 * D::NFN + 4;
   static constexpr int table_int = 4 * D::NFN + 3 * D::NN;
   __host__ __device__ static constexpr int per_macro(int has_uinf) { return per_macro_base + (has_uinf ? H_ : 0); }
-  __host__ __device__ static constexpr size_t bytes(int has_uinf) {
-    return (size_t)(tables + NG * EB * per_macro(has_uinf)) * 8 +
-           (size_t)(table_int + NG * 2 * EB * per_macro_int) * 4;
+  // ng: groups of the launch (NG, fewer when the far-field rows of a
+  // free-stream boundary would not fit: k = 3 with has_uinf runs 3 groups)
+  __host__ __device__ static constexpr size_t bytes(int has_uinf, int ng = NG) {
+    return (size_t)(tables + ng * EB * per_macro(has_uinf)) * 8 +
+           (size_t)(table_int + ng * 2 * EB * per_macro_int) * 4;
   }
 };
 
@@ -250,7 +259,8 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
            double* __restrict__ r_w, double* __restrict__ r_tr, unsigned long long* status) {
   using D = Dims<P>;
   using R = ResCfg<P>;
-  constexpr int NT = R::NT, GT = R::GT, EB = R::EB, NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF;
+  constexpr int GT = R::GT, EB = R::EB, NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF;
+  const int NT = blockDim.x, NG = NT / GT;   // groups of this launch (<= R::NG)
   constexpr int GS = R::GS, RS = R::RS;
   extern __shared__ __align__(16) double smem[];
   const int PM = R::per_macro(g.has_uinf);
@@ -262,7 +272,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   double* sB = sAF + R::AF_;                       // NQ*4*RS (SB)
   double* sPT = sB + (R::SB ? NQ * 4 * RS : 0);    // NN*NQ   (SB)
   double* mball = smem + R::tables;                // NG * EB * PM
-  int* sRows = (int*)(mball + R::NG * EB * PM);    // 4*NFN
+  int* sRows = (int*)(mball + NG * EB * PM);       // 4*NFN
   int* sNF = sRows + 4 * NFN;                      // 3*NN
   int* iball = sNF + 3 * NN;                       // NG * 2 * EB * per_macro_int
   const int tid = threadIdx.x, lane = tid & 31;
@@ -271,11 +281,18 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
   // warps move through the pointwise and the DMMA phases together (a
   // dependent DFMA chain sharing a scheduler with another group's DMMA
   // stream runs 5x slower: 8.8 -> 47.5 cycles per operation, measured).
-#ifndef MHDG_RES_SCHED_GROUPS
-#define MHDG_RES_SCHED_GROUPS 0   // measured: KEPES config 3 2.94 vs 2.85 ms (worse), ES config 2 0.383 vs 0.406 ms (better)
+  // Measured at n = 32 (session 5, ms, contiguous groups vs one group per
+  // scheduler): ES k = 2 1.083 / 1.030, ES k = 3 1.996 / 1.940, KEPES k = 3
+  // 2.194 / 2.231, ES k = 1 0.385 / 0.646: on for the ES instantiation at
+  // k = 2, 3 (MHDG_RES_SCHED_GROUPS = 0 / 1 forces it off / on everywhere).
+#ifdef MHDG_RES_SCHED_GROUPS
+  constexpr bool SCHED = MHDG_RES_SCHED_GROUPS != 0;
+#else
+  constexpr bool SCHED = FK == FLUX_ES && (P == 2 || P == 3);
 #endif
-  const int grp = MHDG_RES_SCHED_GROUPS ? (tid >> 5) % R::NG : tid / GT;
-  const int gwarp = MHDG_RES_SCHED_GROUPS ? (tid >> 5) / R::NG : (tid % GT) >> 5;
+  const bool sched = SCHED && NG == 4;
+  const int grp = sched ? (tid >> 5) % NG : tid / GT;
+  const int gwarp = sched ? (tid >> 5) / NG : (tid % GT) >> 5;
   const int gtid = gwarp * 32 + lane;
   for (int i = tid; i < 4 * NQF * NFN; i += NT) sPF[(i / NFN) * D::FS + i % NFN] = g.pf[i];
   for (int i = tid; i < NQF * NFN; i += NT) sFP[(i / NFN) * D::FS + i % NFN] = g.fphi[i];
@@ -351,7 +368,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       cp_async8(TR(m) + r, trace + ((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s);
     }
   };
-  const int gidx = blockIdx.x * R::NG + grp, gstride = gridDim.x * R::NG;
+  const int gidx = blockIdx.x * NG + grp, gstride = gridDim.x * NG;
   {   // first batch: meta, then its data
     const int e00 = gidx * EB;
     if (e00 < g.E) {
@@ -483,6 +500,54 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       }
     }
 
+    if constexpr (R::POINTWISE_TEST) {
+      // ---- 2'. tests on the FP64 pipe, one thread per output entry:
+      // r_w[m][i][s] = sum_(q,kk) G[q][kk][s] B[q][kk][i] + the face rows of
+      // the faces that contain node i; r_trace side contributions per (k, j, s)
+      for (int o = gtid; o < nm * NN * 5; o += GT) {
+        const int m = o / (NN * 5), is = o % (NN * 5), i = is / 5, s = is % 5;
+        const double* gm = G(m) + s;
+        const double* bcol = Bt + i;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          a0 = fma(gm[q * GS], bcol[(q * 4) * bstride], a0);
+          a1 = fma(gm[q * GS + 5], bcol[(q * 4 + 1) * bstride], a1);
+          a0 = fma(gm[q * GS + 10], bcol[(q * 4 + 2) * bstride], a0);
+          a1 = fma(gm[q * GS + 15], bcol[(q * 4 + 3) * bstride], a1);
+        }
+        const double* hm = H(m) + s;
+        double f0 = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < 3; ++c2) {
+          const int kj = sNF[i * 3 + c2];
+          if (kj < 0) break;
+          const int k = kj / NFN, j = kj % NFN;
+          double f1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQF; ++q) f1 = fma(sPF[(k * NQF + q) * D::FS + j], hm[(k * NQF + q) * 5], f1);
+          f0 += f1;
+        }
+        r_w[(size_t)e0 * NN * 5 + o] = (a0 + a1) + f0;
+      }
+      for (int o = gtid; o < nm * 4 * NFN * 5; o += GT) {
+        const int m = o / (4 * NFN * 5), r = o % (4 * NFN * 5);
+        const int k = r / (NFN * 5), j = (r / 5) % NFN, s = r % 5;
+        const double* hk = H(m) + k * NQF * 5 + s;
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQF; ++q) v = fma(sFP[q * D::FS + j], hk[q * 5], v);
+        if (g.has_uinf && BND(m)[k]) {
+          const double* gk = HG(m) + k * NQF * 5 + s;
+          double vg = 0.0;
+#pragma unroll
+          for (int q = 0; q < NQF; ++q) vg = fma(sFP[q * D::FS + j], gk[q * 5], vg);
+          v += vg;
+        }
+        atomicAdd(&r_tr[((size_t)FID(m)[k] * NFN + TID(m)[k * NFN + j]) * 5 + s], v);
+      }
+      RES_T(5);
+    } else {
     // ---- 2. contraction on the FP64 tensor cores, all WPM warps of a macro
     // alike: warp r takes the volume-test K range q in [r NQ/WPM, (r+1)
     // NQ/WPM) and the face tests of faces k = r, r + WPM, ...
@@ -589,6 +654,7 @@ k_residual(Geo g, const double* __restrict__ w, const double* __restrict__ trace
       r_w[(size_t)e0 * NN * 5 + o] = r;
     }
     RES_T(7);
+    }   // DMMA tests
     cur ^= 1;
   }
 }

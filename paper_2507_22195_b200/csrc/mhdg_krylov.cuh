@@ -38,7 +38,7 @@ struct LevelState {
   double norm_b, beta, rel, prev_rel, tol, rr;
   int total, max_iters, restart, m, j, k, go, cyc, converged, updated;
   int inner_sum;  // outer level: inner iterations accumulated over the solve
-  int pad;
+  int gtest;      // the last column ended the cycle on the Arnoldi residual test
 };
 
 struct Level {  // device pointers of one level (passed by value to kernels)
@@ -96,6 +96,7 @@ __global__ void k_kr_reset(Level L, int outer) {
   s->cyc = 0;
   s->k = 0;
   s->j = 0;
+  s->gtest = 0;
   if (outer) s->inner_sum = 0;
 }
 
@@ -146,6 +147,7 @@ __global__ void k_kr_givens(Level L, cudaGraphConditionalHandle h_cyc) {
   }
   const double denom = hypot_cr(h[j], h[j + 1]);
   int cyc = 1;
+  s->gtest = 0;
   if (denom == 0.0) {
     cyc = 0;  // Krylov space exhausted without progress on this column
   } else {
@@ -157,7 +159,9 @@ __global__ void k_kr_givens(Level L, cudaGraphConditionalHandle h_cyc) {
     L.g[j] = mul(L.g[j], L.cs[j]);
     s->total += 1;
     s->k = j + 1;
-    if (fabs(L.g[j + 1]) / s->norm_b <= s->tol || hnorm <= 1e-300) cyc = 0;
+    const int gt = fabs(L.g[j + 1]) / s->norm_b <= s->tol;
+    s->gtest = gt;
+    if (gt || hnorm <= 1e-300) cyc = 0;
     else if (j + 1 >= s->m) cyc = 0;
     else s->j = j + 1;
   }
@@ -178,6 +182,27 @@ __global__ void k_kr_trisolve(Level L) {
     for (int i = 0; i < c; ++i) L.y[i] = sub(L.y[i], mul(L.H[(int64_t)c * ld + i], yc));
   }
   s->updated = 1;
+}
+
+// End of an inner sweep's cycle without the true-residual matvec
+// (mhdg_krylov_params.inner_true_residual = 0).  solver.py:62-72 after the
+// cycle: r = b - A x, then return x when rel <= tol or total >= max_iters.
+// On the iteration cap x is returned whatever r is, so the matvec is dead
+// work (exact); when the cycle ended on |g_k| / |b| <= tol, that Arnoldi
+// estimate is the residual norm of x in exact arithmetic and stands in for
+// it.  Breakdown exits (hnorm tiny, zero rotation) keep the true residual.
+__global__ void k_kr_cycle_end(Level L, cudaGraphConditionalHandle h_true, cudaGraphConditionalHandle h_go) {
+  LevelState* s = L.st;
+  const bool skip = s->k > 0 && (s->gtest || s->total >= s->max_iters);
+  if (skip) {
+    const double rel = fabs(L.g[s->k]) / s->norm_b;
+    s->rel = rel;
+    s->converged = rel <= s->tol;
+    s->go = 0;
+    s->cyc = 0;
+    cudaGraphSetConditional(h_go, 0u);
+  }
+  cudaGraphSetConditional(h_true, skip ? 0u : 1u);
 }
 
 // inner sweep finished: count its iterations into the outer level and arm
@@ -449,10 +474,30 @@ static cudaGraphNode_t kr_level(mhdg_kr::Builder& B, cudaGraph_t g, cudaGraphNod
   cudaGraph_t body_cyc = nullptr;
   cudaGraphNode_t d2 = B.cond(body_go, d1, h_cyc, cudaGraphCondTypeWhile, &body_cyc);
   kr_column(B, body_cyc, lv, h_cyc);
-  B.seg(body_go, d2, [&](cudaStream_t s) -> int {
-    k_kr_trisolve<<<1, 1, 0, s>>>(L);
-    k_kr_combine<<<gr, 256, 0, s>>>(n, L.Z, L.y, L.st, L.x);
-    CK(cudaGetLastError());
+  // update x, then the true residual and the restart decision; the inner
+  // sweep skips the latter when its cycle ended on the cap or the Arnoldi test
+  cudaGraph_t tail = body_go;
+  cudaGraphNode_t d3 = d2;
+  if (lv == 1 && !K->prm.inner_true_residual) {
+    cudaGraphConditionalHandle h_true = B.handle(body_go);
+    d3 = B.seg(body_go, d2, [&](cudaStream_t s) -> int {
+      k_kr_trisolve<<<1, 1, 0, s>>>(L);
+      k_kr_combine<<<gr, 256, 0, s>>>(n, L.Z, L.y, L.st, L.x);
+      k_kr_cycle_end<<<1, 1, 0, s>>>(L, h_true, h_go);
+      CK(cudaGetLastError());
+      return 0;
+    });
+    B.cond(body_go, d3, h_true, cudaGraphCondTypeIf, &tail);
+    if (B.err) return nullptr;
+    d3 = nullptr;
+  }
+  const bool update_here = tail == body_go;
+  B.seg(tail, d3, [&](cudaStream_t s) -> int {
+    if (update_here) {
+      k_kr_trisolve<<<1, 1, 0, s>>>(L);
+      k_kr_combine<<<gr, 256, 0, s>>>(n, L.Z, L.y, L.st, L.x);
+      CK(cudaGetLastError());
+    }
     int rc = mhdg_matvec(c, &K->lin, L.x, L.tmp, (void*)s);
     if (rc) return rc;
     rc = mhdg_axpby(c, n, 1.0, L.b, -1.0, L.tmp, L.r, (void*)s);

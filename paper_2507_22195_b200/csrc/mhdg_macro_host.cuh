@@ -29,6 +29,11 @@ static mhdg_ctx* mm_create(const mhdg_tables* t, int device, int* err) {
   c->d_scratch = nullptr;
   c->scratch_bytes = 0;
   cudaDeviceGetAttribute(&c->n_sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    c->smem_optin = optin > 0 ? (size_t)optin : 48 * 1024;
+  }
   memset(&c->geo, 0, sizeof(c->geo));
   memset(&c->vg, 0, sizeof(c->vg));
   const size_t E = t->n_macros, F = t->n_faces;

@@ -27,6 +27,8 @@ Cases
                    10 steps
   cons_k2_lf       conservative formulation, LF flux (format coverage)
   fs_k2_es         free-stream boundary on a non-periodic box (ghost flux)
+  fs_k1_es, fs_k1_kepes, fs_k3_kepes
+                   the same at k = 1 and k = 3 (--only-freestream)
   cfg3_*           config 3 (Taylor-Green KEPES k=3): operator at n=4, first
                    accepted step at n=2 through the dt-halving path
   cfg2_step_n8     config 2 at n=8: one DIRK step
@@ -335,7 +337,28 @@ def main_macro():
          integrals=np.array([[disc.integrals(f)[k] for k in keys] for f in (f0, f1)]))
 
 
+def main_freestream():
+    """Free-stream boundary at the other degrees (the far-field flux rows of
+    the residual take their own code path per degree on the device)."""
+    box3 = np.array([[0.0, 1.0]] * 3)
+    uinf = GAS.conservative(1.0, np.array([0.3, -0.2, 0.1]), 0.7)
+    for p, flux, seed in ((1, "es", 188), (1, "kepes", 190), (3, "kepes", 192)):
+        mesh = build_box_macro_mesh(box3, 2, 1, periodic=(True, False, False))
+        disc = Discretization(mesh, p=p, gas=GAS, formulation="entropy",
+                              flux=DissipationSpec(flux), boundary=FreeStream(uinf))
+        fields = perturbed_uniform(disc, seed)
+        x = np.random.default_rng(seed + 1).standard_normal(fields.trace.shape)
+        offset = -30.0 * disc.volume_quad_states(fields)
+        out = operator_case(disc, fields, 30.0, offset, 1.0, x)
+        sens = sensitivity(disc, fields, 30.0, offset, 1.0, x, out)
+        save(f"fs_k{p}_{flux}", w=fields.w, trace=fields.trace, offset=offset, alpha=30.0,
+             ptc=1.0, x=x, uinf=uinf, **out, **sens,
+             **meta(disc, flux, "entropy", box3, 2, 1, p, (True, False, False)))
+
+
 def main():
+    if "--only-freestream" in sys.argv:
+        return main_freestream()
     if "--only-macro" in sys.argv:
         return main_macro()
     if "--only-hsweep" in sys.argv:

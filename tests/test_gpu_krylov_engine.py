@@ -60,6 +60,27 @@ def test_engine_matches_host_loop(cuda_ok, kw):
     assert _rel(x_d, x_h) <= 1e-11, (kw, _rel(x_d, x_h))
 
 
+@pytest.mark.parametrize("kw", [dict(), dict(restart=5, max_outer=12, inner_iters=4, rel_tol=1e-8)])
+def test_inner_residual_modes_agree(cuda_ok, kw):
+    """inner_residual="arnoldi" (default: no true-residual matvec at the end of
+    an inner sweep that ended on the cap or the Arnoldi test) against "true"
+    (solver.py:62-72 literally): same iterates, engine and host loop."""
+    import torch
+
+    from paper_2507_22195_b200 import solver
+
+    case, disc = _disc()
+    lin, res = _system(disc, case, dt=0.25)
+    x_t, s_t = solver.solve_condensed(lin, res, inner_residual="true", **kw)
+    x_a, s_a = solver.solve_condensed(lin, res, inner_residual="arnoldi", **kw)
+    assert (s_a.outer_iterations, s_a.inner_iterations, s_a.converged) == \
+        (s_t.outer_iterations, s_t.inner_iterations, s_t.converged)
+    assert torch.equal(x_a, x_t)
+    x_h, s_h = solver.solve_condensed_host(lin, res, inner_residual="true", **kw)
+    assert (s_h.outer_iterations, s_h.inner_iterations) == (s_t.outer_iterations, s_t.inner_iterations)
+    assert _rel(x_t, x_h) <= 1e-11
+
+
 def test_engine_matches_oracle_solve(cuda_ok):
     """Against the oracle's FGMRES(restart 60) + inner GMRES(20) + face-block
     solve on the oracle's own linearization of the same state."""

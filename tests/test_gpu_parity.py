@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 CASES = ["sweep_k1_es", "sweep_k1_kepes", "sweep_k2_es", "sweep_k2_kepes", "sweep_k2_ec",
          "sweep_k3_es", "sweep_k3_kepes", "sweep_k3_ec", "sweep_k4_es", "sweep_k4_kepes",
-         "cons_k2_lf", "fs_k2_es", "cfg1_ops"]
+         "cons_k2_lf", "fs_k2_es", "fs_k1_es", "fs_k1_kepes", "fs_k3_kepes", "cfg1_ops"]
 
 
 def make_disc(z):

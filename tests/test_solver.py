@@ -93,3 +93,33 @@ def test_max_iters_caps_the_solve():
     res = _solve(A, b, rel_tol=1e-14, restart=5, max_iters=12, raise_on_stagnation=False)
     _, it_ref, _, conv_ref = _oracle(A, b, rel_tol=1e-14, restart=5, max_iters=12)
     assert res.iterations == it_ref <= 12 and res.converged == conv_ref
+
+
+@pytest.mark.parametrize("tol,cap", [(0.1, 20), (1e-3, 4), (1e-8, 6)])
+def test_arnoldi_exit_of_the_inner_sweep(tol, cap):
+    """final_residual="arnoldi" (the inner sweep): same x and iteration count
+    as the literal loop when the cycle ends on the residual test or on the
+    iteration cap, with one matvec less (solver.py:62-72)."""
+    A, b = _random_system(60, 21)
+    At = torch.from_numpy(A)
+    counts = {}
+
+    def run(mode):
+        n = [0]
+
+        def op(v):
+            n[0] += 1
+            return At @ v
+
+        res = solver.fgmres(op, torch.from_numpy(b), vec=CPUVectors(), rel_tol=tol, restart=cap,
+                            max_iters=cap, raise_on_stagnation=False, final_residual=mode)
+        counts[mode] = n[0]
+        return res
+
+    lit, fast = run("true"), run("arnoldi")
+    x_ref, it_ref, _, _ = _oracle(A, b, rel_tol=tol, restart=cap, max_iters=cap)
+    assert lit.iterations == fast.iterations == it_ref
+    assert torch.equal(lit.x, fast.x)
+    assert np.abs(fast.x.numpy() - x_ref).max() <= 1e-12 * np.abs(x_ref).max()
+    assert counts["arnoldi"] == counts["true"] - 1
+    assert abs(fast.rel_residual - lit.rel_residual) <= 1e-10 * lit.rel_residual
