@@ -1012,7 +1012,7 @@ static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, cons
   using V = VFast<P>;
   if (e1 < 0) e1 = c->E;
   if (e1 <= e0) return MHDG_OK;
-  const size_t ism = sizeof(typename V::In) * V::MBI, osm = sizeof(typename V::Out) * V::MBO;
+  const size_t ism = V::in_bytes, osm = V::out_bytes;
   if (set_smem(k_visc_in2<P>, ism) || set_smem(k_visc_out2<P>, osm)) return MHDG_CUDA_ERROR;
   const Geo gv = geo_range(c->geo, e0, e1, c->nfn);
   const int E = e1 - e0;
@@ -1024,7 +1024,8 @@ static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, cons
   const double* rqv = rq ? rq + vm * 3 : nullptr;
   const int nbi = (E + V::MBI - 1) / V::MBI, nbo = (E + V::MBO - 1) / V::MBO;
   if (stages & 1) {
-    CK(launch_pdl(k_visc_in2<P>, grid_for(c, nbi, occ(k_visc_in2<P>, 128, ism)), 128, ism, s, gv, c->vg, mode, wlin,
+    CK(launch_pdl(k_visc_in2<P>, grid_for(c, (nbi + V::NG - 1) / V::NG, occ(k_visc_in2<P>, V::CT, ism)), V::CT, ism, s,
+                  gv, c->vg, mode, wlin,
                   (const double*)(L->hhat + ten), x, rwv, rqv, gbuf));
     using LS = LocalSolveCfg<D::NM>;
     CK(launch_pdl(k_local_solve<D::NM, LS::NT>,
@@ -1033,7 +1034,8 @@ static int condensed_visc(mhdg_ctx* c, int mode, const mhdg_lin_buffers* L, cons
     c->launches += 2;
   }
   if ((stages & 2) && mode != 2) {
-    CK(launch_pdl(k_visc_out2<P>, grid_for(c, nbo, occ(k_visc_out2<P>, 128, osm)), 128, osm, s, gv, c->vg, mode,
+    CK(launch_pdl(k_visc_out2<P>, grid_for(c, (nbo + V::NG - 1) / V::NG, occ(k_visc_out2<P>, V::CT, osm)), V::CT, osm,
+                  s, gv, c->vg, mode,
                   wlin, (const double*)(L->hh + ten), (const double*)(L->hw + ten), x, (const double*)zbuf, rqv, y));
     c->launches++;
   }

@@ -18,6 +18,21 @@
 
 namespace mhdg {
 
+// Row stride of the nodal 5-vectors (w, x, z) in shared memory: 16-byte rows,
+// read as two LDS.128 + one LDS.64 instead of five LDS.64.  The point loops
+// issue one such row per FMA group of five and were bound by the shared-
+// memory instruction rate (six loads per five FMAs), not by the FP64 pipe.
+constexpr int VRS = 6;
+MHDG_DEV void vf_ld5(const double* __restrict__ row, double (&v)[5]) {
+  const double2 a = *reinterpret_cast<const double2*>(row);
+  const double2 b = *reinterpret_cast<const double2*>(row + 2);
+  v[0] = a.x;
+  v[1] = a.y;
+  v[2] = b.x;
+  v[3] = b.y;
+  v[4] = row[4];
+}
+
 template <int P>
 struct VFast {
   using D = Dims<P>;
@@ -34,14 +49,36 @@ struct VFast {
   static constexpr int NKP = (NK + 3) / 4 * 4;          // padded to the DMMA k-step
   static constexpr int NTI = (NN + 7) / 8;              // 8-wide node tiles
   static constexpr int WPM = SPI / 32;                  // warps per macro (in-kernel)
+  // CTA = NG independent groups of GT threads (named barriers), one per
+  // former CTA: the groups drift in phase against each other like separate
+  // CTAs, while the point tables are staged ONCE per CTA in shared memory.
+  // Read through L1 they missed a quarter of the time (111 KB of tables at
+  // k = 3 against the streaming w / x / tensor traffic: ncu L1 hit rate 74%,
+  // long-scoreboard stalls 4.1 per issue, issue slots 27% busy).
+  static constexpr int GT = NT, NG = 4, CT = NG * GT;
+  static constexpr int T_PHIT = NN * NPT, T_CXT = 4 * NFN * NPT, T_TST = NKP * NTI * 8;
+  static constexpr int IN_TAB = T_PHIT + T_CXT + T_TST + NQF * NFN;   // + fphi
+  static constexpr int MT = (NPF + 7) / 8, KX = (NFN + 3) / 4, KZ = (NN + 3) / 4;
+  static constexpr int TM = (NFN + 7) / 8, TK = (NQF + 3) / 4;
+  static constexpr int T_CXF = 4 * MT * KX * 32, T_DZF = 3 * MT * KZ * 32, T_FPF = TM * TK * 32,
+                       T_PF = 4 * NQF * NFN, T_FPHI = NQF * NFN;
+  static constexpr int OUT_TAB = T_CXF + T_DZF + T_FPF + T_PF + T_FPHI;
+  static constexpr int META = 8 + 4 * NFN;   // Geo::meta row: face ids (4), trace permutations (4 NFN), flags (4)
+  // w / x / geometry of a macro arrive by cp.async one macro ahead (two
+  // buffers); the face ids / permutations the x gather needs, two ahead
   struct In {
-    double W[NN * 5], X[4 * NFN * 5], RQ[NN * 15], Gk[NKP * 5], part[WPM][NTI * 8 * 8], geo[26];
-    int fid[4], tid[4 * NFN];
+    alignas(16) double W[2][NN * VRS], X[2][4 * NFN * VRS];
+    double RQ[NN * 15], Gk[NKP * 5], part[WPM][NTI * 8 * 8], geo[2][26];
+    int meta[2][META];
   };
   struct Out {
-    double W[NN * 5], Z[NM], X[4 * NFN * 5], RQ[NN * 15], Gf[NPF * 5], YQ[NPF * 15], geo[26];
+    alignas(16) double W[NN * VRS], Z[NN * VRS], X[4 * NFN * VRS];
+    double RQ[NN * 15], Gf[NPF * 5], YQ[NPF * 15], geo[26];
     int fid[4], tid[4 * NFN];
   };
+  static_assert(IN_TAB % 2 == 0 && OUT_TAB % 2 == 0, "16-byte alignment of the per-group structs");
+  static constexpr size_t in_bytes = (size_t)IN_TAB * 8 + sizeof(In) * MBI * NG;
+  static constexpr size_t out_bytes = (size_t)OUT_TAB * 8 + sizeof(Out) * MBO * NG + 4 * NFN * sizeof(int);
 };
 
 template <int P>
@@ -59,16 +96,18 @@ MHDG_DEV void vf_load_geo(const Geo& g, int e, double* geo, int* fid, int* tid, 
 
 // yq contribution of the trace: (area_k n_k,b) sum_jj CX_k[pt][jj] x_k[jj][t]
 template <int P>
-MHDG_DEV void vf_add_x(const ViscGeo& vg, int pt, const double* X, const double* geo, double yq[5][3]) {
+MHDG_DEV void vf_add_x(const double* __restrict__ cxt, int pt, const double* X, const double* geo, double yq[5][3]) {
   constexpr int NFN = Dims<P>::NFN, NPT = VFast<P>::NPT;
 #pragma unroll 1
   for (int k = 0; k < 4; ++k) {
     double u[5] = {0, 0, 0, 0, 0};
 #pragma unroll
     for (int jj = 0; jj < NFN; ++jj) {
-      const double c = __ldg(vg.cxt + (size_t)(k * NFN + jj) * NPT + pt);
+      const double c = cxt[(k * NFN + jj) * NPT + pt];
+      double xr[5];
+      vf_ld5(X + (k * NFN + jj) * VRS, xr);
 #pragma unroll
-      for (int t = 0; t < 5; ++t) u[t] += c * X[(k * NFN + jj) * 5 + t];
+      for (int t = 0; t < 5; ++t) u[t] += c * xr[t];
     }
     const double a = geo[22 + k];
 #pragma unroll
@@ -103,7 +142,7 @@ MHDG_DEV void vf_add_z(const ViscGeo& vg, int pt, const double* Z, const double*
     for (int i = 0; i < NN; ++i) {
       const double c = __ldg(vg.dzt + (size_t)(k2 * NN + i) * NPT + pt);
 #pragma unroll
-      for (int t = 0; t < 5; ++t) u[t] += c * Z[i * 5 + t];
+      for (int t = 0; t < 5; ++t) u[t] += c * Z[i * VRS + t];
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
@@ -119,7 +158,7 @@ MHDG_DEV void vf_add_z(const ViscGeo& vg, int pt, const double* Z, const double*
 //   (mode 0 matvec, 1 condensed rhs, 2 recovery)
 // ---------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(VFast<P>::CT, 1)
 k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const double* __restrict__ hhat,
            const double* __restrict__ x, const double* __restrict__ r_w, const double* __restrict__ r_q,
            double* __restrict__ gout) {
@@ -128,31 +167,74 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
   constexpr int NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF, NM = D::NM, NPT = V::NPT;
   constexpr int MB = V::MBI, SP = V::SPI, NK = V::NK;
   extern __shared__ __align__(16) double smem[];
-  typename V::In* sm = reinterpret_cast<typename V::In*>(smem);
-  const int tid = threadIdx.x, slot = tid / SP, lt = tid % SP;
+  double* sPHIT = smem;                  // (NN, NPT)
+  double* sCXT = sPHIT + V::T_PHIT;      // (4 NFN, NPT)
+  double* sTST = sCXT + V::T_CXT;        // (NKP, NTI * 8)
+  double* sFPHI = sTST + V::T_TST;       // (NQF, NFN)
+  const int grp = threadIdx.x / V::GT, tid = threadIdx.x % V::GT, slot = tid / SP, lt = tid % SP;
+  typename V::In* sm = reinterpret_cast<typename V::In*>(sFPHI + NQF * NFN) + grp * MB;
   const double gam = g.gamma;
   const bool use_x = mode != 1, use_r = mode != 0;
   const int nblk = (g.E + MB - 1) / MB;
+  for (int i = threadIdx.x; i < V::T_PHIT; i += V::CT) sPHIT[i] = vg.phit[i];
+  for (int i = threadIdx.x; i < V::T_CXT; i += V::CT) sCXT[i] = vg.cxt[i];
+  for (int i = threadIdx.x; i < V::T_TST; i += V::CT) sTST[i] = vg.tst[i];
+  for (int i = threadIdx.x; i < NQF * NFN; i += V::CT) sFPHI[i] = g.fphi[i];
   for (int i = NK * 5 + lt; i < V::NKP * 5; i += SP) sm[slot].Gk[i] = 0.0;
-  pdl_wait();   // before: shared-memory padding only (mhdg_kernels.cuh PDL invariant)
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const int e = blk * MB + slot;
-    const bool live = e < g.E;
-    typename V::In& S = sm[slot];
-    __syncthreads();
-    if (live) {
-      vf_load_geo<P>(g, e, S.geo, S.fid, S.tid, lt, SP);
-      for (int i = lt; i < NN * 5; i += SP) S.W[i] = wlin[(size_t)e * NN * 5 + i];
-      if (use_r)
-        for (int i = lt; i < NN * 15; i += SP) S.RQ[i] = r_q[(size_t)e * NN * 15 + i];
-    }
-    __syncthreads();
-    if (live && use_x)
+  __syncthreads();
+  auto gsync = [&]() { group_sync(1 + grp, V::GT); };
+  pdl_wait();   // before: immutable point tables into shared memory, padding (mhdg_kernels.cuh PDL invariant)
+  // Software pipeline per group (the load phase and the barrier behind it
+  // were 38% of the stall samples: two dependent global round trips per
+  // macro with nothing to overlap them but the other three groups):
+  //   top of macro i:  data(i) and meta(i + 1) have landed
+  //                    issue data(i + 1) (its x gather reads meta(i + 1)),
+  //                    issue meta(i + 2), prefetch hhat(i + 1) towards L2
+  //   then compute macro i from buffer i & 1.
+  typename V::In& S = sm[slot];
+  const int bstride = gridDim.x * V::NG;
+  auto issue_meta = [&](int blkn, int buf) {
+    const int en = blkn * MB + slot;
+    if (blkn < nblk && en < g.E)
+      for (int i = lt; i < V::META; i += SP) cp_async4(&S.meta[buf][i], g.meta + (size_t)en * V::META + i);
+  };
+  auto issue_data = [&](int blkn, int buf) {
+    const int en = blkn * MB + slot;
+    if (blkn >= nblk || en >= g.E) return;
+    for (int i = lt; i < NN * 5; i += SP)
+      cp_async8(&S.W[buf][(i / 5) * VRS + i % 5], wlin + (size_t)en * NN * 5 + i);
+    for (int i = lt; i < 26; i += SP) cp_async8(&S.geo[buf][i], g.geo26 + (size_t)en * 50 + i);
+    if (use_x) {
+      const int* mt = S.meta[buf];
       for (int i = lt; i < 4 * NFN * 5; i += SP) {
         const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
-        S.X[i] = x[((size_t)S.fid[k] * NFN + S.tid[k * NFN + j]) * 5 + s2];
+        cp_async8(&S.X[buf][(i / 5) * VRS + s2], x + ((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s2);
       }
-    __syncthreads();
+      // 25 x NQF doubles per face, contiguous per (macro, face)
+      for (int i = lt * 16; i < 4 * 25 * NQF; i += SP * 16) prefetch_l2(hhat + (size_t)en * 4 * 25 * NQF + i);
+    }
+  };
+  int blk = blockIdx.x * V::NG + grp;
+  issue_meta(blk, 0);
+  cp_async_wait_all();
+  gsync();
+  issue_data(blk, 0);
+  issue_meta(blk + bstride, 1);
+  for (int cur = 0; blk < nblk; blk += bstride, cur ^= 1) {
+    const int e = blk * MB + slot;
+    const bool live = e < g.E;
+    cp_async_wait_all();
+    gsync();
+    issue_data(blk + bstride, cur ^ 1);
+    issue_meta(blk + 2 * bstride, cur);
+    if (use_r) {
+      if (live)
+        for (int i = lt; i < NN * 15; i += SP) S.RQ[i] = r_q[(size_t)e * NN * 15 + i];
+      gsync();
+    }
+    const double* sW = S.W[cur];
+    const double* sX = S.X[cur];
+    const double* sGeo = S.geo[cur];
     if (live && lt < NPT) {
       const int pt = lt;
       double wq[5] = {0, 0, 0, 0, 0}, yq[5][3];
@@ -160,13 +242,15 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
       for (int t = 0; t < 5; ++t) yq[t][0] = yq[t][1] = yq[t][2] = 0.0;
 #pragma unroll 4
       for (int i = 0; i < NN; ++i) {
-        const double a = __ldg(vg.phit + (size_t)i * NPT + pt);
+        const double a = sPHIT[i * NPT + pt];
+        double wr[5];
+        vf_ld5(sW + i * VRS, wr);
 #pragma unroll
-        for (int t = 0; t < 5; ++t) wq[t] += a * S.W[i * 5 + t];
+        for (int t = 0; t < 5; ++t) wq[t] += a * wr[t];
       }
-      if (use_x) vf_add_x<P>(vg, pt, S.X, S.geo, yq);
+      if (use_x) vf_add_x<P>(sCXT, pt, sX, sGeo, yq);
       if (use_r) vf_add_rq<P>(vg, pt, S.RQ, yq);
-      const double idet = 1.0 / S.geo[0];
+      const double idet = 1.0 / sGeo[0];
 #pragma unroll
       for (int t = 0; t < 5; ++t)
 #pragma unroll
@@ -175,26 +259,28 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
       to_conservative(wq, g.form, gam, u);
       visc_G(vg, g.form, wq, u, yq, gam, Gv);
       if (pt < NQ) {
-        const double vw = g.qw[pt] * S.geo[0];
+        const double vw = g.qw[pt] * sGeo[0];
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk) {
-          const double j0 = S.geo[1 + kk * 3], j1 = S.geo[2 + kk * 3], j2 = S.geo[3 + kk * 3];
+          const double j0 = sGeo[1 + kk * 3], j1 = sGeo[2 + kk * 3], j2 = sGeo[3 + kk * 3];
 #pragma unroll
           for (int t = 0; t < 5; ++t)
             S.Gk[(pt * 3 + kk) * 5 + t] = -(vw * ((j0 * Gv[t][0] + j1 * Gv[t][1]) + j2 * Gv[t][2]));
         }
       } else {
         const int it = pt - NQ, k = it / NQF, qp = it % NQF;
-        const double fwq = g.fw[qp] * S.geo[22 + k];
-        const double n0 = S.geo[10 + k * 3], n1 = S.geo[11 + k * 3], n2 = S.geo[12 + k * 3];
+        const double fwq = g.fw[qp] * sGeo[22 + k];
+        const double n0 = sGeo[10 + k * 3], n1 = sGeo[11 + k * 3], n2 = sGeo[12 + k * 3];
         double hx[5] = {0, 0, 0, 0, 0};
         if (use_x) {
           double xq[5] = {0, 0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < NFN; ++j) {
-            const double b2 = __ldg(g.fphi + qp * NFN + j);
+            const double b2 = sFPHI[qp * NFN + j];
+            double xr[5];
+            vf_ld5(sX + (k * NFN + j) * VRS, xr);
 #pragma unroll
-            for (int t = 0; t < 5; ++t) xq[t] += b2 * S.X[(k * NFN + j) * 5 + t];
+            for (int t = 0; t < 5; ++t) xq[t] += b2 * xr[t];
           }
           const double* h = hhat + ((size_t)e * 4 + k) * 25 * NQF + qp;   // (E,4,25,NQF)
 #pragma unroll
@@ -210,7 +296,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
           S.Gk[(3 * NQ + it) * 5 + t] = fwq * (((Gv[t][0] * n0 + Gv[t][1] * n1) + Gv[t][2] * n2) - hx[t]);
       }
     }
-    __syncthreads();
+    gsync();
     // tests on the FP64 tensor cores: gout^T (5 x NN) = Gk^T (5 x NK) . TST (NK x NN),
     // K split across the macro's warps, partials summed in warp order
     {
@@ -226,7 +312,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
         const double a = sa < 5 ? S.Gk[K * 5 + sa] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt)
-          dmma_8x8x4(c[nt], a, __ldg(vg.tst + (size_t)K * (NTI * 8) + nt * 8 + (lane >> 2)));
+          dmma_8x8x4(c[nt], a, sTST[K * (NTI * 8) + nt * 8 + (lane >> 2)]);
       }
 #pragma unroll
       for (int nt = 0; nt < NTI; ++nt) {
@@ -234,7 +320,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
         S.part[wl][(nt * 8 + kl * 2 + 1) * 8 + sa] = c[nt][1];
       }
     }
-    __syncthreads();
+    gsync();
     if (live)
       for (int o = lt; o < NM; o += SP) {
         const int i = o / 5, s2 = o % 5;
@@ -250,7 +336,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
 // k_visc_out2: y += hh x[0] + hw z - vhatq(M^-1 (qv z + qvhat(x)[0] + r_q[1]))
 // ---------------------------------------------------------------------------
 template <int P>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(VFast<P>::CT, 1)
 k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const double* __restrict__ hh,
             const double* __restrict__ hw, const double* __restrict__ x, const double* __restrict__ z,
             const double* __restrict__ r_q, double* __restrict__ y) {
@@ -259,40 +345,54 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
   constexpr int NN = D::NN, NQ = D::NQ, NFN = D::NFN, NQF = D::NQF, NM = D::NM;
   constexpr int MB = V::MBO, NPF = V::NPF;
   extern __shared__ __align__(16) double smem[];
-  typename V::Out* sm = reinterpret_cast<typename V::Out*>(smem);
-  const int tid = threadIdx.x;
+  double* sCXF = smem;                   // fragment-ordered CX slices
+  double* sDZF = sCXF + V::T_CXF;        // fragment-ordered DZ slices
+  double* sFPF = sDZF + V::T_DZF;        // fragment-ordered fphi
+  double* sPF = sFPF + V::T_FPF;         // (4 NQF, NFN)
+  double* sFPHI = sPF + V::T_PF;         // (NQF, NFN)
+  const int grp = threadIdx.x / V::GT, tid = threadIdx.x % V::GT;
+  typename V::Out* sm = reinterpret_cast<typename V::Out*>(sFPHI + V::T_FPHI) + grp * MB;
+  int* sRows = reinterpret_cast<int*>(reinterpret_cast<typename V::Out*>(sFPHI + V::T_FPHI) + V::NG * MB);
   const int slot = tid / NPF, lt = tid % NPF;
   const double gam = g.gamma;
   const int nblk = (g.E + MB - 1) / MB;
-  pdl_wait();   // before: index arithmetic only (mhdg_kernels.cuh PDL invariant)
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  for (int i = threadIdx.x; i < V::T_CXF; i += V::CT) sCXF[i] = vg.cxf[i];
+  for (int i = threadIdx.x; i < V::T_DZF; i += V::CT) sDZF[i] = vg.dzf[i];
+  for (int i = threadIdx.x; i < V::T_FPF; i += V::CT) sFPF[i] = vg.fpf[i];
+  for (int i = threadIdx.x; i < V::T_PF; i += V::CT) sPF[i] = g.pf[i];
+  for (int i = threadIdx.x; i < V::T_FPHI; i += V::CT) sFPHI[i] = g.fphi[i];
+  for (int i = threadIdx.x; i < 4 * NFN; i += V::CT) sRows[i] = g.rows[i];
+  __syncthreads();
+  auto gsync = [&]() { group_sync(1 + grp, V::GT); };
+  pdl_wait();   // before: immutable point tables into shared memory (mhdg_kernels.cuh PDL invariant)
+  for (int blk = blockIdx.x * V::NG + grp; blk < nblk; blk += gridDim.x * V::NG) {
     const int e = blk * MB + slot;
     const bool live = slot < MB && e < g.E;
     typename V::Out& S = sm[slot < MB ? slot : 0];
-    __syncthreads();
+    gsync();
     if (live) {
       vf_load_geo<P>(g, e, S.geo, S.fid, S.tid, lt, NPF);
-      for (int i = lt; i < NN * 5; i += NPF) S.W[i] = wlin[(size_t)e * NN * 5 + i];
-      for (int i = lt; i < NM; i += NPF) S.Z[i] = z[(size_t)e * NM + i];
+      for (int i = lt; i < NN * 5; i += NPF) S.W[(i / 5) * VRS + i % 5] = wlin[(size_t)e * NN * 5 + i];
+      for (int i = lt; i < NM; i += NPF) S.Z[(i / 5) * VRS + i % 5] = z[(size_t)e * NM + i];
       if (mode == 1)
         for (int i = lt; i < NN * 15; i += NPF) S.RQ[i] = r_q[(size_t)e * NN * 15 + i];
+      if (mode == 0)
+        for (int i = lt; i < 4 * NFN * 5; i += NPF) {
+          const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
+          const int f = g.fid[e * 4 + k], tj = g.tidx[(size_t)e * 4 * NFN + k * NFN + j];
+          S.X[(i / 5) * VRS + s2] = x[((size_t)f * NFN + tj) * 5 + s2];
+        }
     }
-    __syncthreads();
-    if (live && mode == 0)
-      for (int i = lt; i < 4 * NFN * 5; i += NPF) {
-        const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
-        S.X[i] = x[((size_t)S.fid[k] * NFN + S.tid[k * NFN + j]) * 5 + s2];
-      }
-    __syncthreads();
+    gsync();
     if (mode == 0) {
       // gradient unknowns at the face points on the FP64 tensor cores, per
       // (macro slot, 8-point tile):
       //   yq = (1/det) sum_k (area n)_k (CX_k x_k) + sum_k2 Jinv[k2] (DZ_k2 z)
       // (the point-per-thread contraction spent one shared-memory load per
       // FMA on the broadcast x / z values)
-      constexpr int MT = (NPF + 7) / 8, KX = (NFN + 3) / 4, KZ = (NN + 3) / 4;
+      constexpr int MT = V::MT, KX = V::KX, KZ = V::KZ;
       const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, nn = lane >> 2;
-      for (int job = warp; job < MB * MT; job += V::NT / 32) {
+      for (int job = warp; job < MB * MT; job += V::GT / 32) {
         const int sl = job / MT, mt = job % MT;
         if (blk * MB + sl >= g.E) continue;
         typename V::Out& Sx = sm[sl];
@@ -303,8 +403,8 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
 #pragma unroll
           for (int ks = 0; ks < KX; ++ks) {
             const int jj = ks * 4 + kq;
-            const double b = (jj < NFN && nn < 5) ? Sx.X[(k * NFN + jj) * 5 + nn] : 0.0;
-            dmma_8x8x4(c, __ldg(vg.cxf + ((k * MT + mt) * KX + ks) * 32 + lane), b);
+            const double b = (jj < NFN && nn < 5) ? Sx.X[(k * NFN + jj) * VRS + nn] : 0.0;
+            dmma_8x8x4(c, sCXF[((k * MT + mt) * KX + ks) * 32 + lane], b);
           }
           const double a = Sx.geo[22 + k];
 #pragma unroll
@@ -325,8 +425,8 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
 #pragma unroll
           for (int ks = 0; ks < KZ; ++ks) {
             const int i = ks * 4 + kq;
-            const double b = (i < NN && nn < 5) ? Sx.Z[i * 5 + nn] : 0.0;
-            dmma_8x8x4(c, __ldg(vg.dzf + ((k2 * MT + mt) * KZ + ks) * 32 + lane), b);
+            const double b = (i < NN && nn < 5) ? Sx.Z[i * VRS + nn] : 0.0;
+            dmma_8x8x4(c, sDZF[((k2 * MT + mt) * KZ + ks) * 32 + lane], b);
           }
 #pragma unroll
           for (int b = 0; b < 3; ++b) {
@@ -344,7 +444,7 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
             for (int b = 0; b < 3; ++b) Sx.YQ[pt2 * 15 + t * 3 + b] = acc[h2][b];
         }
       }
-      __syncthreads();
+      gsync();
     }
     if (live) {
       const int it = lt, k = it / NQF, qp = it % NQF, pt = NQ + it;
@@ -353,17 +453,22 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
       for (int t = 0; t < 5; ++t) yq[t][0] = yq[t][1] = yq[t][2] = 0.0;
 #pragma unroll
       for (int j = 0; j < NFN; ++j) {
-        const double a = __ldg(g.pf + (size_t)it * NFN + j);
-        const int row = __ldg(g.rows + k * NFN + j);
+        const double a = sPF[it * NFN + j];
+        const int row = sRows[k * NFN + j];
+        double wr[5], zr[5];
+        vf_ld5(S.W + row * VRS, wr);
+        vf_ld5(S.Z + row * VRS, zr);
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
-          wq[t] += a * S.W[row * 5 + t];
-          zq[t] += a * S.Z[row * 5 + t];
+          wq[t] += a * wr[t];
+          zq[t] += a * zr[t];
         }
         if (mode == 0) {
-          const double b2 = __ldg(g.fphi + qp * NFN + j);
+          const double b2 = sFPHI[qp * NFN + j];
+          double xr[5];
+          vf_ld5(S.X + (k * NFN + j) * VRS, xr);
 #pragma unroll
-          for (int t = 0; t < 5; ++t) xq[t] += b2 * S.X[(k * NFN + j) * 5 + t];
+          for (int t = 0; t < 5; ++t) xq[t] += b2 * xr[t];
         }
       }
       if (mode == 0) {
@@ -398,13 +503,13 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
         S.Gf[it * 5 + s2] = fwq * b2 + (fwq * a - fwq * gn);
       }
     }
-    __syncthreads();
+    gsync();
     // trace tests on DMMA, per (macro slot, face): C[j][s] = sum_qp fphi[qp][j] Gf[qp][s]
-    // (A fragments of fphi from the fragment-ordered table vg.fpf)
+    // (A fragments of fphi from the fragment-ordered table fpf, staged in shared memory)
     {
-      constexpr int TM = (NFN + 7) / 8, TK = (NQF + 3) / 4;
+      constexpr int TM = V::TM, TK = V::TK;
       const int warp = tid >> 5, lane = tid & 31, kq = lane & 3, nn = lane >> 2;
-      for (int job = warp; job < MB * 4; job += V::NT / 32) {
+      for (int job = warp; job < MB * 4; job += V::GT / 32) {
         const int sl = job / 4, k = job % 4;
         if (blk * MB + sl >= g.E) continue;
         const typename V::Out& Sx = sm[sl];
@@ -416,7 +521,7 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
           const int qp = ks * 4 + kq;
           const double b = (qp < NQF && nn < 5) ? Sx.Gf[(k * NQF + qp) * 5 + nn] : 0.0;
 #pragma unroll
-          for (int t = 0; t < TM; ++t) dmma_8x8x4(c[t], __ldg(vg.fpf + (t * TK + ks) * 32 + lane), b);
+          for (int t = 0; t < TM; ++t) dmma_8x8x4(c[t], sFPF[(t * TK + ks) * 32 + lane], b);
         }
 #pragma unroll
         for (int t = 0; t < TM; ++t)
