@@ -71,28 +71,18 @@ struct VFast {
     double RQ[NN * 15], Gk[NKP * 5], part[WPM][NTI * 8 * 8], geo[2][26];
     int meta[2][META];
   };
+  // out-kernel: the same pipeline; the face ids live in a ring of three (the
+  // trace scatter at the end of macro i still reads meta(i) while meta(i + 2)
+  // arrives); r_q (condensed rhs only) shares YQ (matvec only)
   struct Out {
-    alignas(16) double W[NN * VRS], Z[NN * VRS], X[4 * NFN * VRS];
-    double RQ[NN * 15], Gf[NPF * 5], YQ[NPF * 15], geo[26];
-    int fid[4], tid[4 * NFN];
+    alignas(16) double W[2][NN * VRS], Z[2][NN * VRS], X[2][4 * NFN * VRS];
+    double Gf[NPF * 5], YQ[NPF * 15 > NN * 15 ? NPF * 15 : NN * 15], geo[2][26];
+    int meta[3][META];
   };
   static_assert(IN_TAB % 2 == 0 && OUT_TAB % 2 == 0, "16-byte alignment of the per-group structs");
   static constexpr size_t in_bytes = (size_t)IN_TAB * 8 + sizeof(In) * MBI * NG;
   static constexpr size_t out_bytes = (size_t)OUT_TAB * 8 + sizeof(Out) * MBO * NG + 4 * NFN * sizeof(int);
 };
-
-template <int P>
-MHDG_DEV void vf_load_geo(const Geo& g, int e, double* geo, int* fid, int* tid, int lt, int nt) {
-  constexpr int NFN = Dims<P>::NFN;
-  for (int i = lt; i < 26 + 4 + 4 * NFN; i += nt) {
-    if (i == 0) geo[0] = g.det[e];
-    else if (i < 10) geo[i] = g.invj[(size_t)e * 9 + i - 1];
-    else if (i < 22) geo[i] = g.nrm[(size_t)e * 12 + i - 10];
-    else if (i < 26) geo[i] = g.area[(size_t)e * 4 + i - 22];
-    else if (i < 30) fid[i - 26] = g.fid[e * 4 + i - 26];
-    else tid[i - 30] = g.tidx[(size_t)e * 4 * NFN + i - 30];
-  }
-}
 
 // yq contribution of the trace: (area_k n_k,b) sum_jj CX_k[pt][jj] x_k[jj][t]
 template <int P>
@@ -365,25 +355,53 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
   __syncthreads();
   auto gsync = [&]() { group_sync(1 + grp, V::GT); };
   pdl_wait();   // before: immutable point tables into shared memory (mhdg_kernels.cuh PDL invariant)
-  for (int blk = blockIdx.x * V::NG + grp; blk < nblk; blk += gridDim.x * V::NG) {
+  // software pipeline as in k_visc_in2: data(i + 1) and meta(i + 2) are in
+  // flight while macro i is computed; hw / hh of macro i + 1 go towards L2
+  typename V::Out& S = sm[slot < MB ? slot : 0];
+  const int bstride = gridDim.x * V::NG;
+  auto issue_meta = [&](int blkn, int ms) {
+    const int en = blkn * MB + slot;
+    if (slot < MB && blkn < nblk && en < g.E)
+      for (int i = lt; i < V::META; i += NPF) cp_async4(&S.meta[ms][i], g.meta + (size_t)en * V::META + i);
+  };
+  auto issue_data = [&](int blkn, int buf, int ms) {
+    const int en = blkn * MB + slot;
+    if (slot >= MB || blkn >= nblk || en >= g.E) return;
+    for (int i = lt; i < NN * 5; i += NPF) {
+      cp_async8(&S.W[buf][(i / 5) * VRS + i % 5], wlin + (size_t)en * NN * 5 + i);
+      cp_async8(&S.Z[buf][(i / 5) * VRS + i % 5], z + (size_t)en * NM + i);
+    }
+    for (int i = lt; i < 26; i += NPF) cp_async8(&S.geo[buf][i], g.geo26 + (size_t)en * 50 + i);
+    if (mode == 0) {
+      const int* mt = S.meta[ms];
+      for (int i = lt; i < 4 * NFN * 5; i += NPF) {
+        const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
+        cp_async8(&S.X[buf][(i / 5) * VRS + s2], x + ((size_t)mt[k] * NFN + mt[4 + k * NFN + j]) * 5 + s2);
+      }
+    }
+    for (int i = lt * 16; i < 4 * 25 * NQF; i += NPF * 16) {
+      prefetch_l2(hw + (size_t)en * 4 * 25 * NQF + i);
+      if (mode == 0) prefetch_l2(hh + (size_t)en * 4 * 25 * NQF + i);
+    }
+  };
+  int blk = blockIdx.x * V::NG + grp;
+  issue_meta(blk, 0);
+  cp_async_wait_all();
+  gsync();
+  issue_data(blk, 0, 0);
+  issue_meta(blk + bstride, 1);
+  for (int cur = 0, mc = 0; blk < nblk; blk += bstride, cur ^= 1, mc = (mc + 1) % 3) {
     const int e = blk * MB + slot;
     const bool live = slot < MB && e < g.E;
-    typename V::Out& S = sm[slot < MB ? slot : 0];
+    cp_async_wait_all();
     gsync();
-    if (live) {
-      vf_load_geo<P>(g, e, S.geo, S.fid, S.tid, lt, NPF);
-      for (int i = lt; i < NN * 5; i += NPF) S.W[(i / 5) * VRS + i % 5] = wlin[(size_t)e * NN * 5 + i];
-      for (int i = lt; i < NM; i += NPF) S.Z[(i / 5) * VRS + i % 5] = z[(size_t)e * NM + i];
-      if (mode == 1)
-        for (int i = lt; i < NN * 15; i += NPF) S.RQ[i] = r_q[(size_t)e * NN * 15 + i];
-      if (mode == 0)
-        for (int i = lt; i < 4 * NFN * 5; i += NPF) {
-          const int k = i / (NFN * 5), j = (i / 5) % NFN, s2 = i % 5;
-          const int f = g.fid[e * 4 + k], tj = g.tidx[(size_t)e * 4 * NFN + k * NFN + j];
-          S.X[(i / 5) * VRS + s2] = x[((size_t)f * NFN + tj) * 5 + s2];
-        }
+    issue_data(blk + bstride, cur ^ 1, (mc + 1) % 3);
+    issue_meta(blk + 2 * bstride, (mc + 2) % 3);
+    if (mode == 1) {
+      if (live)
+        for (int i = lt; i < NN * 15; i += NPF) S.YQ[i] = r_q[(size_t)e * NN * 15 + i];
+      gsync();
     }
-    gsync();
     if (mode == 0) {
       // gradient unknowns at the face points on the FP64 tensor cores, per
       // (macro slot, 8-point tile):
@@ -403,18 +421,18 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
 #pragma unroll
           for (int ks = 0; ks < KX; ++ks) {
             const int jj = ks * 4 + kq;
-            const double b = (jj < NFN && nn < 5) ? Sx.X[(k * NFN + jj) * VRS + nn] : 0.0;
+            const double b = (jj < NFN && nn < 5) ? Sx.X[cur][(k * NFN + jj) * VRS + nn] : 0.0;
             dmma_8x8x4(c, sCXF[((k * MT + mt) * KX + ks) * 32 + lane], b);
           }
-          const double a = Sx.geo[22 + k];
+          const double a = Sx.geo[cur][22 + k];
 #pragma unroll
           for (int b = 0; b < 3; ++b) {
-            const double an = a * Sx.geo[10 + k * 3 + b];
+            const double an = a * Sx.geo[cur][10 + k * 3 + b];
             acc[0][b] += an * c[0];
             acc[1][b] += an * c[1];
           }
         }
-        const double idet = 1.0 / Sx.geo[0];
+        const double idet = 1.0 / Sx.geo[cur][0];
 #pragma unroll
         for (int h2 = 0; h2 < 2; ++h2)
 #pragma unroll
@@ -425,12 +443,12 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
 #pragma unroll
           for (int ks = 0; ks < KZ; ++ks) {
             const int i = ks * 4 + kq;
-            const double b = (i < NN && nn < 5) ? Sx.Z[i * VRS + nn] : 0.0;
+            const double b = (i < NN && nn < 5) ? Sx.Z[cur][i * VRS + nn] : 0.0;
             dmma_8x8x4(c, sDZF[((k2 * MT + mt) * KZ + ks) * 32 + lane], b);
           }
 #pragma unroll
           for (int b = 0; b < 3; ++b) {
-            const double jb = Sx.geo[1 + k2 * 3 + b];
+            const double jb = Sx.geo[cur][1 + k2 * 3 + b];
             acc[0][b] += jb * c[0];
             acc[1][b] += jb * c[1];
           }
@@ -456,8 +474,8 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
         const double a = sPF[it * NFN + j];
         const int row = sRows[k * NFN + j];
         double wr[5], zr[5];
-        vf_ld5(S.W + row * VRS, wr);
-        vf_ld5(S.Z + row * VRS, zr);
+        vf_ld5(S.W[cur] + row * VRS, wr);
+        vf_ld5(S.Z[cur] + row * VRS, zr);
 #pragma unroll
         for (int t = 0; t < 5; ++t) {
           wq[t] += a * wr[t];
@@ -466,7 +484,7 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
         if (mode == 0) {
           const double b2 = sFPHI[qp * NFN + j];
           double xr[5];
-          vf_ld5(S.X + (k * NFN + j) * VRS, xr);
+          vf_ld5(S.X[cur] + (k * NFN + j) * VRS, xr);
 #pragma unroll
           for (int t = 0; t < 5; ++t) xq[t] += b2 * xr[t];
         }
@@ -477,19 +495,19 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
 #pragma unroll
           for (int b = 0; b < 3; ++b) yq[t][b] = S.YQ[it * 15 + t * 3 + b];
       } else {
-        if (mode == 1) vf_add_rq<P>(vg, pt, S.RQ, yq);
-        const double idet = 1.0 / S.geo[0];
+        if (mode == 1) vf_add_rq<P>(vg, pt, S.YQ, yq);
+        const double idet = 1.0 / S.geo[cur][0];
 #pragma unroll
         for (int t = 0; t < 5; ++t)
 #pragma unroll
           for (int b = 0; b < 3; ++b) yq[t][b] *= idet;
-        vf_add_z<P>(vg, pt, S.Z, S.geo, yq);
+        vf_add_z<P>(vg, pt, S.Z[cur], S.geo[cur], yq);
       }
       double u[5], Gv[5][3];
       to_conservative(wq, g.form, gam, u);
       visc_G(vg, g.form, wq, u, yq, gam, Gv);
-      const double fwq = g.fw[qp] * S.geo[22 + k];
-      const double n0 = S.geo[10 + k * 3], n1 = S.geo[11 + k * 3], n2 = S.geo[12 + k * 3];
+      const double fwq = g.fw[qp] * S.geo[cur][22 + k];
+      const double n0 = S.geo[cur][10 + k * 3], n1 = S.geo[cur][11 + k * 3], n2 = S.geo[cur][12 + k * 3];
       const size_t base = ((size_t)e * 4 + k) * 25 * NQF + qp;   // (E,4,25,NQF)
 #pragma unroll
       for (int s2 = 0; s2 < 5; ++s2) {
@@ -529,7 +547,7 @@ k_visc_out2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const 
           for (int h2 = 0; h2 < 2; ++h2) {
             const int j = t * 8 + nn, s2 = kq * 2 + h2;
             if (j < NFN && s2 < 5)
-              atomicAdd(&y[((size_t)Sx.fid[k] * NFN + Sx.tid[k * NFN + j]) * 5 + s2], c[t][h2]);
+              atomicAdd(&y[((size_t)Sx.meta[mc][k] * NFN + Sx.meta[mc][4 + k * NFN + j]) * 5 + s2], c[t][h2]);
           }
       }
     }
