@@ -56,7 +56,11 @@ struct VFast {
   // k = 3 against the streaming w / x / tensor traffic: ncu L1 hit rate 74%,
   // long-scoreboard stalls 4.1 per issue, issue slots 27% busy).
   static constexpr int GT = NT, NG = 4, CT = NG * GT;
-  static constexpr int T_PHIT = NN * NPT, T_CXT = 4 * NFN * NPT, T_TST = NKP * NTI * 8;
+  // test-table row stride in shared memory: >= NN and = 4 (mod 16), so the
+  // B-fragment reads (lane = 4 n + kk -> word kk * TS + n) hit 32 distinct
+  // banks (the global table's stride NTI * 8 = 24 gave two-way conflicts)
+  static constexpr int TS = NN + ((4 - NN) % 16 + 16) % 16;
+  static constexpr int T_PHIT = NN * NPT, T_CXT = 4 * NFN * NPT, T_TST = NKP * TS;
   static constexpr int IN_TAB = T_PHIT + T_CXT + T_TST + NQF * NFN;   // + fphi
   static constexpr int MT = (NPF + 7) / 8, KX = (NFN + 3) / 4, KZ = (NN + 3) / 4;
   static constexpr int TM = (NFN + 7) / 8, TK = (NQF + 3) / 4;
@@ -159,7 +163,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
   extern __shared__ __align__(16) double smem[];
   double* sPHIT = smem;                  // (NN, NPT)
   double* sCXT = sPHIT + V::T_PHIT;      // (4 NFN, NPT)
-  double* sTST = sCXT + V::T_CXT;        // (NKP, NTI * 8)
+  double* sTST = sCXT + V::T_CXT;        // (NKP, TS)
   double* sFPHI = sTST + V::T_TST;       // (NQF, NFN)
   const int grp = threadIdx.x / V::GT, tid = threadIdx.x % V::GT, slot = tid / SP, lt = tid % SP;
   typename V::In* sm = reinterpret_cast<typename V::In*>(sFPHI + NQF * NFN) + grp * MB;
@@ -168,7 +172,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
   const int nblk = (g.E + MB - 1) / MB;
   for (int i = threadIdx.x; i < V::T_PHIT; i += V::CT) sPHIT[i] = vg.phit[i];
   for (int i = threadIdx.x; i < V::T_CXT; i += V::CT) sCXT[i] = vg.cxt[i];
-  for (int i = threadIdx.x; i < V::T_TST; i += V::CT) sTST[i] = vg.tst[i];
+  for (int i = threadIdx.x; i < V::NKP * NN; i += V::CT) sTST[(i / NN) * V::TS + i % NN] = vg.tst[(i / NN) * (V::NTI * 8) + i % NN];
   for (int i = threadIdx.x; i < NQF * NFN; i += V::CT) sFPHI[i] = g.fphi[i];
   for (int i = NK * 5 + lt; i < V::NKP * 5; i += SP) sm[slot].Gk[i] = 0.0;
   __syncthreads();
@@ -302,7 +306,7 @@ k_visc_in2(Geo g, ViscGeo vg, int mode, const double* __restrict__ wlin, const d
         const double a = sa < 5 ? S.Gk[K * 5 + sa] : 0.0;
 #pragma unroll
         for (int nt = 0; nt < NTI; ++nt)
-          dmma_8x8x4(c[nt], a, sTST[K * (NTI * 8) + nt * 8 + (lane >> 2)]);
+          dmma_8x8x4(c[nt], a, nt * 8 + (lane >> 2) < NN ? sTST[K * V::TS + nt * 8 + (lane >> 2)] : 0.0);
       }
 #pragma unroll
       for (int nt = 0; nt < NTI; ++nt) {
