@@ -535,7 +535,8 @@ def run_b200(args, rank, local_rank, world):
                     "dt": args.implicit_dt, "tableau": "DIRK(3,3)",
                     "halvings": integ.halvings,
                     "krylov": ("host loop" if os.environ.get("MHDG_KRYLOV") == "host" else
-                               "device graph (solver.KrylovEngine)")}
+                               "device graph (solver.KrylovEngine)"),
+                    "inner_residual": os.environ.get("MHDG_INNER_RESIDUAL", "arnoldi")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -731,7 +732,8 @@ def run_b200_partitioned(args, rank, local_rank, world):
                     "jacobian_builds": sum(r["jacobian_builds"] for r in rec),
                     "dt": args.implicit_dt, "tableau": "DIRK(3,3)",
                     "halvings": integ.halvings,
-                    "krylov": f"host loop (distributed dots, {args.orth})"}
+                    "krylov": f"host loop (distributed dots, {args.orth})",
+                    "inner_residual": os.environ.get("MHDG_INNER_RESIDUAL", "arnoldi")}
     peaks = load_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     nqf = t.fphi.shape[0]

@@ -262,6 +262,14 @@ typedef struct {
    * true residual (equal in exact arithmetic); breakdown exits still form
    * the true residual.  The outer level always forms it. */
   int inner_true_residual;
+  /* 1 (needs inner_true_residual = 0): the outer column's w = A z for the z an
+   * inner sweep returned comes from that sweep's Arnoldi relation,
+   * A z = V_{k+1} (H y) with H the sweep's Hessenberg matrix before the
+   * rotations (k + 1 vector updates instead of a matvec; the relation holds
+   * to working precision whatever the orthogonality of V).  0: w = A z by the
+   * operator, as solver.py:86-88 does literally.  Sweeps that took the
+   * true-residual path or never updated x always use the operator. */
+  int outer_matvec_reuse;
 } mhdg_krylov_params;
 
 typedef struct {

@@ -59,7 +59,7 @@ class Tables(C.Structure):
 class KrylovParams(C.Structure):
     _fields_ = [("rel_tol", C.c_double), ("restart", C.c_int), ("max_outer", C.c_int),
                 ("inner_rtol", C.c_double), ("inner_iters", C.c_int), ("inner_precond", C.c_int),
-                ("inner_true_residual", C.c_int)]
+                ("inner_true_residual", C.c_int), ("outer_matvec_reuse", C.c_int)]
 
 
 class KrylovStats(C.Structure):

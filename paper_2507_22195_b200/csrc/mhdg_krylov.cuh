@@ -39,11 +39,14 @@ struct LevelState {
   int total, max_iters, restart, m, j, k, go, cyc, converged, updated;
   int inner_sum;  // outer level: inner iterations accumulated over the solve
   int gtest;      // the last column ended the cycle on the Arnoldi residual test
+  int ncyc;       // restart cycles finished in this solve
+  int ax_ok;      // L.t holds H y of the (single) cycle: A x = V_{k+1} t
 };
 
 struct Level {  // device pointers of one level (passed by value to kernels)
   LevelState* st;
   double *H, *cs, *sn, *g, *y;   // H column-major, column j at H + j * (R + 1)
+  double *Hraw, *t;              // H before the rotations; t = Hraw[:k+1,:k] y
   double *V, *Z, *vin, *zout, *w, *x, *r, *tmp;
   const double* b;
   int R;
@@ -97,6 +100,8 @@ __global__ void k_kr_reset(Level L, int outer) {
   s->k = 0;
   s->j = 0;
   s->gtest = 0;
+  s->ncyc = 0;
+  s->ax_ok = 0;
   if (outer) s->inner_sum = 0;
 }
 
@@ -140,6 +145,7 @@ __global__ void k_kr_givens(Level L, cudaGraphConditionalHandle h_cyc) {
   const int j = s->j, ld = L.R + 1;
   double* h = L.H + (int64_t)j * ld;
   const double hnorm = h[j + 1];
+  for (int i = 0; i <= j + 1; ++i) L.Hraw[(int64_t)j * ld + i] = h[i];
   for (int i = 0; i < j; ++i) {
     const double t = add(mul(L.cs[i], h[i]), mul(L.sn[i], h[i + 1]));
     h[i + 1] = add(mul(-L.sn[i], h[i]), mul(L.cs[i], h[i + 1]));
@@ -194,6 +200,18 @@ __global__ void k_kr_trisolve(Level L) {
 __global__ void k_kr_cycle_end(Level L, cudaGraphConditionalHandle h_true, cudaGraphConditionalHandle h_go) {
   LevelState* s = L.st;
   const bool skip = s->k > 0 && (s->gtest || s->total >= s->max_iters);
+  // A x of this sweep from its Arnoldi relation A Z = V H (x = Z y, one
+  // cycle from x = 0): t = H y over the k + 1 basis vectors
+  if (skip && s->ncyc == 0) {
+    const int k = s->k, ld = L.R + 1;
+    for (int i = 0; i <= k; ++i) {
+      double a = 0.0;
+      for (int c = (i > 0 ? i - 1 : 0); c < k; ++c) a += L.Hraw[(int64_t)c * ld + i] * L.y[c];
+      L.t[i] = a;
+    }
+    s->ax_ok = 1;
+  }
+  s->ncyc += 1;
   if (skip) {
     const double rel = fabs(L.g[s->k]) / s->norm_b;
     s->rel = rel;
@@ -207,9 +225,25 @@ __global__ void k_kr_cycle_end(Level L, cudaGraphConditionalHandle h_true, cudaG
 
 // inner sweep finished: count its iterations into the outer level and arm
 // the IF node "inner never updated x -> face solve" (solver.py:150-154)
-__global__ void k_kr_inner_done(Level inner, Level outer, cudaGraphConditionalHandle h_noupd) {
+__global__ void k_kr_inner_done(Level inner, Level outer, cudaGraphConditionalHandle h_noupd,
+                                cudaGraphConditionalHandle h_ax, cudaGraphConditionalHandle h_mv, int reuse) {
   outer.st->inner_sum += inner.st->total;
   cudaGraphSetConditional(h_noupd, inner.st->updated ? 0u : 1u);
+  // w = A z from the sweep's Arnoldi relation, or by the operator
+  const unsigned ax = (reuse && inner.st->updated && inner.st->ax_ok) ? 1u : 0u;
+  cudaGraphSetConditional(h_ax, ax);
+  cudaGraphSetConditional(h_mv, 1u - ax);
+}
+
+// w = V_{k+1} t (A x of the inner sweep, k and t read on the device)
+__global__ void k_kr_lincomb(int64_t n, const double* __restrict__ V, const double* __restrict__ t,
+                             const LevelState* __restrict__ s, double* __restrict__ w) {
+  const int k = s->k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r <= k; ++r) acc += V[(int64_t)r * n + i] * t[r];
+    w[i] = acc;
+  }
 }
 
 // ---- vector kernels --------------------------------------------------------
@@ -518,6 +552,8 @@ static cudaGraphNode_t kr_column(mhdg_kr::Builder& B, cudaGraph_t g, int lv, cud
   const Level L = K->L[lv];
   const int64_t n = K->n;
   const int gr = kr_grid(K, n);
+  cudaGraphConditionalHandle h_ax = 0, h_mv = 0;
+  bool split_w = false;
   // vin = V_j
   cudaGraphNode_t dep = B.seg(g, nullptr, [&](cudaStream_t s) -> int {
     k_kr_row_copy<<<gr, 256, 0, s>>>(n, L.V, &L.st->j, 0, L.vin);
@@ -529,8 +565,11 @@ static cudaGraphNode_t kr_column(mhdg_kr::Builder& B, cudaGraph_t g, int lv, cud
     const Level I = K->L[1];
     dep = kr_level(B, g, dep, 1);  // inner program: b = outer vin
     cudaGraphConditionalHandle h_noupd = B.handle(g);
+    h_ax = B.handle(g);
+    h_mv = B.handle(g);
+    split_w = true;
     dep = B.seg(g, dep, [&](cudaStream_t s) -> int {
-      k_kr_inner_done<<<1, 1, 0, s>>>(I, L, h_noupd);
+      k_kr_inner_done<<<1, 1, 0, s>>>(I, L, h_noupd, h_ax, h_mv, K->prm.outer_matvec_reuse);
       CK(cudaGetLastError());
       return 0;
     });
@@ -550,10 +589,30 @@ static cudaGraphNode_t kr_column(mhdg_kr::Builder& B, cudaGraph_t g, int lv, cud
       return mhdg_precond(c, &K->lin, L.vin, L.zout, (void*)s);
     });
   }
-  // w = A zout; Z_j = zout; MGS; Givens (sets cyc)
+  // w = A zout: from the inner sweep's Arnoldi relation when it has one
+  // (IF h_ax), by the operator otherwise (IF h_mv)
+  if (split_w) {
+    const Level I = K->L[1];
+    cudaGraph_t body_ax = nullptr, body_mv = nullptr;
+    dep = B.cond(g, dep, h_ax, cudaGraphCondTypeIf, &body_ax);
+    if (B.err) return nullptr;
+    B.seg(body_ax, nullptr, [&](cudaStream_t s) -> int {
+      k_kr_lincomb<<<gr, 256, 0, s>>>(n, I.V, I.t, I.st, L.w);
+      CK(cudaGetLastError());
+      return 0;
+    });
+    dep = B.cond(g, dep, h_mv, cudaGraphCondTypeIf, &body_mv);
+    if (B.err) return nullptr;
+    B.seg(body_mv, nullptr, [&](cudaStream_t s) -> int {
+      return mhdg_matvec(c, &K->lin, L.zout, L.w, (void*)s);
+    });
+  }
+  // Z_j = zout; MGS; Givens (sets cyc)
   return B.seg(g, dep, [&](cudaStream_t s) -> int {
-    int rc = mhdg_matvec(c, &K->lin, L.zout, L.w, (void*)s);
-    if (rc) return rc;
+    if (!split_w) {
+      const int rc = mhdg_matvec(c, &K->lin, L.zout, L.w, (void*)s);
+      if (rc) return rc;
+    }
     k_kr_row_copy<<<gr, 256, 0, s>>>(n, L.Z, &L.st->j, 1, L.zout);
     CK(cudaGetLastError());
     CK(kr_coop(k_kr_mgs, K->coop_grid, s, n, L.V, L.w, L.st, L.H, L.R + 1, K->part));
@@ -588,7 +647,7 @@ extern "C" int64_t mhdg_krylov_workspace(const mhdg_ctx* c, const mhdg_krylov_pa
   const int64_t n = (int64_t)c->F * c->nfn * 5;
   auto level = [&](int R) {
     return (int64_t)(R + 1) * n + (int64_t)R * n + 6 * n  // V, Z, vin zout w x r tmp
-           + (int64_t)(R + 1) * R + 4 * (int64_t)R + 2 + 16;   // H, cs sn g y, state
+           + 2 * (int64_t)(R + 1) * R + 5 * (int64_t)R + 3 + 16;   // H, Hraw, cs sn g y t, state
   };
   return level(prm->restart) + (prm->inner_precond ? level(prm->inner_iters) : 0) + n + 4 +
          2 * (int64_t)c->n_sms * 32;
@@ -598,7 +657,7 @@ extern "C" mhdg_krylov* mhdg_krylov_create(mhdg_ctx* c, const mhdg_krylov_params
                                            int64_t workspace_len, int* err) {
   *err = MHDG_OK;
   if (prm->restart < 1 || prm->max_outer < 0 || prm->inner_iters < 1 || !(prm->rel_tol > 0) ||
-      !(prm->inner_rtol > 0)) {
+      !(prm->inner_rtol > 0) || (prm->outer_matvec_reuse && prm->inner_true_residual)) {
     *err = MHDG_INVALID_CONFIG;
     return nullptr;
   }
@@ -634,6 +693,8 @@ extern "C" mhdg_krylov* mhdg_krylov_create(mhdg_ctx* c, const mhdg_krylov_params
     L.sn = take(R);
     L.g = take(R + 2);
     L.y = take(R);
+    L.Hraw = take((int64_t)(R + 1) * R);
+    L.t = take(R + 1);
     L.V = take((int64_t)(R + 1) * n);
     L.Z = take((int64_t)R * n);
     L.vin = take(n);

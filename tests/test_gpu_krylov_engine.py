@@ -62,9 +62,12 @@ def test_engine_matches_host_loop(cuda_ok, kw):
 
 @pytest.mark.parametrize("kw", [dict(), dict(restart=5, max_outer=12, inner_iters=4, rel_tol=1e-8)])
 def test_inner_residual_modes_agree(cuda_ok, kw):
-    """inner_residual="arnoldi" (default: no true-residual matvec at the end of
-    an inner sweep that ended on the cap or the Arnoldi test) against "true"
-    (solver.py:62-72 literally): same iterates, engine and host loop."""
+    """The Arnoldi shortcuts against the literal loop (solver.py:62-72, 86-88).
+    inner_residual="arnoldi" alone (no true-residual matvec at the end of an
+    inner sweep that ended on the cap or the Arnoldi test) gives the same
+    iterates bit for bit; with outer_matvec="arnoldi" (default: w = A z from
+    the sweep's Arnoldi relation) the counts are the same and x agrees to
+    round-off.  Engine and host loop."""
     import torch
 
     from paper_2507_22195_b200 import solver
@@ -72,13 +75,23 @@ def test_inner_residual_modes_agree(cuda_ok, kw):
     case, disc = _disc()
     lin, res = _system(disc, case, dt=0.25)
     x_t, s_t = solver.solve_condensed(lin, res, inner_residual="true", **kw)
-    x_a, s_a = solver.solve_condensed(lin, res, inner_residual="arnoldi", **kw)
-    assert (s_a.outer_iterations, s_a.inner_iterations, s_a.converged) == \
-        (s_t.outer_iterations, s_t.inner_iterations, s_t.converged)
+    x_a, s_a = solver.solve_condensed(lin, res, inner_residual="arnoldi", outer_matvec="true", **kw)
+    x_f, s_f = solver.solve_condensed(lin, res, **kw)
+    counts = (s_t.outer_iterations, s_t.inner_iterations, s_t.converged)
+    assert (s_a.outer_iterations, s_a.inner_iterations, s_a.converged) == counts
+    assert (s_f.outer_iterations, s_f.inner_iterations, s_f.converged) == counts
     assert torch.equal(x_a, x_t)
+    assert _rel(x_f, x_t) <= 1e-11
+    # the true residual of x moves with x's round-off: |d rel| ~ |dx| / |x| against rel itself
+    assert abs(s_f.rel_residual - s_t.rel_residual) <= 1e-2 * s_t.rel_residual + 1e-11
     x_h, s_h = solver.solve_condensed_host(lin, res, inner_residual="true", **kw)
-    assert (s_h.outer_iterations, s_h.inner_iterations) == (s_t.outer_iterations, s_t.inner_iterations)
+    assert (s_h.outer_iterations, s_h.inner_iterations) == counts[:2]
     assert _rel(x_t, x_h) <= 1e-11
+    x_g, s_g = solver.solve_condensed_host(lin, res, **kw)
+    assert (s_g.outer_iterations, s_g.inner_iterations) == counts[:2]
+    assert _rel(x_g, x_t) <= 1e-11
+    with pytest.raises(Exception):
+        solver.solve_condensed(lin, res, inner_residual="true", outer_matvec="arnoldi", **kw)
 
 
 def test_engine_matches_oracle_solve(cuda_ok):

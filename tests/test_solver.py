@@ -123,3 +123,18 @@ def test_arnoldi_exit_of_the_inner_sweep(tol, cap):
     assert np.abs(fast.x.numpy() - x_ref).max() <= 1e-12 * np.abs(x_ref).max()
     assert counts["arnoldi"] == counts["true"] - 1
     assert abs(fast.rel_residual - lit.rel_residual) <= 1e-10 * lit.rel_residual
+
+
+def test_arnoldi_relation_gives_the_matvec_of_the_result():
+    """final_residual="arnoldi": result.ax = A x from A Z = V H (what the outer
+    column of solve_condensed uses instead of a matvec of the inner result)."""
+    A, b = _random_system(70, 33)
+    At = torch.from_numpy(A)
+    pre = torch.from_numpy(np.diag(1.0 / np.diag(A)))
+    for tol, cap in ((0.1, 20), (1e-6, 5)):
+        res = solver.fgmres(lambda v: At @ v, torch.from_numpy(b), precond=lambda v: pre @ v,
+                            vec=CPUVectors(), rel_tol=tol, restart=cap, max_iters=cap,
+                            raise_on_stagnation=False, final_residual="arnoldi")
+        assert res.ax is not None
+        ax = (At @ res.x).numpy()
+        assert np.abs(res.ax.numpy() - ax).max() <= 1e-13 * np.abs(ax).max()
