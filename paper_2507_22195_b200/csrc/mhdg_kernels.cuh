@@ -204,13 +204,16 @@ struct ResCfg {
   using D = Dims<P>;
   // macros per group iteration: enough quadrature points for the group's
   // threads at low degree (P = 1: 8 volume + 16 face points per macro)
-  static constexpr int EB = (P >= 4) ? 1 : (P == 1 ? 8 : (P == 2 ? 3 : 2));
+  // (P = 4: two macros per 8-warp group: one macro's 100 face / 125 volume
+  // points left half of the group's 256 threads waiting at the phase barrier,
+  // 26% of the stall samples)
+  static constexpr int EB = (P >= 4) ? 2 : (P == 1 ? 8 : (P == 2 ? 3 : 2));
   static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per group
   static constexpr int GT = NW * 32;               // threads per group
-  static constexpr int NG = (P >= 4) ? 1 : 4;      // groups per CTA
+  static constexpr int NG = (P >= 4) ? 2 : 4;      // groups per CTA
   static constexpr bool SB = P <= 3;               // basis tables in shared memory
   static constexpr int NT = NG * GT;
-  static constexpr int MINB = (P >= 4) ? 2 : 1;    // resident CTAs per SM (register cap)
+  static constexpr int MINB = 1;                   // resident CTAs per SM (register cap: 128 x 512 threads)
   // warps per macro in the contraction.  P = 2 has EB = 3 macros for 4 warps:
   // one job per macro left a warp idle (barrier stalls 19% of the samples), so
   // each macro is split four ways (K quarters of the volume test, one face each)
