@@ -207,7 +207,10 @@ struct ResCfg {
   // (P = 4: two macros per 8-warp group: one macro's 100 face / 125 volume
   // points left half of the group's 256 threads waiting at the phase barrier,
   // 26% of the stall samples)
-  static constexpr int EB = (P >= 4) ? 2 : (P == 1 ? 8 : (P == 2 ? 3 : 2));
+#ifndef MHDG_RES_EB1
+#define MHDG_RES_EB1 16   // k = 1 macros per group iteration (A/B builds: 8)
+#endif
+  static constexpr int EB = (P >= 4) ? 2 : (P == 1 ? MHDG_RES_EB1 : (P == 2 ? 3 : 2));
   static constexpr int NW = (P >= 4) ? 8 : 4;      // warps per group
   static constexpr int GT = NW * 32;               // threads per group
   static constexpr int NG = (P >= 4) ? 2 : 4;      // groups per CTA
@@ -238,7 +241,7 @@ struct ResCfg {
   // w / trace / geometry of a batch arrive by cp.async in a staging region of
   // their own (STG_ per macro), read in place by phase 1; the face / volume
   // partial rows (phases 2-3) have theirs
-  static constexpr int AREG = FR_ + VOL_;
+  static constexpr int AREG = POINTWISE_TEST ? 0 : FR_ + VOL_;   // partial rows of the DMMA tests
   static constexpr int STG_ = W_ + TR_ + GEO_;
   static constexpr int per_macro_base = AREG + G_ + H_ + STG_;
   static constexpr int tables = 4 * D::NQF * D::FS + D::NQF * D::FS + D::NQ + D::NQF + AF_ +
