@@ -1824,8 +1824,11 @@ struct Face2 {
   static constexpr size_t bytes = (size_t)doubles * 8 + ints * 4;
 };
 
+#ifndef MHDG_FACE_MINB_LOW
+#define MHDG_FACE_MINB_LOW 4   // resident CTAs per SM of the k <= 2 face-in kernel (measured 3 / 4 / 5: k = 1 matvec 0.655 / 0.640 / 0.678 ms, k = 2 1.645 / 1.622 / 1.621)
+#endif
 template <int P, int MODE>   // MODE 0: g = -A_vh x (+ -r_w); 1: y += A_hh x + A_hv z
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, (P <= 2 && MODE == 0) ? MHDG_FACE_MINB_LOW : 3)
 k_face2(Geo g, int mode, const double* __restrict__ tenA, const double* __restrict__ tenB,
         const double* __restrict__ x, const double* __restrict__ zin, const double* __restrict__ r_w,
         double* __restrict__ out) {
