@@ -2,6 +2,7 @@
 import argparse
 import json
 import math
+import os
 import sys
 import time
 
@@ -53,4 +54,9 @@ tot = {k: sum(r[k] for r in integ.records) for k in keys}
 print(json.dumps({"case": a.case, "viscous": a.viscous, "n": a.n, "p": a.p, "macros": mesh.n_macros,
                   "setup_s": setup, "gpu_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
                   "steps": a.steps, "wall_s": wall, "s_per_step": wall / a.steps, "totals": tot,
+                  "state": {"w_l2": float(torch.linalg.vector_norm(fields.w)),
+                            "trace_l2": float(torch.linalg.vector_norm(fields.trace)),
+                            "w_sum": float(fields.w.sum()), "t": float(t)},
+                  "krylov_modes": {k: os.environ.get(k, "default") for k in
+                                   ("MHDG_INNER_RESIDUAL", "MHDG_OUTER_MATVEC", "MHDG_KRYLOV")},
                   "records": integ.records}))
