@@ -25,6 +25,9 @@ ap.add_argument("--n", type=int, default=32)
 ap.add_argument("--flux", default="kepes")
 ap.add_argument("--dt", type=float, default=0.01425)
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--pair", default="modes", choices=["modes", "literal-host-vs-graph"],
+                help="modes: literal loop vs Arnoldi shortcuts; literal-host-vs-graph: the literal loop run by the\n"
+                     "host-driven control against the device graph (they differ by round-off only: a yardstick)")
 a = ap.parse_args()
 gas = GasModel(1.4)
 if a.case == "vortex":
@@ -35,8 +38,11 @@ else:
     box = case.box
 disc = Discretization(build_box_macro_mesh(box, a.n, 1), p=3, gas=gas, flux=DissipationSpec(a.flux), device="cuda:0")
 out = {}
-for mode in ("true", "arnoldi"):
+runs = (("true", "graph"), ("arnoldi", "graph")) if a.pair == "modes" else (("true", "host"), ("true", "graph"))
+for idx, (mode, ctl) in enumerate(runs):
     os.environ["MHDG_INNER_RESIDUAL"] = mode
+    os.environ["MHDG_KRYLOV"] = ctl
+    mode = ("true", "arnoldi")[idx]   # slot names of the comparison below
     integ = DIRKIntegrator(disc)
     fields, t = integ.run(disc.project(case.initial), t_final=a.steps * a.dt, dt=a.dt)
     torch.cuda.synchronize()
@@ -44,6 +50,6 @@ for mode in ("true", "arnoldi"):
                  [(r["newton_iters"], r["fgmres_iters"], r["inner_iters_total"]) for r in integ.records])
 (wt, tt, ct), (wa, ta, ca) = out["true"], out["arnoldi"]
 rel = lambda x, y: float(torch.linalg.vector_norm(x - y) / torch.linalg.vector_norm(y))   # noqa: E731
-print(json.dumps({"case": a.case, "n": a.n, "steps": a.steps, "counts_identical": ct == ca, "counts": ct,
+print(json.dumps({"pair": a.pair, "case": a.case, "n": a.n, "steps": a.steps, "counts_identical": ct == ca, "counts": ct,
                   "rel_diff_w": rel(wa, wt), "rel_diff_trace": rel(ta, tt),
                   "max_abs_diff_w": float((wa - wt).abs().max())}))
