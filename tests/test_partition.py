@@ -151,6 +151,25 @@ def _worker(rank, world, port, flux, results):
         xd2 = res2.x.view(shape).numpy()[: part.n_owned]
         err_cgs2 = (abs(res2.iterations - it_ref),
                     float(np.abs(xd2 - xr.reshape(tr.shape)[own]).max() / np.abs(xr).max()))
+        # the inner sweep's Arnoldi exit on the distributed vectors: same
+        # iterate as the literal loop with one matvec less, and A x from the
+        # Arnoldi relation (what the outer column uses instead of a matvec)
+        calls = [0]
+
+        def dop_counted(v):
+            calls[0] += 1
+            return dop(v)
+
+        lit = solver.fgmres(dop_counted, b, rel_tol=0.1, restart=20, max_iters=20,
+                            raise_on_stagnation=False, vec=vec)
+        n_lit, calls[0] = calls[0], 0
+        fast = solver.fgmres(dop_counted, b, rel_tol=0.1, restart=20, max_iters=20,
+                             raise_on_stagnation=False, vec=vec, final_residual="arnoldi")
+        ax_true = dop(fast.x).view(shape).numpy()[: part.n_owned]
+        ax_arn = fast.ax.view(shape).numpy()[: part.n_owned]
+        scale = float(vec.norm(b))   # global norm: the same normalisation on every rank
+        arnoldi = (fast.iterations == lit.iterations, bool(torch.equal(fast.x, lit.x)), n_lit - calls[0],
+                   float(np.abs(ax_arn - ax_true).max()) / scale)
         # remote face sides for the face-block preconditioner: every rank
         # takes part, including one that owns no halo face
         nqf = t.fphi.shape[0]
@@ -159,7 +178,7 @@ def _worker(rank, world, port, flux, results):
         got = ex.gather_sides(hh_loc, nqf).numpy()
         ok_sides = np.array_equal(got, hh_glob[part.remote_side_ids])
         results[rank] = (ok_res and ok_sides, ok_fill, err_mv, res.iterations, it_ref, err_x,
-                         part.n_remote_sides, err_cgs2)
+                         part.n_remote_sides, err_cgs2, arnoldi)
     finally:
         dist.destroy_process_group()
 
@@ -174,8 +193,9 @@ def test_gloo_world2_partitioned_operator_and_fgmres(flux):
                        join=True, start_method="spawn")
     assert min(results[r][6] for r in range(world)) == 0, "one rank should own no halo face"
     for rank in range(world):
-        ok_res, ok_fill, err_mv, it, it_ref, err_x, _, err_cgs2 = results[rank]
+        ok_res, ok_fill, err_mv, it, it_ref, err_x, _, err_cgs2, arnoldi = results[rank]
         assert err_cgs2[0] <= 1 and err_cgs2[1] <= 1e-7, err_cgs2
+        assert arnoldi[0] and arnoldi[1] and arnoldi[2] == 1 and arnoldi[3] <= 1e-12, arnoldi
         assert ok_res, "partitioned residual must be bit-identical"
         assert ok_fill
         assert err_mv <= 1e-14
