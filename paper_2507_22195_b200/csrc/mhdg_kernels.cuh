@@ -1345,7 +1345,6 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
 #endif
   for (int e = blockIdx.x; e < g.E; e += gridDim.x) {
     double* const S = L::GS ? sinv + (size_t)e * NM * NM : sS;
-    if (!L::GS && tid == 0) bulk_wait_read();   // previous macro's S left shared memory
     __syncthreads();
     const int en = e + gridDim.x;
     for (int i = tid; i < NN * 5; i += NT) sW[i] = w[(size_t)e * NN * 5 + i];
@@ -1434,6 +1433,11 @@ k_linearize2(Geo g, ViscGeo vg, const double* __restrict__ w, const double* __re
           }
         }
       }
+      // the previous macro's S must have left shared memory before the
+      // scatter below overwrites it: waited for here, a load phase, the volume
+      // duals and the DMMA chunks after its bulk store was issued (at the loop
+      // top the wait exposed the store's drain), and published by the barrier
+      if (!L::GS && ch == L::NCH - 1 && tid == 0) bulk_wait_read();
       __syncthreads();
     }
     // scatter the accumulators into S[(i,s)][(j,t)]
